@@ -1,0 +1,102 @@
+"""Host-side logic (CPU only): ingestion, stage classes, flop counters, validation."""
+
+import numpy as np
+import pytest
+
+import cases
+from conftest import load_golden
+from paper_2304_04980_b200 import generators as G
+from paper_2304_04980_b200.counts import counters
+from paper_2304_04980_b200.errors import DimensionMismatchError
+from paper_2304_04980_b200.problem import (ConstSeq, GridLayout, arrays_from_problem,
+                                           arrays_to_problem, validate_arrays)
+
+
+def test_counters_match_reference(golden):
+    name, ga, rec = golden
+    c = counters(ga, rec["L"], rec["S"])
+    for key in ("matvec_flops", "outer_coupling_flops", "inner_coupling_flops",
+                "pair_solve_flops", "apply_flops"):
+        assert c[key] == int(rec[key]), (name, key, c[key], int(rec[key]))
+
+
+def test_roundtrip_problem_arrays():
+    ga = G.config1(3)
+    back = arrays_from_problem(arrays_to_problem(ga))
+    for f in ("A", "B", "R", "C", "Q", "offset", "cmask", "dyn_class", "cost_class"):
+        assert np.array_equal(getattr(back, f), getattr(ga, f)), f
+
+
+def test_stage_classes_time_invariant():
+    ga = G.config2(0)
+    pc, pkeys = ga.psi_classes()
+    xc, xkeys = ga.xi_classes()
+    assert len(pkeys) == 2 and pc[0] == 0 and np.all(pc[1:] == 1)
+    assert len(xkeys) == 1 and np.all(xc == 0)
+
+
+def test_stage_classes_time_varying():
+    ga = arrays_from_problem(cases.time_varying(T=5))
+    pc, pkeys = ga.psi_classes()
+    assert len(pkeys) == 6          # every stage distinct (terminal weight too)
+    assert len(ga.xi_classes()[1]) == 5
+
+
+def test_terminal_weight_class():
+    p = arrays_to_problem(G.config1(0))
+    T = p.T
+    for row in p.subsystems:
+        for s in row:
+            q = list(s.Q)
+            q[-1] = 2.0 * q[-1]
+            s.Q = q
+    ga = arrays_from_problem(p)
+    assert list(ga.cost_class[:-1]) == [0] * T and ga.cost_class[-1] == 1
+    pc, pkeys = ga.psi_classes()
+    assert len(pkeys) == 3 and pc[-1] == 2
+
+
+def test_heterogeneous_dimensions_rejected():
+    p = cases.uncoupled(K=1, N=2, T=1)
+    s = p.subsystems[0][1]
+    s.n = 3
+    s.A = [np.zeros((3, 3))]
+    s.B = [np.zeros((3, 1))]
+    s.Q = [np.eye(3)] * 2
+    p.boundary.init[0][1] = np.ones(3)
+    with pytest.raises(DimensionMismatchError):
+        arrays_from_problem(p)
+
+
+def test_invalid_problem_raises_value_error():
+    p = arrays_to_problem(G.config1(0))
+    s = p.subsystems[1][1]
+    s.Q = ConstSeq(-np.eye(2), p.T + 1)
+    with pytest.raises(ValueError, match="invalid problem"):
+        arrays_from_problem(p)
+    ga = G.config1(0)
+    ga.R[0, 0, 0] = np.array([[0.0]])
+    assert validate_arrays(ga)
+
+
+def test_layout_matches_reference_order():
+    lay = GridLayout(K=3, N=4, T=2, n=2)
+    assert lay.x_offset(1, 2, 1) == 1 * 24 + (2 * 3 + 1) * 2
+    assert lay.pairs == [(0, 1), (2, 3)]
+    assert GridLayout(3, 5, 1, 1).pairs[-1] == (4,)
+
+
+def test_boundary_offset_matches_reference():
+    ga, rec = load_golden("boundary")
+    assert np.array_equal(ga.offset, rec["ref_offset"])
+    assert np.any(ga.offset[ga.K * ga.N * ga.n:] != 0)
+
+
+def test_generators_are_seeded():
+    a, b = G.config3(5, K=4, N=4, T=3), G.config3(5, K=4, N=4, T=3)
+    assert np.array_equal(a.A, b.A) and np.array_equal(a.offset, b.offset)
+    c = G.config3(6, K=4, N=4, T=3)
+    assert not np.array_equal(a.A, c.A)
+    m = G.config4(0, K=8, N=8, T=4)
+    # spectral radius check of the MSD dynamics: stable-ish Euler discretisation
+    assert m.n == 2 and m.m == 1 and np.all(np.isfinite(m.A))
