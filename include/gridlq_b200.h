@@ -1,0 +1,110 @@
+/*
+ * gridlq_b200 -- C ABI of the B200-native PCGM hot path (arXiv 2304.04980).
+ *
+ * Drop-in boundary for the reference package `gridlq` (Python, /root/reference/pkg/src).
+ * The reference has no FFI of its own: its hot path is the duck-typed operator /
+ * preconditioner protocol consumed by `pcg_solve`.  Each entry point below replaces one
+ * member of that protocol (reference file:line in brackets):
+ *
+ *   gq_create            build_stacked + build_schur + NestedJacobiPreconditioner.__init__
+ *                        (factor_all)          [kkt_assembly.py:204,487,695; nested_jacobi.py:31-43]
+ *   gq_apply_delta       SchurOperator.apply / apply_delta        [kkt_assembly.py:389-403,547]
+ *   gq_apply_outer_coupling  SchurOperator.apply_outer_coupling   [kkt_assembly.py:414-425]
+ *   gq_apply_inner_coupling  PairSplitting.apply_inner_coupling   [kkt_assembly.py:645-662]
+ *   gq_pair_solve        NestedJacobiPreconditioner._pair_solves  [nested_jacobi.py:65-77]
+ *   gq_apply_precond     NestedJacobiPreconditioner.apply         [nested_jacobi.py:105-122]
+ *   gq_pcg_start / gq_pcg_run / gq_pcg_read / gq_pcg_history / gq_pcg
+ *                        pcg_solve / cg_solve                     [pcg.py:50-156]
+ *
+ * Conventions
+ *   - Vectors are fp64 in the reference's global order (t, j, i, k): element
+ *     t*K*N*n + (j*K + i)*n + k  [grid_problem.py:143-144].  Vector pointers may be host
+ *     (pageable or pinned) or device pointers; the library detects which.
+ *   - Problem arrays in gq_problem_desc are HOST pointers, copied at gq_create.
+ *   - All functions return a gq_status; gq_last_error() gives the message of the most
+ *     recent failure on the calling thread.
+ *   - A context is not thread-safe; one solve at a time per context.
+ */
+#ifndef GRIDLQ_B200_H
+#define GRIDLQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gq_status {
+  GQ_OK = 0,
+  GQ_MAX_ITER = 1,        /* MaxIterationsExceeded        [pcg.py:141-148]  */
+  GQ_BREAKDOWN = 2,       /* BreakdownError               [pcg.py:103-107]  */
+  GQ_DIM_MISMATCH = 3,    /* DimensionMismatchError       [pcg.py:63-64]    */
+  GQ_INVALID_ARG = 4,     /* ValueError (odd L, tol<=0, non-finite rhs, ...) */
+  GQ_NOT_SPD = 5,         /* NotPositiveDefiniteError     [block_linalg.py:54-60] */
+  GQ_CUDA_ERROR = 6,
+  GQ_UNSUPPORTED = 7      /* e.g. state dimension without a compiled kernel */
+} gq_status;
+
+enum { GQ_VEC_X = 0, GQ_VEC_R = 1 };
+
+/* Dense, stage-class-deduplicated problem description (see GridArrays in problem.py).
+ * Node axes are [N][K] (column j, then row i).  Stage t < T uses dynamics set
+ * dyn_class[t]; stage t <= T uses state-cost set cost_class[t]. */
+typedef struct gq_problem_desc {
+  int32_t K, N, T, n, m;
+  int32_t n_dyn, n_cost;
+  const int32_t* dyn_class;   /* [T]   */
+  const int32_t* cost_class;  /* [T+1] */
+  const double* A;            /* [n_dyn][N][K][n][n] */
+  const double* B;            /* [n_dyn][N][K][n][m] */
+  const double* R;            /* [n_dyn][N][K][m][m] */
+  const double* C;            /* [n_dyn][4][N][K][n][n]  west, east, north, south */
+  const double* Q;            /* [n_cost][N][K][n][n] */
+} gq_problem_desc;
+
+typedef struct gq_ctx gq_ctx;
+
+const char* gq_last_error(void);
+const char* gq_version(void);
+
+int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps, int32_t outer_sweeps,
+              gq_ctx** out);
+void gq_destroy(gq_ctx* ctx);
+int64_t gq_dim(const gq_ctx* ctx);
+int gq_set_stream(gq_ctx* ctx, void* cuda_stream);
+int gq_synchronize(gq_ctx* ctx);
+/* change the nested-Jacobi budgets L (inner) and S (outer); factors are independent of them */
+int gq_set_sweeps(gq_ctx* ctx, int32_t inner_sweeps, int32_t outer_sweeps);
+
+int gq_apply_delta(gq_ctx* ctx, const double* x, double* y);
+int gq_apply_outer_coupling(gq_ctx* ctx, const double* x, double* y);
+int gq_apply_inner_coupling(gq_ctx* ctx, const double* x, double* y);
+int gq_pair_solve(gq_ctx* ctx, const double* rhs, double* out);
+int gq_apply_precond(gq_ctx* ctx, const double* r, double* q);
+
+/* Stateful PCG: start (r = rhs - Delta x0, d = P r, mu = d.r), then run until convergence
+ * (||r||_inf < tol, absolute), breakdown or max_steps total steps. */
+int gq_pcg_start(gq_ctx* ctx, const double* rhs, const double* x0, int32_t use_precond);
+int gq_pcg_run(gq_ctx* ctx, double tol, int64_t max_steps, int64_t* steps_done,
+               int32_t* converged);
+int gq_pcg_read(gq_ctx* ctx, int32_t which, double* out);
+int gq_pcg_history(gq_ctx* ctx, double* out, int64_t count);
+int gq_pcg_scalars(gq_ctx* ctx, double* mu, double* curvature, double* alpha, double* beta);
+/* one-shot: start + run + read x + history; returns GQ_OK / GQ_MAX_ITER / GQ_BREAKDOWN */
+int gq_pcg(gq_ctx* ctx, const double* rhs, const double* x0, double tol, int64_t max_steps,
+           int32_t use_precond, double* x_out, double* hist_out, int64_t hist_capacity,
+           int64_t* steps, int32_t* converged);
+
+/* Measurement helpers (bench.py): run `steps` PCG steps as individual launches with CUDA
+ * events around every kernel; per-kernel total milliseconds go to ms_out[0..count) in the
+ * order gq_kernel_name(ctx, i) reports.  Returns the number of kernels per step. */
+int gq_profile_steps(gq_ctx* ctx, int32_t steps, float* ms_out, int32_t count);
+const char* gq_kernel_name(gq_ctx* ctx, int32_t i);
+/* kernels launched per PCG step (graph nodes) */
+int gq_launches_per_step(gq_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRIDLQ_B200_H */

@@ -1,0 +1,27 @@
+"""B200-native PCGM hot path for LQ optimal control of K x N grids (arXiv 2304.04980).
+
+Drop-in for the reference package ``gridlq``'s solver path: the problem data model
+(``GridLQProblem``...), ``pcg_solve`` / ``cg_solve`` / ``SolveReport`` and the operator /
+preconditioner duck types, executed by hand-written sm_100a CUDA in libgridlq_b200.so.
+"""
+
+from .errors import (BreakdownError, DimensionGuardError, DimensionMismatchError, GridLQError,
+                     MaxIterationsExceeded, NotPositiveDefiniteError)
+from .problem import (BoundaryData, ConstSeq, GridArrays, GridLayout, GridLQProblem,
+                      SubsystemData, arrays_from_problem, arrays_to_problem, validate_arrays)
+from .solver import (COUNT_KEYS, GpuNestedJacobiPreconditioner, GpuSchurOperator, SolveReport,
+                     apply_delta, build_schur, cg_solve, pcg_solve)
+
+NestedJacobiPreconditioner = GpuNestedJacobiPreconditioner
+SchurOperator = GpuSchurOperator
+
+__all__ = [
+    "BoundaryData", "BreakdownError", "COUNT_KEYS", "ConstSeq", "DimensionGuardError",
+    "DimensionMismatchError", "GpuNestedJacobiPreconditioner", "GpuSchurOperator",
+    "GridArrays", "GridLQError", "GridLQProblem", "GridLayout", "MaxIterationsExceeded",
+    "NestedJacobiPreconditioner", "NotPositiveDefiniteError", "SchurOperator", "SolveReport",
+    "SubsystemData", "apply_delta", "arrays_from_problem", "arrays_to_problem", "build_schur",
+    "cg_solve", "pcg_solve", "validate_arrays",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,631 @@
+// C ABI of libgridlq_b200.so: context lifetime, setup, unit applies and the PCG driver.
+//
+// PCG driver = pcg_solve's loop (gridlq/pcg.py:98-131) as one captured CUDA graph per
+// step.  All scalars (mu, alpha, beta, curvature, residual), the step counter, the
+// residual history and the done/converged/breakdown flags live in device memory, so a
+// step needs no host round trip; the host launches the graph in growing batches and only
+// reads the 64-byte state between batches.  Kernels of a step after convergence,
+// breakdown or the step budget see `done` and exit immediately, which preserves the
+// reference's exact stopping semantics while launching ahead.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <map>
+#include <array>
+#include <algorithm>
+
+#include "gq_internal.h"
+#include "../../include/gridlq_b200.h"
+
+using namespace gq;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(GQ_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct gq_ctx {
+  Geo g{};
+  int m = 0, L = 2, S = 2, n_dyn = 0, n_cost = 0, npc = 0, nxc = 0, sm_count = 148;
+  cudaStream_t stream = nullptr;
+  double *A = nullptr, *B = nullptr, *R = nullptr, *C = nullptr, *Q = nullptr;
+  double *qinv = nullptr, *rinv = nullptr, *brb = nullptr;
+  double *psi = nullptr, *xi = nullptr, *xit = nullptr, *fac = nullptr;
+  int *psi_cls = nullptr, *xi_cls = nullptr, *psi_keys = nullptr, *xi_keys = nullptr;
+  double *x = nullptr, *r = nullptr, *d = nullptr, *y = nullptr, *q = nullptr;
+  double *th[2] = {nullptr, nullptr}, *dl[2] = {nullptr, nullptr};
+  double *tmp0 = nullptr, *tmp1 = nullptr;
+  double* partials = nullptr;
+  PcgState* st = nullptr;
+  PcgState* h_st = nullptr;   // pinned mirror
+  double* hist = nullptr;
+  long long hist_cap = 0;
+  SetupErr* err = nullptr;
+  Ops op{};
+  StencilShape sh_delta{}, sh_outer{}, sh_inner{};
+  SweepShape sw{}, sw_outer{};
+  int vblocks = 0;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  bool started = false;
+  int use_precond = 1;
+  std::vector<std::string> knames;
+};
+
+extern "C" const char* gq_last_error(void) { return g_err.c_str(); }
+extern "C" const char* gq_version(void) { return "gridlq_b200 0.1.0 (sm_100a, fp64)"; }
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+}
+
+static void release(gq_ctx* c) {
+  if (!c) return;
+  for (auto& ge : c->gexec)
+    if (ge) cudaGraphExecDestroy(ge);
+  void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
+                  c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
+                  c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
+                  c->tmp1, c->partials, c->st, c->hist, c->err};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_st) cudaFreeHost(c->h_st);
+  delete c;
+}
+
+extern "C" void gq_destroy(gq_ctx* ctx) { release(ctx); }
+
+extern "C" int64_t gq_dim(const gq_ctx* ctx) { return ctx ? ctx->g.dim : -1; }
+
+extern "C" int gq_set_stream(gq_ctx* ctx, void* stream) {
+  if (!ctx) return fail(GQ_INVALID_ARG, "null context");
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  for (auto& ge : ctx->gexec)
+    if (ge) {
+      cudaGraphExecDestroy(ge);
+      ge = nullptr;
+    }
+  return GQ_OK;
+}
+
+extern "C" int gq_set_sweeps(gq_ctx* ctx, int32_t inner_sweeps, int32_t outer_sweeps) {
+  if (!ctx) return fail(GQ_INVALID_ARG, "null context");
+  if (inner_sweeps < 1 || outer_sweeps < 1)
+    return fail(GQ_INVALID_ARG, "sweep budgets must be at least 1");
+  if (inner_sweeps == ctx->L && outer_sweeps == ctx->S) return GQ_OK;
+  ctx->L = inner_sweeps;
+  ctx->S = outer_sweeps;
+  for (auto& ge : ctx->gexec)
+    if (ge) {
+      cudaGraphExecDestroy(ge);
+      ge = nullptr;
+    }
+  return GQ_OK;
+}
+
+extern "C" int gq_synchronize(gq_ctx* ctx) {
+  if (!ctx) return fail(GQ_INVALID_ARG, "null context");
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GQ_OK;
+}
+
+static int check_setup_err(gq_ctx* c) {
+  SetupErr e;
+  CK(cudaMemcpy(&e, c->err, sizeof(e), cudaMemcpyDeviceToHost));
+  if (e.code == 0) return GQ_OK;
+  char buf[256];
+  if (e.code == 1)
+    snprintf(buf, sizeof(buf),
+             "pivot %.3e at index %d (threshold %.3e) in pair block %d of pair %d, stage class %d",
+             e.pivot, e.j, e.tol, e.k, e.v, e.cls);
+  else
+    snprintf(buf, sizeof(buf), "cost weight %d: pivot %.3e at index %d (threshold %.3e)", e.cls,
+             e.pivot, e.j, e.tol);
+  return fail(GQ_NOT_SPD, buf);
+}
+
+extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
+                         int32_t outer_sweeps, gq_ctx** out) {
+  if (!desc || !out) return fail(GQ_INVALID_ARG, "null argument");
+  *out = nullptr;
+  const gq_problem_desc& D = *desc;
+  if (D.K < 1 || D.N < 1 || D.T < 1)
+    return fail(GQ_INVALID_ARG, "grid dimensions must be positive");
+  if (D.n < 1 || D.m < 1 || D.m > 8) return fail(GQ_INVALID_ARG, "bad state/input dimension");
+  if (!n_supported(D.n))
+    return fail(GQ_UNSUPPORTED, "state dimension n=" + std::to_string(D.n) +
+                                    " has no compiled kernel (supported: 1, 2, 3, 4, 8)");
+  if (inner_sweeps < 1 || outer_sweeps < 1)
+    return fail(GQ_INVALID_ARG, "sweep budgets must be at least 1");
+  if (D.n_dyn < 1 || D.n_cost < 1) return fail(GQ_INVALID_ARG, "need at least one data set");
+  for (int t = 0; t < D.T; ++t)
+    if (D.dyn_class[t] < 0 || D.dyn_class[t] >= D.n_dyn)
+      return fail(GQ_INVALID_ARG, "dyn_class out of range");
+  for (int t = 0; t <= D.T; ++t)
+    if (D.cost_class[t] < 0 || D.cost_class[t] >= D.n_cost)
+      return fail(GQ_INVALID_ARG, "cost_class out of range");
+
+  gq_ctx* c = new gq_ctx();
+  c->m = D.m;
+  c->L = inner_sweeps;
+  c->S = outer_sweeps;
+  c->n_dyn = D.n_dyn;
+  c->n_cost = D.n_cost;
+  Geo& g = c->g;
+  g.K = D.K;
+  g.N = D.N;
+  g.T = D.T;
+  g.T1 = D.T + 1;
+  g.n = D.n;
+  g.V = (D.N + 1) / 2;
+  g.nb = (D.K + 1) / 2;
+  g.nk = (long long)D.K * D.N;
+  g.dim = g.nk * D.n * g.T1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev);
+
+  // stage classes (GridArrays.psi_classes / xi_classes)
+  std::map<std::array<int, 3>, int> pmap;
+  std::vector<int> pcls(g.T1), pkeys;
+  for (int t = 0; t < g.T1; ++t) {
+    std::array<int, 3> key = t == 0 ? std::array<int, 3>{D.cost_class[0], -1, -1}
+                                    : std::array<int, 3>{D.cost_class[t], D.dyn_class[t - 1],
+                                                         D.cost_class[t - 1]};
+    auto it = pmap.find(key);
+    if (it == pmap.end()) {
+      it = pmap.emplace(key, (int)pmap.size()).first;
+      pkeys.insert(pkeys.end(), key.begin(), key.end());
+    }
+    pcls[t] = it->second;
+  }
+  std::map<std::array<int, 2>, int> xmap;
+  std::vector<int> xcls(std::max(g.T, 1)), xkeys;
+  for (int t = 0; t < g.T; ++t) {
+    std::array<int, 2> key{D.dyn_class[t], D.cost_class[t]};
+    auto it = xmap.find(key);
+    if (it == xmap.end()) {
+      it = xmap.emplace(key, (int)xmap.size()).first;
+      xkeys.insert(xkeys.end(), key.begin(), key.end());
+    }
+    xcls[t] = it->second;
+  }
+  c->npc = (int)pmap.size();
+  c->nxc = (int)xmap.size();
+
+  const int n = D.n, m = D.m, q = 4 * n;
+  const size_t nn = (size_t)n * n;
+  const size_t nk = (size_t)g.nk;
+  auto bail = [&](int code) {
+    release(c);
+    return code;
+  };
+#define CKB(call)                                                                          \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return bail(fail(GQ_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_))); \
+  } while (0)
+  CKB(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CKB(dalloc(&c->A, D.n_dyn * nk * nn));
+  CKB(dalloc(&c->B, D.n_dyn * nk * n * m));
+  CKB(dalloc(&c->R, D.n_dyn * nk * m * m));
+  CKB(dalloc(&c->C, D.n_dyn * 4 * nk * nn));
+  CKB(dalloc(&c->Q, D.n_cost * nk * nn));
+  CKB(cudaMemcpy(c->A, D.A, D.n_dyn * nk * nn * 8, cudaMemcpyHostToDevice));
+  CKB(cudaMemcpy(c->B, D.B, D.n_dyn * nk * n * m * 8, cudaMemcpyHostToDevice));
+  CKB(cudaMemcpy(c->R, D.R, D.n_dyn * nk * m * m * 8, cudaMemcpyHostToDevice));
+  CKB(cudaMemcpy(c->C, D.C, D.n_dyn * 4 * nk * nn * 8, cudaMemcpyHostToDevice));
+  CKB(cudaMemcpy(c->Q, D.Q, D.n_cost * nk * nn * 8, cudaMemcpyHostToDevice));
+  CKB(dalloc(&c->psi_cls, g.T1));
+  CKB(dalloc(&c->xi_cls, xcls.size()));
+  CKB(dalloc(&c->psi_keys, pkeys.size()));
+  CKB(dalloc(&c->xi_keys, std::max<size_t>(xkeys.size(), 1)));
+  CKB(cudaMemcpy(c->psi_cls, pcls.data(), pcls.size() * 4, cudaMemcpyHostToDevice));
+  CKB(cudaMemcpy(c->xi_cls, xcls.data(), xcls.size() * 4, cudaMemcpyHostToDevice));
+  CKB(cudaMemcpy(c->psi_keys, pkeys.data(), pkeys.size() * 4, cudaMemcpyHostToDevice));
+  if (!xkeys.empty())
+    CKB(cudaMemcpy(c->xi_keys, xkeys.data(), xkeys.size() * 4, cudaMemcpyHostToDevice));
+  CKB(dalloc(&c->err, 1));
+  CKB(cudaMemset(c->err, 0, sizeof(SetupErr)));
+
+  // cost inverses, B R^-1 B'
+  CKB(dalloc(&c->qinv, D.n_cost * nk * nn));
+  CKB(dalloc(&c->rinv, D.n_dyn * nk * m * m));
+  CKB(dalloc(&c->brb, D.n_dyn * nk * nn));
+  CKB(launch_spd_inverse(c->Q, c->qinv, D.n_cost * (long long)nk, n, c->err, c->stream));
+  CKB(launch_spd_inverse(c->R, c->rinv, D.n_dyn * (long long)nk, m, c->err, c->stream));
+  CKB(cudaStreamSynchronize(c->stream));
+  {
+    int rc = check_setup_err(c);
+    if (rc != GQ_OK) return bail(rc);
+  }
+  CKB(launch_brb(g, m, D.n_dyn, c->B, c->rinv, c->brb, c->stream));
+  // operator blocks per stage class
+  CKB(dalloc(&c->psi, (size_t)c->npc * nk * 13 * nn));
+  CKB(dalloc(&c->xi, (size_t)std::max(c->nxc, 1) * nk * 5 * nn));
+  CKB(dalloc(&c->xit, (size_t)std::max(c->nxc, 1) * nk * 5 * nn));
+  CKB(launch_xi(g, c->nxc, c->xi_keys, c->A, c->C, c->qinv, c->xi, c->xit, c->stream));
+  CKB(launch_psi(g, c->npc, c->psi_keys, c->A, c->C, c->qinv, c->brb, c->psi, c->stream));
+  // pair factors
+  double* scratch = nullptr;
+  CKB(dalloc(&c->fac, (size_t)c->npc * g.V * g.nb * 2 * q * q));
+  CKB(dalloc(&scratch, (size_t)c->npc * g.V * 5 * q * q));
+  cudaError_t fe = launch_factor(g, c->npc, c->psi, c->fac, scratch, c->err, c->stream);
+  cudaError_t se = cudaStreamSynchronize(c->stream);
+  cudaFree(scratch);
+  CKB(fe);
+  CKB(se);
+  {
+    int rc = check_setup_err(c);
+    if (rc != GQ_OK) return bail(rc);
+  }
+  c->op = Ops{c->psi, c->xi, c->xit, c->fac, c->psi_cls, c->xi_cls};
+
+  // work vectors (stage-inner layout) and the reference-layout staging buffers
+  const size_t dim = (size_t)g.dim;
+  double** vecs[] = {&c->x, &c->r, &c->d, &c->y, &c->q, &c->th[0], &c->th[1],
+                     &c->dl[0], &c->dl[1], &c->tmp0, &c->tmp1};
+  for (double** p : vecs) CKB(dalloc(p, dim));
+  c->sh_delta = stencil_shape(g, kDelta, c->sm_count);
+  c->sh_outer = stencil_shape(g, kOuter, c->sm_count);
+  c->sh_inner = stencil_shape(g, kInner, c->sm_count);
+  c->sw = sweep_shape(g, false);
+  c->sw_outer = sweep_shape(g, true);
+  c->vblocks = vec_blocks(c->sm_count);
+  int maxb = std::max({c->sh_delta.blocks, c->sw.blocks, c->sw_outer.blocks, c->vblocks});
+  CKB(dalloc(&c->partials, (size_t)maxb + 32));
+  CKB(dalloc(&c->st, 1));
+  CKB(cudaMemset(c->st, 0, sizeof(PcgState)));
+  CKB(cudaMallocHost(reinterpret_cast<void**>(&c->h_st), sizeof(PcgState)));
+  memset(c->h_st, 0, sizeof(PcgState));
+#undef CKB
+  *out = c;
+  return GQ_OK;
+}
+
+// ---- boundary helpers -----------------------------------------------------------------
+
+// user vector (reference layout, host or device) -> internal vector `dst`
+static int import_vec(gq_ctx* c, const double* src, double* dst) {
+  const double* ref = src;
+  if (!is_device_ptr(src)) {
+    CK(cudaMemcpyAsync(c->tmp1, src, c->g.dim * 8, cudaMemcpyHostToDevice, c->stream));
+    ref = c->tmp1;
+  }
+  CK(launch_to_internal(c->g, ref, dst, c->stream));
+  return GQ_OK;
+}
+
+// internal vector -> user vector (reference layout, host or device); synchronises
+static int export_vec(gq_ctx* c, const double* src, double* dst) {
+  if (is_device_ptr(dst)) {
+    CK(launch_to_reference(c->g, src, dst, c->stream));
+  } else {
+    CK(launch_to_reference(c->g, src, c->tmp1, c->stream));
+    CK(cudaMemcpyAsync(dst, c->tmp1, c->g.dim * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return GQ_OK;
+}
+
+// S outer x L inner sweeps from zero: out = P r  (nested_jacobi.py:105-122)
+static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* st, int dotmode,
+                           std::vector<std::string>* names) {
+  for (int s = 0; s < c->S; ++s) {
+    for (int l = 0; l < c->L; ++l) {
+      const bool last = (l == c->L - 1);
+      double* ob = last ? (s == c->S - 1 ? out : c->dl[s % 2]) : c->th[l % 2];
+      const double* tp = l > 0 ? c->th[(l - 1) % 2] : nullptr;
+      const double* dp = s > 0 ? c->dl[(s - 1) % 2] : nullptr;
+      const int dm = (last && s == c->S - 1) ? dotmode : kDotNone;
+      CK(launch_sweep(c->g, c->op, l > 0, s > 0, rin, tp, dp, ob, s > 0 ? c->sw_outer : c->sw,
+                      c->partials, st, dm, c->stream));
+      if (names) names->push_back("sweep_s" + std::to_string(s) + "_l" + std::to_string(l));
+    }
+  }
+  return GQ_OK;
+}
+
+extern "C" int gq_apply_delta(gq_ctx* c, const double* x, double* y) {
+  if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
+  int rc = import_vec(c, x, c->tmp0);
+  if (rc) return rc;
+  CK(launch_stencil(c->g, c->op, kDelta, c->tmp0, c->y, c->sh_delta, c->partials, nullptr,
+                    kDotNone, c->stream));
+  return export_vec(c, c->y, y);
+}
+
+extern "C" int gq_apply_outer_coupling(gq_ctx* c, const double* x, double* y) {
+  if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
+  int rc = import_vec(c, x, c->tmp0);
+  if (rc) return rc;
+  CK(launch_stencil(c->g, c->op, kOuter, c->tmp0, c->y, c->sh_outer, c->partials, nullptr,
+                    kDotNone, c->stream));
+  return export_vec(c, c->y, y);
+}
+
+extern "C" int gq_apply_inner_coupling(gq_ctx* c, const double* x, double* y) {
+  if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
+  int rc = import_vec(c, x, c->tmp0);
+  if (rc) return rc;
+  CK(launch_stencil(c->g, c->op, kInner, c->tmp0, c->y, c->sh_inner, c->partials, nullptr,
+                    kDotNone, c->stream));
+  return export_vec(c, c->y, y);
+}
+
+extern "C" int gq_pair_solve(gq_ctx* c, const double* rhs, double* out) {
+  if (!c || !rhs || !out) return fail(GQ_INVALID_ARG, "null argument");
+  int rc = import_vec(c, rhs, c->tmp0);
+  if (rc) return rc;
+  CK(launch_sweep(c->g, c->op, false, false, c->tmp0, nullptr, nullptr, c->y, c->sw,
+                  c->partials, nullptr, kDotNone, c->stream));
+  return export_vec(c, c->y, out);
+}
+
+extern "C" int gq_apply_precond(gq_ctx* c, const double* r, double* q) {
+  if (!c || !r || !q) return fail(GQ_INVALID_ARG, "null argument");
+  if (c->L % 2)
+    return fail(GQ_INVALID_ARG, "preconditioner use requires an even inner budget (got " +
+                                    std::to_string(c->L) + "); odd budgets are standalone-only");
+  int rc = import_vec(c, r, c->tmp0);
+  if (rc) return rc;
+  rc = enqueue_precond(c, c->tmp0, c->y, nullptr, kDotNone, nullptr);
+  if (rc) return rc;
+  return export_vec(c, c->y, q);
+}
+
+// ---- PCG ----------------------------------------------------------------------------------
+
+static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* names,
+                        std::vector<cudaEvent_t>* evs) {
+  size_t ei = 0;
+  auto mark = [&]() -> int {
+    if (evs) CK(cudaEventRecord((*evs)[ei++], c->stream));
+    return GQ_OK;
+  };
+  int rc = mark();
+  if (rc) return rc;
+  CK(launch_stencil(c->g, c->op, kDelta, c->d, c->y, c->sh_delta, c->partials, c->st,
+                    kDotStep, c->stream));
+  if (names) names->push_back("delta");
+  if ((rc = mark())) return rc;
+  CK(launch_update(c->g, c->x, c->r, c->d, c->y, c->vblocks, c->partials, c->st, c->stream));
+  if (names) names->push_back("update");
+  if ((rc = mark())) return rc;
+  const double* qv = c->q;
+  if (use_precond) {
+    // one event per sweep
+    for (int s = 0; s < c->S; ++s)
+      for (int l = 0; l < c->L; ++l) {
+        const bool last = (l == c->L - 1);
+        double* ob = last ? (s == c->S - 1 ? c->q : c->dl[s % 2]) : c->th[l % 2];
+        const double* tp = l > 0 ? c->th[(l - 1) % 2] : nullptr;
+        const double* dp = s > 0 ? c->dl[(s - 1) % 2] : nullptr;
+        const int dm = (last && s == c->S - 1) ? kDotStep : kDotNone;
+        CK(launch_sweep(c->g, c->op, l > 0, s > 0, c->r, tp, dp, ob, s > 0 ? c->sw_outer : c->sw,
+                        c->partials, c->st, dm, c->stream));
+        if (names) names->push_back("sweep_s" + std::to_string(s) + "_l" + std::to_string(l));
+        if ((rc = mark())) return rc;
+      }
+  } else {
+    CK(launch_dot(c->g, c->r, c->r, c->vblocks, c->partials, c->st, kDotStep, c->stream));
+    if (names) names->push_back("dot");
+    if ((rc = mark())) return rc;
+    qv = c->r;
+  }
+  CK(launch_dirupdate(c->g, c->d, qv, c->vblocks, c->st, c->stream));
+  if (names) names->push_back("dirupdate");
+  return mark();
+}
+
+extern "C" int gq_launches_per_step(gq_ctx* c) {
+  return c ? (c->use_precond ? 3 + c->S * c->L : 4) : -1;
+}
+
+extern "C" int gq_pcg_start(gq_ctx* c, const double* rhs, const double* x0, int32_t use_precond) {
+  if (!c || !rhs) return fail(GQ_INVALID_ARG, "null argument");
+  if (use_precond && (c->L % 2))
+    return fail(GQ_INVALID_ARG, "preconditioner use requires an even inner budget (got " +
+                                    std::to_string(c->L) + "); odd budgets are standalone-only");
+  c->use_precond = use_precond ? 1 : 0;
+  c->started = false;
+  memset(c->h_st, 0, sizeof(PcgState));
+  c->h_st->hist = c->hist;
+  c->h_st->max_steps = 1;
+  CK(cudaMemcpyAsync(c->st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
+  int rc = import_vec(c, rhs, c->r);
+  if (rc) return rc;
+  if (x0) {
+    // r = rhs - Delta x0  (pcg.py:82-85)
+    rc = import_vec(c, x0, c->x);
+    if (rc) return rc;
+    CK(launch_stencil(c->g, c->op, kDelta, c->x, c->y, c->sh_delta, c->partials, nullptr,
+                      kDotNone, c->stream));
+    CK(launch_sub(c->g, c->tmp0, c->r, c->y, c->vblocks, c->stream));
+    CK(cudaMemcpyAsync(c->r, c->tmp0, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CK(cudaMemsetAsync(c->x, 0, c->g.dim * 8, c->stream));
+  }
+  if (use_precond) {
+    // d = P r ; mu = d.r   (pcg.py:87-93)
+    rc = enqueue_precond(c, c->r, c->q, c->st, kDotInit, nullptr);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->d, c->q, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CK(cudaMemcpyAsync(c->d, c->r, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(launch_dot(c->g, c->d, c->r, c->vblocks, c->partials, c->st, kDotInit, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  c->started = true;
+  return GQ_OK;
+}
+
+static int ensure_hist(gq_ctx* c, long long cap) {
+  if (cap <= c->hist_cap) return GQ_OK;
+  long long ncap = std::max(cap, std::max(64LL, c->hist_cap * 2));
+  double* nh = nullptr;
+  CK(dalloc(&nh, (size_t)ncap));
+  if (c->hist) {
+    CK(cudaMemcpyAsync(nh, c->hist, c->hist_cap * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(c->hist);
+  }
+  c->hist = nh;
+  c->hist_cap = ncap;
+  return GQ_OK;
+}
+
+static int ensure_graph(gq_ctx* c) {
+  const int k = c->use_precond;
+  if (c->gexec[k]) return GQ_OK;
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_step(c, k, nullptr, nullptr);
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(GQ_CUDA_ERROR, std::string("capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&c->gexec[k], graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(GQ_CUDA_ERROR, std::string("instantiate: ") + cudaGetErrorString(e));
+  return GQ_OK;
+}
+
+extern "C" int gq_pcg_run(gq_ctx* c, double tol, int64_t max_steps, int64_t* steps_done,
+                          int32_t* converged) {
+  if (!c) return fail(GQ_INVALID_ARG, "null context");
+  if (!c->started) return fail(GQ_INVALID_ARG, "gq_pcg_start has not been called");
+  if (!(tol > 0)) return fail(GQ_INVALID_ARG, "tolerance must be positive");
+  if (max_steps < 1) return fail(GQ_INVALID_ARG, "need at least one step");
+  CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  PcgState& h = *c->h_st;
+  if (!h.converged && !h.breakdown && h.step < max_steps) {
+    int rc = ensure_hist(c, max_steps);
+    if (rc) return rc;
+    h.hist = c->hist;
+    h.tol = tol;
+    h.max_steps = max_steps;
+    h.done = 0;
+    CK(cudaMemcpyAsync(c->st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
+    rc = ensure_graph(c);
+    if (rc) return rc;
+    long long chunk = 2;
+    while (true) {
+      const long long todo = std::min<long long>(chunk, max_steps - h.step);
+      for (long long i = 0; i < todo; ++i) CK(cudaGraphLaunch(c->gexec[c->use_precond], c->stream));
+      CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (h.done || h.step >= max_steps) break;
+      chunk = std::min<long long>(chunk * 2, 64);
+    }
+  }
+  if (steps_done) *steps_done = h.step;
+  if (converged) *converged = h.converged;
+  if (h.breakdown)
+    return fail(GQ_BREAKDOWN, "non-positive curvature " + std::to_string(h.curv) +
+                                  "; operator or preconditioner is not positive definite");
+  if (h.converged) return GQ_OK;
+  return fail(GQ_MAX_ITER, "conjugate gradient did not reach the tolerance within " +
+                               std::to_string(h.step) + " steps");
+}
+
+extern "C" int gq_pcg_read(gq_ctx* c, int32_t which, double* out) {
+  if (!c || !out) return fail(GQ_INVALID_ARG, "null argument");
+  if (!c->started) return fail(GQ_INVALID_ARG, "gq_pcg_start has not been called");
+  const double* src = which == GQ_VEC_R ? c->r : c->x;
+  return export_vec(c, src, out);
+}
+
+extern "C" int gq_pcg_history(gq_ctx* c, double* out, int64_t count) {
+  if (!c || (!out && count > 0)) return fail(GQ_INVALID_ARG, "null argument");
+  if (count <= 0) return GQ_OK;
+  if (count > c->hist_cap) return fail(GQ_INVALID_ARG, "history request exceeds recorded steps");
+  CK(cudaMemcpyAsync(out, c->hist, count * 8, cudaMemcpyDefault, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return GQ_OK;
+}
+
+extern "C" int gq_pcg_scalars(gq_ctx* c, double* mu, double* curv, double* alpha, double* beta) {
+  if (!c) return fail(GQ_INVALID_ARG, "null context");
+  CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (mu) *mu = c->h_st->mu;
+  if (curv) *curv = c->h_st->curv;
+  if (alpha) *alpha = c->h_st->alpha;
+  if (beta) *beta = c->h_st->beta;
+  return GQ_OK;
+}
+
+extern "C" int gq_pcg(gq_ctx* c, const double* rhs, const double* x0, double tol,
+                      int64_t max_steps, int32_t use_precond, double* x_out, double* hist_out,
+                      int64_t hist_capacity, int64_t* steps, int32_t* converged) {
+  int rc = gq_pcg_start(c, rhs, x0, use_precond);
+  if (rc) return rc;
+  int64_t s = 0;
+  int32_t conv = 0;
+  const int status = gq_pcg_run(c, tol, max_steps, &s, &conv);
+  if (status != GQ_OK && status != GQ_MAX_ITER && status != GQ_BREAKDOWN) return status;
+  const std::string msg = g_err;
+  if (x_out && (rc = gq_pcg_read(c, GQ_VEC_X, x_out))) return rc;
+  if (hist_out && (rc = gq_pcg_history(c, hist_out, std::min<int64_t>(s, hist_capacity))))
+    return rc;
+  if (steps) *steps = s;
+  if (converged) *converged = conv;
+  g_err = msg;
+  return status;
+}
+
+extern "C" int gq_profile_steps(gq_ctx* c, int32_t steps, float* ms_out, int32_t count) {
+  if (!c || !c->started) return fail(GQ_INVALID_ARG, "gq_pcg_start has not been called");
+  const int nk = gq_launches_per_step(c);
+  std::vector<cudaEvent_t> ev(nk + 1);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  std::vector<double> acc(nk, 0.0);
+  c->knames.clear();
+  int rc = GQ_OK;
+  for (int s = 0; s < steps && rc == GQ_OK; ++s) {
+    std::vector<std::string> names;
+    rc = enqueue_step(c, c->use_precond, &names, &ev);
+    if (rc) break;
+    cudaError_t e = cudaEventSynchronize(ev[nk]);
+    if (e != cudaSuccess) {
+      rc = fail(GQ_CUDA_ERROR, cudaGetErrorString(e));
+      break;
+    }
+    for (int i = 0; i < nk; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      acc[i] += ms;
+    }
+    c->knames = names;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (rc) return rc;
+  for (int i = 0; i < nk && i < count; ++i) ms_out[i] = (float)acc[i];
+  return nk;
+}
+
+extern "C" const char* gq_kernel_name(gq_ctx* c, int32_t i) {
+  if (!c || i < 0 || i >= (int)c->knames.size()) return "";
+  return c->knames[i].c_str();
+}

@@ -1,0 +1,67 @@
+// Host-side launchers shared between the kernel translation units and the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "gq_common.cuh"
+
+namespace gq {
+
+enum StencilMode { kDelta = 0, kOuter = 1, kInner = 2 };
+
+struct SetupErr {
+  int code;        // 0 ok, 1 not SPD
+  int cls, v, k, j;
+  double pivot, tol;
+};
+
+// Returns false if n has no compiled instantiation.
+bool n_supported(int n);
+
+// ---- setup (gq_setup.cu) ----
+cudaError_t launch_spd_inverse(const double* in, double* out, long long count, int dim,
+                               SetupErr* err, cudaStream_t s);
+cudaError_t launch_brb(const Geo& g, int m, int n_dyn, const double* B, const double* rinv,
+                       double* brb, cudaStream_t s);
+cudaError_t launch_xi(const Geo& g, int nxc, const int* xi_keys, const double* A,
+                      const double* C, const double* qinv, double* xi, double* xit,
+                      cudaStream_t s);
+cudaError_t launch_psi(const Geo& g, int npc, const int* psi_keys, const double* A,
+                       const double* C, const double* qinv, const double* brb, double* psi,
+                       cudaStream_t s);
+cudaError_t launch_factor(const Geo& g, int npc, const double* psi, double* fac,
+                          double* scratch, SetupErr* err, cudaStream_t s);
+
+// ---- stencil (gq_stencil.cu) ----
+struct StencilShape {
+  int nchunk, nstrip, rows, blocks, threads;
+};
+StencilShape stencil_shape(const Geo& g, int mode, int sm_count);
+cudaError_t launch_stencil(const Geo& g, const Ops& op, int mode, const double* x, double* y,
+                           const StencilShape& sh, double* partials, PcgState* st,
+                           int dotmode, cudaStream_t s);
+
+// ---- pair sweeps (gq_sweep.cu) ----
+struct SweepShape {
+  int blocks, threads;
+};
+SweepShape sweep_shape(const Geo& g, bool outer);
+cudaError_t launch_sweep(const Geo& g, const Ops& op, bool inner, bool outer, const double* r,
+                         const double* theta, const double* delta, double* out,
+                         const SweepShape& sh, double* partials, PcgState* st, int dotmode,
+                         cudaStream_t s);
+
+// ---- vector kernels (gq_vec.cu) ----
+int vec_blocks(int sm_count);
+cudaError_t launch_update(const Geo& g, double* x, double* r, const double* d, const double* y,
+                          int blocks, double* partials, PcgState* st, cudaStream_t s);
+cudaError_t launch_dirupdate(const Geo& g, double* d, const double* q, int blocks,
+                             PcgState* st, cudaStream_t s);
+cudaError_t launch_dot(const Geo& g, const double* a, const double* b, int blocks,
+                       double* partials, PcgState* st, int dotmode, cudaStream_t s);
+cudaError_t launch_sub(const Geo& g, double* out, const double* a, const double* b, int blocks,
+                       cudaStream_t s);
+cudaError_t launch_to_internal(const Geo& g, const double* ref, double* dev, cudaStream_t s);
+cudaError_t launch_to_reference(const Geo& g, const double* dev, double* ref, cudaStream_t s);
+
+}  // namespace gq

@@ -1,0 +1,172 @@
+// CG vector updates with fused reductions, plus the boundary layout transposes.
+//
+// Reference: pcg_solve loop body (gridlq/pcg.py:98-131).  The element-wise updates use
+// explicitly rounded multiply and add (no FMA contraction) so that, given identical
+// inputs, they reproduce numpy's `x += alpha*d`, `r - alpha*y`, `q + beta*d` bit for bit.
+// Reductions are grid-wide with a fixed partial order (bitwise reproducible run to run).
+#include "gq_internal.h"
+
+namespace gq {
+
+int vec_blocks(int sm_count) { return sm_count * 4; }
+
+__global__ void __launch_bounds__(256) k_update(long long dim, double* __restrict__ x,
+                                                double* __restrict__ r,
+                                                const double* __restrict__ d,
+                                                const double* __restrict__ y, double* partials,
+                                                PcgState* st) {
+  if (st->done) return;
+  const double alpha = st->alpha;
+  double m = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride) {
+    x[e] = __dadd_rn(x[e], __dmul_rn(alpha, d[e]));          // pcg.py:109
+    const double rn = __dsub_rn(r[e], __dmul_rn(alpha, y[e]));  // pcg.py:111
+    r[e] = rn;
+    m = nmax(m, fabs(rn));                                     // pcg.py:113
+  }
+  double res;
+  if (grid_reduce<true>(m, partials, &st->counter[1], res) && threadIdx.x == 0) {
+    st->res = res;
+    st->hist[st->step] = res;
+    st->step += 1;
+    if (res < st->tol) {            // pcg.py:119-121
+      st->converged = 1;
+      st->done = 1;
+    } else if (st->step >= st->max_steps) {
+      st->done = 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dirupdate(long long dim, double* __restrict__ d,
+                                                   const double* __restrict__ q, PcgState* st) {
+  if (st->done) return;
+  const double beta = st->beta;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride)
+    d[e] = __dadd_rn(q[e], __dmul_rn(beta, d[e]));            // pcg.py:129
+}
+
+__global__ void __launch_bounds__(256) k_dot(long long dim, const double* __restrict__ a,
+                                             const double* __restrict__ b, double* partials,
+                                             PcgState* st, int dotmode) {
+  if (st->done) return;
+  double s = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride)
+    s = fma(a[e], b[e], s);
+  double mu;
+  if (grid_reduce<false>(s, partials, &st->counter[3], mu) && threadIdx.x == 0) {
+    if (dotmode == kDotInit) {
+      st->mu = mu;
+    } else {
+      st->beta = mu / st->mu;
+      st->mu = mu;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sub(long long dim, double* __restrict__ out,
+                                             const double* __restrict__ a,
+                                             const double* __restrict__ b) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride)
+    out[e] = __dsub_rn(a[e], b[e]);
+}
+
+cudaError_t launch_update(const Geo& g, double* x, double* r, const double* d, const double* y,
+                          int blocks, double* partials, PcgState* st, cudaStream_t s) {
+  k_update<<<blocks, 256, 0, s>>>(g.dim, x, r, d, y, partials, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dirupdate(const Geo& g, double* d, const double* q, int blocks, PcgState* st,
+                             cudaStream_t s) {
+  k_dirupdate<<<blocks, 256, 0, s>>>(g.dim, d, q, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dot(const Geo& g, const double* a, const double* b, int blocks,
+                       double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  k_dot<<<blocks, 256, 0, s>>>(g.dim, a, b, partials, st, dotmode);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sub(const Geo& g, double* out, const double* a, const double* b, int blocks,
+                       cudaStream_t s) {
+  k_sub<<<blocks, 256, 0, s>>>(g.dim, out, a, b);
+  return cudaGetLastError();
+}
+
+// ---- layout transposes ------------------------------------------------------------------
+// reference order (t, node, k) <-> stage-inner order (node, t, k); a tile is TS stages x
+// TN nodes of n-double records staged through shared memory so both sides are coalesced.
+constexpr int kTS = 32;
+
+template <bool TO_INTERNAL>
+__global__ void __launch_bounds__(256) k_transpose(Geo g, int tn, const double* __restrict__ src,
+                                                   double* __restrict__ dst) {
+  extern __shared__ double tile[];   // [kTS][tn][n]
+  const int n = g.n;
+  const long long nodes = g.nk;
+  const int t0 = blockIdx.y * kTS;
+  const long long nd0 = (long long)blockIdx.x * tn;
+  const int rec = tn * n;            // doubles per stage row of the tile
+  const int total = kTS * rec;
+  if (TO_INTERNAL) {
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int ts = e / rec, w = e % rec;
+      const int t = t0 + ts;
+      const long long nd = nd0 + w / n;
+      if (t < g.T1 && nd < nodes) tile[e] = src[(long long)t * nodes * n + nd0 * n + w];
+    }
+    __syncthreads();
+    const int rec2 = kTS * n;        // doubles per node row of the output
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int nl = e / rec2, w = e % rec2;
+      const int ts = w / n, k = w % n;
+      const long long nd = nd0 + nl;
+      const int t = t0 + ts;
+      if (t < g.T1 && nd < nodes) dst[(nd * g.T1 + t) * n + k] = tile[ts * rec + nl * n + k];
+    }
+  } else {
+    const int rec2 = kTS * n;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int nl = e / rec2, w = e % rec2;
+      const int ts = w / n, k = w % n;
+      const long long nd = nd0 + nl;
+      const int t = t0 + ts;
+      if (t < g.T1 && nd < nodes) tile[ts * rec + nl * n + k] = src[(nd * g.T1 + t) * n + k];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int ts = e / rec, w = e % rec;
+      const int t = t0 + ts;
+      const long long nd = nd0 + w / n;
+      if (t < g.T1 && nd < nodes) dst[(long long)t * nodes * n + nd0 * n + w] = tile[e];
+    }
+  }
+}
+
+static cudaError_t launch_transpose(const Geo& g, bool to_internal, const double* src,
+                                    double* dst, cudaStream_t s) {
+  const int tn = g.n <= 2 ? 32 : (g.n <= 4 ? 16 : 8);
+  dim3 grid((unsigned)((g.nk + tn - 1) / tn), (unsigned)((g.T1 + kTS - 1) / kTS));
+  const size_t smem = (size_t)kTS * tn * g.n * sizeof(double);
+  if (to_internal)
+    k_transpose<true><<<grid, 256, smem, s>>>(g, tn, src, dst);
+  else
+    k_transpose<false><<<grid, 256, smem, s>>>(g, tn, src, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_internal(const Geo& g, const double* ref, double* dev, cudaStream_t s) {
+  return launch_transpose(g, true, ref, dev, s);
+}
+
+cudaError_t launch_to_reference(const Geo& g, const double* dev, double* ref, cudaStream_t s) {
+  return launch_transpose(g, false, dev, ref, s);
+}
+
+}  // namespace gq
