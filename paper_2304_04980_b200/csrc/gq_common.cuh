@@ -62,9 +62,15 @@ struct PcgState {
   double mu, curv, alpha, beta, res, tol;
   long long step, max_steps;
   double* hist;
-  int done, converged, breakdown, pad;
+  int done, converged, breakdown;
+  int skip;   // set by the first kernel of a step when the step budget is exhausted
   unsigned int counter[4];
 };
+
+// kernels after the first one of a step stop on convergence, breakdown or budget
+__device__ __forceinline__ bool halted(const PcgState* st) {
+  return st != nullptr && (st->done || st->skip);
+}
 
 enum DotMode { kDotNone = 0, kDotInit = 1, kDotStep = 2 };
 

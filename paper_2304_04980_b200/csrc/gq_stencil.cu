@@ -30,7 +30,17 @@ __global__ void __launch_bounds__(256) k_stencil(Geo g, Ops op, const double* __
                                                  double* __restrict__ y, int nchunk,
                                                  int nstrip, int rows, double* partials,
                                                  PcgState* st, int dotmode) {
-  if (st != nullptr && st->done) return;
+  if (st != nullptr) {
+    if (dotmode == kDotStep) {
+      // first kernel of a PCG step: the step budget is checked here so that the step
+      // that reaches max_steps still completes (pcg.py:98-131 runs its whole body)
+      const bool stop = st->done || st->step >= st->max_steps;
+      if (blockIdx.x == 0 && threadIdx.x == 0) st->skip = stop ? 1 : 0;
+      if (stop) return;
+    } else if (halted(st)) {
+      return;
+    }
+  }
   constexpr bool HALO = (MODE != kInner);
   constexpr int CH = HALO ? kHaloChunk : 32;
   constexpr int B2 = NS * NS;

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(128) k_sweep(Geo g, Ops op, const double* __re
                                                const double* __restrict__ th,
                                                const double* __restrict__ dl, double* out,
                                                double* partials, PcgState* st, int dotmode) {
-  if (st != nullptr && st->done) return;
+  if (halted(st)) return;
   constexpr int Q = 4 * NS;
   constexpr int B2 = NS * NS;
   constexpr int CH = OUTER ? kHaloChunk : 32;

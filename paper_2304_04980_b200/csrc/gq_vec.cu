@@ -15,7 +15,7 @@ __global__ void __launch_bounds__(256) k_update(long long dim, double* __restric
                                                 const double* __restrict__ d,
                                                 const double* __restrict__ y, double* partials,
                                                 PcgState* st) {
-  if (st->done) return;
+  if (halted(st)) return;
   const double alpha = st->alpha;
   double m = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -33,15 +33,13 @@ __global__ void __launch_bounds__(256) k_update(long long dim, double* __restric
     if (res < st->tol) {            // pcg.py:119-121
       st->converged = 1;
       st->done = 1;
-    } else if (st->step >= st->max_steps) {
-      st->done = 1;
     }
   }
 }
 
 __global__ void __launch_bounds__(256) k_dirupdate(long long dim, double* __restrict__ d,
                                                    const double* __restrict__ q, PcgState* st) {
-  if (st->done) return;
+  if (halted(st)) return;
   const double beta = st->beta;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride)
@@ -51,7 +49,7 @@ __global__ void __launch_bounds__(256) k_dirupdate(long long dim, double* __rest
 __global__ void __launch_bounds__(256) k_dot(long long dim, const double* __restrict__ a,
                                              const double* __restrict__ b, double* partials,
                                              PcgState* st, int dotmode) {
-  if (st->done) return;
+  if (halted(st)) return;
   double s = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride)
