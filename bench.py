@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 PCGM hot path (BASELINE.json metric: PCGM steps/s and achieved
+HBM GB/s at K=N=256, T=200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+A "step" is one PCGM iteration (pcg.py:98-131): Delta-apply + curvature, x/r update +
+||r||_inf, S x L nested-block-Jacobi sweeps + q.r, direction update.  Default workload is
+BASELINE config 4 (mass-spring-damper 256 x 256 grid, T=200, n=2, m=1, S=L=2; seeded
+synthetic data, no dataset involved).  Every vector is 210.8 MB, larger than the 126 MB
+L2, so no L2 flush is needed between timed steps.
+
+Multi-GPU (torchrun): the PCGM step does not shard in round 1 (SURVEY.md 8(e) lists
+stage-slab sharding as "next"), so N ranks run N independent replicas ("replicas only");
+value = total steps of all ranks / max-over-ranks device time.
+
+--impl reference times the CPU restatement of the reference algorithm (oracle/, the
+reference itself is pure Python + NumPy and cannot run at this size: SURVEY.md 6) on
+the host cores for a bounded number of steps of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCGM steps/s"
+UNIT = "steps/s"
+CONFIG_NAMES = {1: "config1 random 4x4 T=20 n=2", 2: "config2 msd 16x16 T=50 n=2",
+                3: "config3 random 64x64 T=100 n=4", 4: "config4 msd 256x256 T=200 n=2",
+                5: "config5 random 32x1024 T=500 n=8"}
+
+
+def c_factor(S, L):
+    """canonical full-vector passes per step, C(S,L)."""
+    return 10 + (3 * L - 1) + (S - 1) * (4 * L - 1)
+
+
+def kernel_passes(name):
+    """Algorithmic full-vector reads+writes of one launch of each step kernel."""
+    if name == "delta":
+        return 2                       # read d, write y (+ y.d)
+    if name == "update":
+        return 6                       # read x, r, d, y; write x, r (+ max|r|)
+    if name == "dirupdate":
+        return 3                       # read q, d; write d
+    if name == "dot":
+        return 2
+    if name.startswith("sweep_s"):
+        s = int(name.split("_s")[1].split("_")[0])
+        l_ = int(name.split("_l")[1])
+        return 2 + (1 if l_ > 0 else 0) + (1 if s > 0 else 0)
+    return 0
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def traffic_from_profiles(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh)
+        return data.get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_04980_b200 import (GpuNestedJacobiPreconditioner, GpuSchurOperator,
+                                       MaxIterationsExceeded, _lib, generators, pcg_solve)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    S, L = args.S, args.L
+    ga = generators.CONFIGS[args.config](args.seed)
+    t0 = time.perf_counter()
+    op = GpuSchurOperator(ga, L, S)
+    pc = GpuNestedJacobiPreconditioner(op, L, S)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    ctx = op._ctx
+    lib = ctx.lib
+    stream = torch.cuda.Stream(device=dev)
+    _lib.check(lib.gq_set_stream(ctx.h, ctypes.c_void_p(stream.cuda_stream)))
+    rhs = torch.tensor(ga.offset, device=dev, dtype=torch.float64)
+    tol = 1e-300            # fixed-step run (BASELINE config 4: fixed 100 steps)
+    steps = ctypes.c_int64()
+    conv = ctypes.c_int32()
+    _lib.check(lib.gq_pcg_start(ctx.h, ctypes.c_void_p(rhs.data_ptr()), None, 1))
+    W, K = args.warmup, args.steps
+    rc = lib.gq_pcg_run(ctx.h, tol, W, ctypes.byref(steps), ctypes.byref(conv))
+    assert rc in (_lib.GQ_OK, _lib.GQ_MAX_ITER), _lib.last_error()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        rc = lib.gq_pcg_run(ctx.h, tol, W + K, ctypes.byref(steps), ctypes.byref(conv))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    assert rc in (_lib.GQ_OK, _lib.GQ_MAX_ITER), _lib.last_error()
+    assert steps.value == W + K, (steps.value, W + K)
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    hist = np.empty(W + K)
+    _lib.check(lib.gq_pcg_history(ctx.h, hist.ctypes.data, W + K))
+
+    # per-kernel device times (CUDA events on the launch stream, individual launches)
+    nk = lib.gq_launches_per_step(ctx.h)
+    prof_steps = 3
+    buf = (ctypes.c_float * nk)()
+    got = lib.gq_profile_steps(ctx.h, prof_steps, buf, nk)
+    assert got == nk, _lib.last_error()
+    names = [lib.gq_kernel_name(ctx.h, i).decode() for i in range(nk)]
+    kms = {nm: buf[i] / prof_steps for i, nm in enumerate(names)}
+    dim = op.dim
+    vec_bytes = 8 * dim
+    peak, peak_src = load_peaks()
+    top = max(kms, key=kms.get)
+    top_bytes = kernel_passes(top) * vec_bytes
+    achieved = top_bytes / (kms[top] * 1e-3) / 1e9
+    step_bytes = 8 * dim * c_factor(S, L)
+    step_ms = ms / K
+    step_gbs = step_bytes / (step_ms * 1e-3) / 1e9
+    total_ms = sum(kms.values())
+
+    # end to end through the public API with host buffers (H2D rhs, D2H x + history)
+    rhs_host = torch.from_numpy(ga.offset.copy()).pin_memory().numpy()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    try:
+        pcg_solve(op, pc, rhs_host, tol=tol, max_steps=K)
+        raise RuntimeError("unexpected convergence in a fixed-step run")
+    except MaxIterationsExceeded as exc:
+        x_out = exc.iterate
+    e2e_s = time.perf_counter() - t0
+    assert x_out.shape == (dim,)
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    line = {
+        "metric": METRIC,
+        "value": K * ws / (ms * 1e-3),
+        "unit": UNIT,
+        "n_gpus": ws,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": ms / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator, no dataset)",
+        "config": {
+            "workload": CONFIG_NAMES.get(args.config, str(args.config)),
+            "K": ga.K, "N": ga.N, "T": ga.T, "n": ga.n, "m": ga.m,
+            "outer_sweeps_S": S, "inner_sweeps_L": L, "dim": dim,
+            "parallelism": "replicas only" if ws > 1 else "single GPU",
+            "l2": "inputs larger than L2 (one vector = %.1f MB)" % (vec_bytes / 1e6),
+            "setup_s": round(setup_s, 3),
+        },
+        "roofline": {
+            "bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic_from_profiles(top),
+            "algorithmic_bytes_per_launch": top_bytes,
+        },
+        "step_roofline": {
+            "bytes_per_step": step_bytes, "C(S,L)": c_factor(S, L), "achieved": step_gbs,
+            "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
+            "model": "SURVEY.md 8(d): 8*dim*C(S,L) canonical full-vector traffic",
+        },
+        "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
+        "kernel_share": {k: round(v / total_ms, 4) for k, v in kms.items()},
+        "gpu_launches": K * nk,
+        "residual_inf": [float(hist[0]), float(hist[-1])],
+        "e2e": {
+            "value": K * ws / e2e_s, "unit": UNIT,
+            "h2d_bytes_per_step": vec_bytes / K, "d2h_bytes_per_step": (vec_bytes + 8 * K) / K,
+            "includes": "pcg_solve() on host numpy rhs: H2D rhs + layout transpose, "
+                        "initial preconditioner apply, K steps, D2H x + history",
+        },
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, ga)
+    return line
+
+
+def _oracle_steps(ga, S, L, steps, threads, budget_s=None):
+    """Time PCGM steps of the C oracle (oracle/gridlq_oracle.c, restating pcg.py's loop);
+    setup and the initial preconditioner apply are excluded.  Returns (seconds per
+    step, setup seconds, steps timed, threads)."""
+    from oracle.coracle import COracle
+    from oracle.gridlq_oracle import Oracle
+
+    t0 = time.perf_counter()
+    orc = COracle(Oracle(ga, L, S), threads=threads)
+    setup = time.perf_counter() - t0
+    if budget_s is not None:
+        # one probe step, then as many as fit in the budget (at least 2, at most `steps`)
+        _, _, _, _, _, secs = orc.pcg(ga.offset, tol=1e-300, max_steps=2)
+        per = secs[1] - secs[0]
+        steps = int(max(2, min(steps, budget_s / max(per, 1e-9))))
+    _, _, k, _, _, secs = orc.pcg(ga.offset, tol=1e-300, max_steps=max(2, steps))
+    per_step = (secs[k - 1] - secs[0]) / (k - 1)
+    return per_step, setup, k - 1, orc.threads
+
+
+def cpu_baseline(args, ga):
+    per_step, setup, k, th = _oracle_steps(ga, args.S, args.L, args.cpu_steps + 1, 1)
+    return {
+        "value": 1.0 / per_step, "unit": UNIT, "cores": th, "kind": "port",
+        "sample": f"{k} PCGM step(s) of the same workload with the C restatement of the "
+                  f"reference loop (oracle/gridlq_oracle.c), 1 thread; setup {setup:.1f}s "
+                  "and the initial preconditioner apply excluded",
+        "host_cpus": os.cpu_count(),
+    }
+
+
+def run_reference(args, ws, rank):
+    from paper_2304_04980_b200 import generators
+
+    ga = generators.CONFIGS[args.config](args.seed)
+    threads = os.cpu_count() or 1
+    per_step, setup, k, th = _oracle_steps(ga, args.S, args.L, args.steps + 1, threads,
+                                           budget_s=args.ref_budget_s)
+    value = 1.0 / per_step
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator, no dataset)", "impl": "reference",
+        "config": {"workload": CONFIG_NAMES.get(args.config, str(args.config)),
+                   "K": ga.K, "N": ga.N, "T": ga.T, "n": ga.n, "m": ga.m,
+                   "outer_sweeps_S": args.S, "inner_sweeps_L": args.L, "dim": ga.dim},
+        "cpu_baseline": {
+            "value": value, "unit": UNIT, "cores": th, "kind": "port",
+            "sample": f"{k} of {args.steps} PCGM steps of the same workload, C/OpenMP "
+                      "restatement of the reference loop (oracle/gridlq_oracle.c; the "
+                      "reference itself is pure Python/NumPy, ~530 s/step here per "
+                      f"SURVEY.md 6); setup {setup:.1f}s excluded",
+        },
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--S", type=int, default=None)
+    ap.add_argument("--L", type=int, default=None)
+    ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.S is None:
+        args.S = 3 if args.config == 3 else 2
+    if args.L is None:
+        args.L = 2
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args, ws, rank)), flush=True)
+        return
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    try:
+        line = run_ours(args, ws, rank, local)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
