@@ -598,6 +598,19 @@ extern "C" int gq_pcg(gq_ctx* c, const double* rhs, const double* x0, double tol
 extern "C" int gq_profile_steps(gq_ctx* c, int32_t steps, float* ms_out, int32_t count) {
   if (!c || !c->started) return fail(GQ_INVALID_ARG, "gq_pcg_start has not been called");
   const int nk = gq_launches_per_step(c);
+  // extend the step budget so the profiled steps really run
+  CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->h_st->converged || c->h_st->breakdown)
+    return fail(GQ_INVALID_ARG, "solve already finished; restart with gq_pcg_start");
+  c->h_st->max_steps = c->h_st->step + steps;
+  c->h_st->done = 0;
+  {
+    int rc0 = ensure_hist(c, c->h_st->max_steps);
+    if (rc0) return rc0;
+  }
+  c->h_st->hist = c->hist;
+  CK(cudaMemcpyAsync(c->st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
   std::vector<cudaEvent_t> ev(nk + 1);
   for (auto& e : ev) CK(cudaEventCreate(&e));
   std::vector<double> acc(nk, 0.0);
