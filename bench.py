@@ -57,10 +57,11 @@ def kernel_passes(name):
         return 3                       # read q, d; write d
     if name == "dot":
         return 2
+    if name.startswith("outer_rhs"):
+        return 3                       # read delta, r; write r + Xi~ delta
     if name.startswith("sweep_s"):
-        s = int(name.split("_s")[1].split("_")[0])
-        l_ = int(name.split("_l")[1])
-        return 2 + (1 if l_ > 0 else 0) + (1 if s > 0 else 0)
+        l_ = int(name.split("_l")[1].split("_")[0])
+        return 2 + (1 if l_ > 0 else 0) + (1 if name.endswith("_xi") else 0)
     return 0
 
 

@@ -14,6 +14,7 @@
 #include <map>
 #include <array>
 #include <algorithm>
+#include <functional>
 
 #include "gq_internal.h"
 #include "../../include/gridlq_b200.h"
@@ -45,6 +46,10 @@ struct gq_ctx {
   double *x = nullptr, *r = nullptr, *d = nullptr, *y = nullptr, *q = nullptr;
   double *th[2] = {nullptr, nullptr}, *dl[2] = {nullptr, nullptr};
   double *tmp0 = nullptr, *tmp1 = nullptr;
+  double* rs = nullptr;        // r + Xi~ delta of the current outer sweep (fast path)
+  double *oprow = nullptr, *omega = nullptr, *fac3 = nullptr, *fac4 = nullptr;
+  FastOps fo{};
+  bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
   double* partials = nullptr;
   PcgState* st = nullptr;
   PcgState* h_st = nullptr;   // pinned mirror
@@ -85,7 +90,7 @@ static void release(gq_ctx* c) {
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
                   c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
                   c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->partials, c->st, c->hist, c->err};
+                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -211,6 +216,24 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   }
   c->npc = (int)pmap.size();
   c->nxc = (int)xmap.size();
+  {
+    // v2 kernels: one Xi class and at most two Psi classes inside every warp's stage range
+    auto ok_chunks = [&](int chunk, int halo) {
+      for (int t0 = -halo; t0 < g.T1; t0 += chunk) {
+        int ca = -1, cb = -1;
+        for (int t = std::max(t0, 0); t < std::min(t0 + 32, g.T1); ++t) {
+          const int cl = pcls[t];
+          if (ca < 0 || cl == ca) ca = cl;
+          else if (cb < 0 || cl == cb) cb = cl;
+          else return false;
+        }
+      }
+      return true;
+    };
+    const char* force = getenv("GQ_FORCE_V1");
+    c->fast = fast_supported(g.n) && c->nxc == 1 && ok_chunks(kHaloChunk, 1) &&
+              ok_chunks(32, 0) && !(force && *force == '1');
+  }
 
   const int n = D.n, m = D.m, q = 4 * n;
   const size_t nn = (size_t)n * n;
@@ -280,11 +303,22 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
     if (rc != GQ_OK) return bail(rc);
   }
   c->op = Ops{c->psi, c->xi, c->xit, c->fac, c->psi_cls, c->xi_cls};
+  if (c->fast) {
+    CKB(dalloc(&c->oprow, (size_t)c->npc * nk * 23 * nn));
+    CKB(dalloc(&c->omega, (size_t)c->npc * nk * 5 * nn));
+    if (tc_supported(g.n))
+      CKB(dalloc(&c->fac4, (size_t)c->npc * g.V * g.nb * 4 * q * q));
+    else
+      CKB(dalloc(&c->fac3, (size_t)c->npc * g.V * g.nb * 3 * q * q));
+    CKB(launch_build_fast(g, c->npc, c->op, c->oprow, c->omega, c->fac3, c->fac4, c->stream));
+    CKB(cudaStreamSynchronize(c->stream));
+    c->fo = FastOps{c->oprow, c->omega, c->fac3, c->psi_cls, c->fac4};
+  }
 
   // work vectors (stage-inner layout) and the reference-layout staging buffers
   const size_t dim = (size_t)g.dim;
   double** vecs[] = {&c->x, &c->r, &c->d, &c->y, &c->q, &c->th[0], &c->th[1],
-                     &c->dl[0], &c->dl[1], &c->tmp0, &c->tmp1};
+                     &c->dl[0], &c->dl[1], &c->tmp0, &c->tmp1, &c->rs};
   for (double** p : vecs) CKB(dalloc(p, dim));
   c->sh_delta = stencil_shape(g, kDelta, c->sm_count);
   c->sh_outer = stencil_shape(g, kOuter, c->sm_count);
@@ -292,7 +326,10 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   c->sw = sweep_shape(g, false);
   c->sw_outer = sweep_shape(g, true);
   c->vblocks = vec_blocks(c->sm_count);
-  int maxb = std::max({c->sh_delta.blocks, c->sw.blocks, c->sw_outer.blocks, c->vblocks});
+  long long maxb = std::max({(long long)c->sh_delta.blocks, (long long)c->sw.blocks,
+                             (long long)c->sw_outer.blocks, (long long)c->vblocks,
+                             fast_max_blocks(g, c->sh_delta, c->sm_count),
+                             fast_max_blocks(g, c->sh_outer, c->sm_count)});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));
   CKB(dalloc(&c->st, 1));
   CKB(cudaMemset(c->st, 0, sizeof(PcgState)));
@@ -330,17 +367,39 @@ static int export_vec(gq_ctx* c, const double* src, double* dst) {
 
 // S outer x L inner sweeps from zero: out = P r  (nested_jacobi.py:105-122)
 static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* st, int dotmode,
-                           std::vector<std::string>* names) {
+                           std::vector<std::string>* names,
+                           const std::function<int()>& mark = nullptr) {
   for (int s = 0; s < c->S; ++s) {
+    if (c->fast && s > 0) {
+      // rhs_s = r + Xi~ delta_{s-1}, materialised once per outer sweep (nested_jacobi.py:119-121)
+      CK(launch_stencil3(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->sh_outer,
+                         c->partials, st, kDotNone, c->stream));
+      if (names) names->push_back("outer_rhs_s" + std::to_string(s));
+      if (mark) {
+        const int rc = mark();
+        if (rc) return rc;
+      }
+    }
     for (int l = 0; l < c->L; ++l) {
       const bool last = (l == c->L - 1);
       double* ob = last ? (s == c->S - 1 ? out : c->dl[s % 2]) : c->th[l % 2];
       const double* tp = l > 0 ? c->th[(l - 1) % 2] : nullptr;
       const double* dp = s > 0 ? c->dl[(s - 1) % 2] : nullptr;
       const int dm = (last && s == c->S - 1) ? dotmode : kDotNone;
-      CK(launch_sweep(c->g, c->op, l > 0, s > 0, rin, tp, dp, ob, s > 0 ? c->sw_outer : c->sw,
-                      c->partials, st, dm, c->stream));
-      if (names) names->push_back("sweep_s" + std::to_string(s) + "_l" + std::to_string(l));
+      if (c->fast) {
+        CK(launch_sweep3(c->g, c->fo, l > 0, s > 0 ? c->rs : rin, tp, ob, rin, c->sm_count,
+                         c->partials, st, dm, c->stream));
+      } else {
+        CK(launch_sweep(c->g, c->op, l > 0, s > 0, rin, tp, dp, ob, s > 0 ? c->sw_outer : c->sw,
+                        c->partials, st, dm, c->stream));
+      }
+      if (names)
+        names->push_back("sweep_s" + std::to_string(s) + "_l" + std::to_string(l) +
+                         (!c->fast && s > 0 ? "_xi" : ""));
+      if (mark) {
+        const int rc = mark();
+        if (rc) return rc;
+      }
     }
   }
   return GQ_OK;
@@ -350,8 +409,12 @@ extern "C" int gq_apply_delta(gq_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, x, c->tmp0);
   if (rc) return rc;
-  CK(launch_stencil(c->g, c->op, kDelta, c->tmp0, c->y, c->sh_delta, c->partials, nullptr,
-                    kDotNone, c->stream));
+  if (c->fast)
+    CK(launch_stencil3(c->g, c->fo, kDelta, c->tmp0, nullptr, c->y, c->sh_delta, c->partials,
+                       nullptr, kDotNone, c->stream));
+  else
+    CK(launch_stencil(c->g, c->op, kDelta, c->tmp0, c->y, c->sh_delta, c->partials, nullptr,
+                      kDotNone, c->stream));
   return export_vec(c, c->y, y);
 }
 
@@ -405,8 +468,12 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
   };
   int rc = mark();
   if (rc) return rc;
-  CK(launch_stencil(c->g, c->op, kDelta, c->d, c->y, c->sh_delta, c->partials, c->st,
-                    kDotStep, c->stream));
+  if (c->fast)
+    CK(launch_stencil3(c->g, c->fo, kDelta, c->d, nullptr, c->y, c->sh_delta, c->partials, c->st,
+                       kDotStep, c->stream));
+  else
+    CK(launch_stencil(c->g, c->op, kDelta, c->d, c->y, c->sh_delta, c->partials, c->st,
+                      kDotStep, c->stream));
   if (names) names->push_back("delta");
   if ((rc = mark())) return rc;
   CK(launch_update(c->g, c->x, c->r, c->d, c->y, c->vblocks, c->partials, c->st, c->stream));
@@ -414,19 +481,9 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
   if ((rc = mark())) return rc;
   const double* qv = c->q;
   if (use_precond) {
-    // one event per sweep
-    for (int s = 0; s < c->S; ++s)
-      for (int l = 0; l < c->L; ++l) {
-        const bool last = (l == c->L - 1);
-        double* ob = last ? (s == c->S - 1 ? c->q : c->dl[s % 2]) : c->th[l % 2];
-        const double* tp = l > 0 ? c->th[(l - 1) % 2] : nullptr;
-        const double* dp = s > 0 ? c->dl[(s - 1) % 2] : nullptr;
-        const int dm = (last && s == c->S - 1) ? kDotStep : kDotNone;
-        CK(launch_sweep(c->g, c->op, l > 0, s > 0, c->r, tp, dp, ob, s > 0 ? c->sw_outer : c->sw,
-                        c->partials, c->st, dm, c->stream));
-        if (names) names->push_back("sweep_s" + std::to_string(s) + "_l" + std::to_string(l));
-        if ((rc = mark())) return rc;
-      }
+    rc = enqueue_precond(c, c->r, c->q, c->st, kDotStep, names,
+                         evs ? std::function<int()>(mark) : std::function<int()>());
+    if (rc) return rc;
   } else {
     CK(launch_dot(c->g, c->r, c->r, c->vblocks, c->partials, c->st, kDotStep, c->stream));
     if (names) names->push_back("dot");
@@ -439,7 +496,9 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
 }
 
 extern "C" int gq_launches_per_step(gq_ctx* c) {
-  return c ? (c->use_precond ? 3 + c->S * c->L : 4) : -1;
+  if (!c) return -1;
+  if (!c->use_precond) return 4;
+  return 3 + c->S * c->L + (c->fast ? c->S - 1 : 0);
 }
 
 extern "C" int gq_pcg_start(gq_ctx* c, const double* rhs, const double* x0, int32_t use_precond) {

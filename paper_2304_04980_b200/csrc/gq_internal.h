@@ -7,7 +7,7 @@
 
 namespace gq {
 
-enum StencilMode { kDelta = 0, kOuter = 1, kInner = 2 };
+enum StencilMode { kDelta = 0, kOuter = 1, kInner = 2, kOuterRhs = 3 };
 
 struct SetupErr {
   int code;        // 0 ok, 1 not SPD
@@ -50,6 +50,27 @@ cudaError_t launch_sweep(const Geo& g, const Ops& op, bool inner, bool outer, co
                          const double* theta, const double* delta, double* out,
                          const SweepShape& sh, double* partials, PcgState* st, int dotmode,
                          cudaStream_t s);
+
+// ---- pipelined fast-path kernels (gq_fast.cu) ----
+struct FastOps {
+  const double* oprow;   // [npc][N][K][23][n][n]  Psi(13) | Xi_0(5) | Xi_0'(5)
+  const double* omega;   // [npc][N][K][5][n][n]   cross-pair Psi blocks, sweep order
+  const double* fac3;    // [npc][V][nb][3][q][q]  G_k | L_k^-1 | H_k        (FMA sweep)
+  const int* psi_cls;
+  const double* fac4;    // [npc][V][nb][4][q][q]  L^-1 | -G | L^-T | -H      (DMMA sweep)
+};
+cudaError_t launch_build_fast(const Geo& g, int npc, const Ops& op, double* oprow, double* omega,
+                              double* fac3, double* fac4, cudaStream_t s);
+bool tc_supported(int n);
+// stencil modes kDelta (y = Delta x, optional y.x) and kOuterRhs (y = r + Xi~ x)
+cudaError_t launch_stencil3(const Geo& g, const FastOps& fo, int mode, const double* x,
+                            const double* rin, double* y, const StencilShape& sh,
+                            double* partials, PcgState* st, int dotmode, cudaStream_t s);
+cudaError_t launch_sweep3(const Geo& g, const FastOps& fo, bool inner, const double* rhs,
+                          const double* th, double* out, const double* rdot, int sm_count,
+                          double* partials, PcgState* st, int dotmode, cudaStream_t s);
+bool fast_supported(int n);
+long long fast_max_blocks(const Geo& g, const StencilShape& sh, int sm_count);
 
 // ---- vector kernels (gq_vec.cu) ----
 int vec_blocks(int sm_count);
