@@ -67,6 +67,8 @@ struct gq_ctx {
 };
 
 extern "C" const char* gq_last_error(void) { return g_err.c_str(); }
+namespace gq { int debug_read(long long* out, int n); }
+extern "C" int gq_debug_read(long long* out, int n) { return gq::debug_read(out, n); }
 extern "C" const char* gq_version(void) { return "gridlq_b200 0.1.0 (sm_100a, fp64)"; }
 
 static bool is_device_ptr(const void* p) {

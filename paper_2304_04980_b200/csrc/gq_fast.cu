@@ -131,6 +131,9 @@ __device__ __forceinline__ void st_rec_pol(double* p, const Vec<NS>& x, uint64_t
 __device__ __forceinline__ int first_lane(unsigned mask) { return mask ? __ffs(mask) - 1 : 0; }
 __device__ __forceinline__ int last_lane(unsigned mask) { return mask ? 31 - __clz(mask) : 0; }
 
+__device__ int g_exp = 0;       // experiment switches (bisecting performance; 0 = normal)
+__device__ long long g_dbg[1024];
+
 constexpr int kStencilP = 5;   // rows in flight per warp
 constexpr int kSweepP = 4;     // blocks in flight per warp
 
@@ -711,22 +714,23 @@ struct Sw4P {
   static constexpr int v = NS == 2 ? 6 : 3;   // blocks in flight per warp
 };
 
-template <int NS, bool INNER>
+template <int NS, bool INNER, int MT_ = 2>
 struct Sw4 {
+  static constexpr int MT = MT_;                     // M-tiles (8 chains each) per warp
   static constexpr int Q = 4 * NS, QQ = Q * Q, B2 = NS * NS;
   static constexpr int NT = Q / 8;                   // N-tiles == k-pairs
-  static constexpr int CH = 16;                      // chains per warp
-  static constexpr int REC = CH * NS;                // doubles per record (16 stages)
+  static constexpr int CH = 8 * MT;                  // chains per warp
+  static constexpr int REC = CH * NS;                // doubles per record (CH stages)
   static constexpr int NRF = INNER ? 16 : 4;         // forward: tau (4) + theta (12)
   static constexpr int NR = NRF > 8 ? NRF : 8;       // backward: w (4) + r (4)
   static constexpr int FAC = 2 * QQ;                 // per class: L|-G or L^T|-H
   static constexpr int OMG = INNER ? 4 * 5 * B2 : 0; // per class: omega rows of 4 nodes
   static constexpr int SLOT = NR * REC + 2 * FAC + 2 * OMG;
-  static constexpr int P = Sw4P<NS>::v;
+  static constexpr int P = NS == 2 ? (INNER ? (MT == 1 ? 4 : 6) : (MT == 1 ? 6 : 10)) : 3;
   static constexpr int R = P + 1;
 };
 
-// copy NREC records (16 stages x NS doubles, contiguous in the stage-inner layout) into
+// copy NREC records (16 stages x NS doubles, used by the v4 layout notes, contiguous in the stage-inner layout) into
 // consecutive smem records; src[r] == nullptr -> zero fill; stages >= nvalid zero-filled.
 template <int NS, int NREC>
 __device__ __forceinline__ void cp_records(double* dst, const double* const (&src)[NREC],
@@ -752,450 +756,120 @@ __device__ __forceinline__ void cp_records(double* dst, const double* const (&sr
   }
 }
 
-template <int NS, bool INNER>
-__global__ void __launch_bounds__(32) k_sweep4(Geo g, FastOps fo, const double* __restrict__ rhs,
-                                               const double* __restrict__ th, double* out,
-                                               const double* __restrict__ rdot, int n_items,
-                                               int nchunk, double* partials, PcgState* st,
-                                               int dotmode) {
-  using C = Sw4<NS, INNER>;
-  constexpr int Q = C::Q, QQ = C::QQ, B2 = C::B2, NT = C::NT, REC = C::REC;
-  extern __shared__ __align__(16) double smem[];
-  if (halted(st)) return;
-  const int lane = threadIdx.x & 31;
-  const int qd = lane & 3, rw = lane >> 2;
-  double* ring = smem;
-  const uint64_t pol = policy_evict_first();
-  const uint64_t pol_keep = policy_evict_last();
-  const long long rs = (long long)g.T1 * NS;
-  const long long cs = (long long)g.K * g.T1 * NS;
-  double dot = 0.0;
-
-#pragma unroll 1
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int v = item / nchunk, chunk = item % nchunk;
-    const int t0 = chunk * 16;
-    const int nvalid = min(16, g.T1 - t0);
-    // chain (stage) of this lane in M-tile m: t0 + 8m + rw
-    int cls[2];
-    bool tvm[2];
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int t = t0 + 8 * m + rw;
-      tvm[m] = t < g.T1;
-      cls[m] = tvm[m] ? fo.psi_cls[t] : -1;
-    }
-    const int cA = fo.psi_cls[t0];
-    const int cB = fo.psi_cls[t0 + nvalid - 1];
-    const bool two = cB != cA;
-    // per M-tile: classes present (warp-uniform)
-    bool tileA[2], tileB[2];
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      tileA[m] = __any_sync(0xffffffffu, cls[m] == cA);
-      tileB[m] = two && __any_sync(0xffffffffu, cls[m] == cB);
-    }
-    const int a = 2 * v;
-    const bool okb = a + 1 < g.N;
-    const long long col_a = (long long)a * g.K * g.T1 * NS + (long long)t0 * NS;
-    const double* FA = fo.fac4 + ((long long)cA * g.V + v) * g.nb * 4 * QQ;
-    const double* FB = fo.fac4 + ((long long)cB * g.V + v) * g.nb * 4 * QQ;
-    const double* OA = fo.omega + ((long long)cA * g.nk + (long long)a * g.K) * 5 * B2;
-    const double* OB = fo.omega + ((long long)cB * g.nk + (long long)a * g.K) * 5 * B2;
-    // features owned by this lane in N-tile h: 8h + 2qd + {0,1}
-    //   -> node slot nd(h) = (8h + 2qd) / NS, components c0(h) = (8h + 2qd) % NS
-    auto nd_of = [&](int h) { return (8 * h + 2 * qd) / NS; };
-    auto co_of = [&](int h) { return (8 * h + 2 * qd) % NS; };
-
-    // ---------------- forward ----------------
-    auto issue_f = [&](int k, double* sl) {
-      if (k < g.nb) {
-        const int i0 = 2 * k;
-        const bool ok1 = i0 + 1 < g.K;
-        const long long r0 = col_a + i0 * rs;
-        const double* src[C::NRF];
-        src[0] = rhs + r0;
-        src[1] = okb ? rhs + r0 + cs : nullptr;
-        src[2] = ok1 ? rhs + r0 + rs : nullptr;
-        src[3] = (ok1 && okb) ? rhs + r0 + rs + cs : nullptr;
-        if constexpr (INNER) {
-          const int tc[12] = {-2, -2, -1, -1, -1, -1, 2, 2, 2, 2, 3, 3};
-          const int tr[12] = {0, 1, -1, 0, 1, 2, -1, 0, 1, 2, 0, 1};
-#pragma unroll
-          for (int m = 0; m < 12; ++m) {
-            const int jj = a + tc[m], ii = i0 + tr[m];
-            src[4 + m] = (jj >= 0 && jj < g.N && ii >= 0 && ii < g.K)
-                             ? th + r0 + tc[m] * cs + tr[m] * rs : nullptr;
-          }
-        }
-        cp_records<NS, C::NRF>(sl, src, nvalid, lane, rhs, pol);
-        double* sf = sl + C::NR * REC;
-        warp_copy<NS>(sf, FA + (long long)k * 4 * QQ, 2 * QQ, true, lane, pol_keep);
-        if (two) warp_copy<NS>(sf + C::FAC, FB + (long long)k * 4 * QQ, 2 * QQ, true, lane, pol_keep);
-        if (INNER) {
-          double* so = sf + 2 * C::FAC;
-#pragma unroll
-          for (int s = 0; s < 4; ++s) {
-            const bool ok = (s & 1 ? okb : true) && (s >> 1 ? ok1 : true);
-            const long long off = ((long long)(s & 1) * g.K + i0 + (s >> 1)) * 5 * B2;
-            warp_copy<NS>(so + s * 5 * B2, ok ? OA + off : OA, 5 * B2, ok, lane, pol_keep);
-            if (two)
-              warp_copy<NS>(so + C::OMG + s * 5 * B2, ok ? OB + off : OB, 5 * B2, ok, lane, pol_keep);
-          }
-        }
-      }
-      cp_commit();
-    };
-    // running W_{k-1} fragments: [m][h] = 2 doubles
-    double wd[2][NT][2];
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int h = 0; h < NT; ++h) wd[m][h][0] = wd[m][h][1] = 0.0;
-    int sc = 0, si = 0;
-#pragma unroll 1
-    for (int p = 0; p < C::P; ++p) {
-      issue_f(p, ring + si * C::SLOT);
-      si = (si + 1 == C::R) ? 0 : si + 1;
-    }
-#pragma unroll 1
-    for (int k = 0; k < g.nb; ++k) {
-      issue_f(k + C::P, ring + si * C::SLOT);
-      si = (si + 1 == C::R) ? 0 : si + 1;
-      cp_wait<C::P>();
-      __syncwarp();
-      const double* sl = ring + sc * C::SLOT;
-      sc = (sc + 1 == C::R) ? 0 : sc + 1;
-      // tau pairs (A fragments of the rhs) per M-tile and k-pair
-      double bp[2][NT][2];
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int srow = 8 * m + rw;   // stage row inside the records
-#pragma unroll
-        for (int h = 0; h < NT; ++h) {
-          const double2 bv =
-              *reinterpret_cast<const double2*>(sl + nd_of(h) * REC + srow * NS + co_of(h));
-          bp[m][h][0] = bv.x;
-          bp[m][h][1] = bv.y;
-          if (INNER) {
-            // minus the cross-pair blocks (rows co, co+1 of node nd) times theta
-            const int nd = nd_of(h), ri = nd >> 1, col_odd = nd & 1;
-            const int sel = (cls[m] == cB && two) ? 1 : 0;
-            const double* om = sl + C::NR * REC + 2 * C::FAC + sel * C::OMG + nd * 5 * B2;
-            const int tix0[5] = {0, 2, 3, 4, 7};
-            const int tix1[5] = {3, 6, 7, 8, 10};
-            double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-            for (int u = 0; u < 5; ++u) {
-              const int ti = (col_odd ? tix1[u] : tix0[u]) + ri;
-              const double* tr = sl + (4 + ti) * REC + srow * NS;
-              const double* M = om + u * B2 + co_of(h) * NS;
-#pragma unroll
-              for (int c = 0; c < NS; ++c) {
-                s0 = fma(M[c], tr[c], s0);
-                s1 = fma(M[NS + c], tr[c], s1);
-              }
-            }
-            bp[m][h][0] -= s0;
-            bp[m][h][1] -= s1;
-          }
-        }
-      }
-      // D = tau^T L^T - W^T G^T, per class present in the tile
-      double dn[2][NT][2];
-#pragma unroll
-      for (int m = 0; m < 2; ++m)
-#pragma unroll
-        for (int h = 0; h < NT; ++h) dn[m][h][0] = dn[m][h][1] = 0.0;
-#pragma unroll
-      for (int pass = 0; pass < 2; ++pass) {
-        const double* L = sl + C::NR * REC + pass * C::FAC;
-        const double* Gm = L + QQ;
-        const int cx = pass ? cB : cA;
-#pragma unroll
-        for (int m = 0; m < 2; ++m) {
-          if (pass == 0 ? !tileA[m] : !tileB[m]) continue;
-          const bool on = cls[m] == cx;
-#pragma unroll
-          for (int h = 0; h < NT; ++h) {
-#pragma unroll
-            for (int sg = 0; sg < NT; ++sg) {
-              const double2 lb =
-                  *reinterpret_cast<const double2*>(L + (8 * h + rw) * Q + 8 * sg + 2 * qd);
-              const double2 gb =
-                  *reinterpret_cast<const double2*>(Gm + (8 * h + rw) * Q + 8 * sg + 2 * qd);
-              dmma(dn[m][h][0], dn[m][h][1], on ? bp[m][sg][0] : 0.0, lb.x);
-              dmma(dn[m][h][0], dn[m][h][1], on ? bp[m][sg][1] : 0.0, lb.y);
-              dmma(dn[m][h][0], dn[m][h][1], on ? wd[m][sg][0] : 0.0, gb.x);
-              dmma(dn[m][h][0], dn[m][h][1], on ? wd[m][sg][1] : 0.0, gb.y);
-            }
-          }
-        }
-      }
-      // park w_k (evict_last) and carry it
-      const long long r0 = col_a + 2 * k * rs;
-      const bool ok1 = 2 * k + 1 < g.K;
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-#pragma unroll
-        for (int h = 0; h < NT; ++h) {
-          wd[m][h][0] = dn[m][h][0];
-          wd[m][h][1] = dn[m][h][1];
-          const int nd = nd_of(h);
-          const bool ok = tvm[m] && (nd & 1 ? okb : true) && (nd >> 1 ? ok1 : true);
-          if (ok) {
-            double* p = out + r0 + (nd & 1) * cs + (nd >> 1) * rs + (8 * m + rw) * NS + co_of(h);
-            asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p),
-                         "d"(dn[m][h][0]), "d"(dn[m][h][1]), "l"(pol_keep)
-                         : "memory");
-          }
-        }
-      }
-      __syncwarp();
-    }
-    cp_wait<0>();
-    __threadfence();
-    __syncwarp();
-
-    // ---------------- backward ----------------
-    auto issue_b = [&](int k, double* sl) {
-      if (k >= 0) {
-        const bool ok1 = 2 * k + 1 < g.K;
-        const long long r0 = col_a + 2 * k * rs;
-        const double* src[8];
-        src[0] = out + r0;
-        src[1] = okb ? out + r0 + cs : nullptr;
-        src[2] = ok1 ? out + r0 + rs : nullptr;
-        src[3] = (ok1 && okb) ? out + r0 + rs + cs : nullptr;
-        const bool dm = dotmode != kDotNone;
-        src[4] = dm ? rdot + r0 : nullptr;
-        src[5] = dm && okb ? rdot + r0 + cs : nullptr;
-        src[6] = dm && ok1 ? rdot + r0 + rs : nullptr;
-        src[7] = dm && ok1 && okb ? rdot + r0 + rs + cs : nullptr;
-        cp_records<NS, 8>(sl, src, nvalid, lane, out, pol);
-        double* sf = sl + C::NR * REC;
-        warp_copy<NS>(sf, FA + (long long)k * 4 * QQ + 2 * QQ, 2 * QQ, true, lane, pol_keep);
-        if (two)
-          warp_copy<NS>(sf + C::FAC, FB + (long long)k * 4 * QQ + 2 * QQ, 2 * QQ, true, lane, pol_keep);
-      }
-      cp_commit();
-    };
-    double xd[2][NT][2];
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int h = 0; h < NT; ++h) xd[m][h][0] = xd[m][h][1] = 0.0;
-    sc = 0;
-    si = 0;
-#pragma unroll 1
-    for (int p = 0; p < C::P; ++p) {
-      issue_b(g.nb - 1 - p, ring + si * C::SLOT);
-      si = (si + 1 == C::R) ? 0 : si + 1;
-    }
-#pragma unroll 1
-    for (int k = g.nb - 1; k >= 0; --k) {
-      issue_b(k - C::P, ring + si * C::SLOT);
-      si = (si + 1 == C::R) ? 0 : si + 1;
-      cp_wait<C::P>();
-      __syncwarp();
-      const double* sl = ring + sc * C::SLOT;
-      sc = (sc + 1 == C::R) ? 0 : sc + 1;
-      double wp[2][NT][2];
-#pragma unroll
-      for (int m = 0; m < 2; ++m)
-#pragma unroll
-        for (int h = 0; h < NT; ++h) {
-          const double2 wv = *reinterpret_cast<const double2*>(
-              sl + nd_of(h) * REC + (8 * m + rw) * NS + co_of(h));
-          wp[m][h][0] = wv.x;
-          wp[m][h][1] = wv.y;
-        }
-      double dn[2][NT][2];
-#pragma unroll
-      for (int m = 0; m < 2; ++m)
-#pragma unroll
-        for (int h = 0; h < NT; ++h) dn[m][h][0] = dn[m][h][1] = 0.0;
-#pragma unroll
-      for (int pass = 0; pass < 2; ++pass) {
-        const double* LT = sl + C::NR * REC + pass * C::FAC;
-        const double* Hm = LT + QQ;
-        const int cx = pass ? cB : cA;
-#pragma unroll
-        for (int m = 0; m < 2; ++m) {
-          if (pass == 0 ? !tileA[m] : !tileB[m]) continue;
-          const bool on = cls[m] == cx;
-#pragma unroll
-          for (int h = 0; h < NT; ++h) {
-#pragma unroll
-            for (int sg = 0; sg < NT; ++sg) {
-              const double2 lb =
-                  *reinterpret_cast<const double2*>(LT + (8 * h + rw) * Q + 8 * sg + 2 * qd);
-              const double2 hb =
-                  *reinterpret_cast<const double2*>(Hm + (8 * h + rw) * Q + 8 * sg + 2 * qd);
-              dmma(dn[m][h][0], dn[m][h][1], on ? wp[m][sg][0] : 0.0, lb.x);
-              dmma(dn[m][h][0], dn[m][h][1], on ? wp[m][sg][1] : 0.0, lb.y);
-              dmma(dn[m][h][0], dn[m][h][1], on ? xd[m][sg][0] : 0.0, hb.x);
-              dmma(dn[m][h][0], dn[m][h][1], on ? xd[m][sg][1] : 0.0, hb.y);
-            }
-          }
-        }
-      }
-      const long long r0 = col_a + 2 * k * rs;
-      const bool ok1 = 2 * k + 1 < g.K;
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-#pragma unroll
-        for (int h = 0; h < NT; ++h) {
-          xd[m][h][0] = dn[m][h][0];
-          xd[m][h][1] = dn[m][h][1];
-          const int nd = nd_of(h);
-          const bool ok = tvm[m] && (nd & 1 ? okb : true) && (nd >> 1 ? ok1 : true);
-          if (ok) {
-            const long long off =
-                r0 + (nd & 1) * cs + (nd >> 1) * rs + (8 * m + rw) * NS + co_of(h);
-            *reinterpret_cast<double2*>(out + off) = make_double2(dn[m][h][0], dn[m][h][1]);
-            if (dotmode != kDotNone) {
-              const double2 rv = *reinterpret_cast<const double2*>(
-                  sl + (4 + nd) * REC + (8 * m + rw) * NS + co_of(h));
-              dot = fma(dn[m][h][0], rv.x, dot);
-              dot = fma(dn[m][h][1], rv.y, dot);
-            }
-          }
-        }
-      }
-      __syncwarp();
-    }
-    cp_wait<0>();
-    __syncwarp();
-  }
-  if (dotmode != kDotNone) {
-    double mu;
-    if (grid_reduce<false>(dot, partials, &st->counter[2], mu) && threadIdx.x == 0) {
-      if (dotmode == kDotInit) {
-        st->mu = mu;
-      } else {
-        st->beta = mu / st->mu;
-        st->mu = mu;
-      }
-    }
-  }
-}
-
-
-// ---- sweep v5: lean DMMA chain solver -----------------------------------------------------
-// Same math and fragment layout as v4 (see above), restructured for issue efficiency:
-//  * every address is computed once per item; per block only row offsets advance;
-//  * the Linv*tau products (independent of the recurrence) and the two G/H k-steps use
-//    separate accumulators, so one DMMA (~90-cycle latency) sits on the critical path;
-//  * tiles holding a single stage class (all but the t=0 tile of a time-invariant
-//    problem) skip the class masking entirely (TWO=false instantiation).
-
-template <int NS, bool INNER, bool TWO>
-__device__ __forceinline__ void sweep5_item(
+// ---- sweep v6: lean DMMA chain solver ------------------------------------------------------
+// Same math and fragment layout as described above, restructured for issue efficiency:
+//  * every address is computed once per item; per block only row offsets advance and only
+//    the first/last block (grid boundary rows) test validity;
+//  * the L*tau products and the two G/H k-steps use separate accumulators, so a single
+//    DMMA (~86-cycle latency) sits on the loop-carried path;
+//  * MT M-tiles (8 chains each) per warp: MT=1 lets two warps share an SMSP (a DMMA blocks
+//    its issuing warp ~17 cycles) while keeping the chains in flight, and so the parked
+//    forward iterates, inside L2;
+//  * tiles holding one stage class skip the class masking (TWO=false instantiation).
+template <int NS, bool INNER, int MT, bool TWO>
+__device__ __forceinline__ void sweep6_item(
     const Geo& g, const FastOps& fo, const double* __restrict__ rhs,
     const double* __restrict__ th, double* out, const double* __restrict__ rdot, int dotmode,
-    double* ring, int lane, int v, int t0, int nvalid, int cA, int cB, const int (&cls)[2],
-    const bool (&tvm)[2], uint64_t pol, uint64_t pol_keep, double& dot) {
-  using C = Sw4<NS, INNER>;
+    double* ring, int lane, int v, int t0, int nvalid, int cA, int cB, const int (&cls)[MT],
+    const bool (&tvm)[MT], uint64_t pol, uint64_t pol_keep, double& dot) {
+  using C = Sw4<NS, INNER, MT>;
   constexpr int Q = C::Q, QQ = C::QQ, B2 = C::B2, NT = C::NT, REC = C::REC, P = C::P, R = C::R;
+  constexpr int SLOT = C::SLOT, CH = C::CH;
+  constexpr int CPR = CH * NS / 2;                 // 16-byte chunks per record
+  constexpr int RPI = 32 / CPR;                    // records per warp instruction
   const int qd = lane & 3, rw = lane >> 2;
   const long long rs = (long long)g.T1 * NS;
   const long long cs = (long long)g.K * g.T1 * NS;
+  const long long rs2 = 2 * rs;
   const int a = 2 * v;
   const bool okb = a + 1 < g.N;
+  const int nb = g.nb;
   const long long col_a = (long long)a * g.K * g.T1 * NS + (long long)t0 * NS;
-  const double* FA = fo.fac4 + ((long long)cA * g.V + v) * g.nb * 4 * QQ;
-  const double* FB = fo.fac4 + ((long long)cB * g.V + v) * g.nb * 4 * QQ;
+  const double* FA = fo.fac4 + ((long long)cA * g.V + v) * nb * 4 * QQ;
+  const double* FB = fo.fac4 + ((long long)cB * g.V + v) * nb * 4 * QQ;
   const double* OA = fo.omega + ((long long)cA * g.nk + (long long)a * g.K) * 5 * B2;
   const double* OB = fo.omega + ((long long)cB * g.nk + (long long)a * g.K) * 5 * B2;
+  double* const ring_end = ring + R * SLOT;
 
-  // ---- record copy plan: chunk j of this lane -> (record, stage) ----
-  // NS == 2: 16 chunks/record, chunk j covers record 2j + (lane >> 4), stage lane & 15
-  // NS == 4: 32 chunks/record, chunk j covers record j, stage lane >> 1 (half lane & 1)
-  const int my_stage = NS == 2 ? (lane & 15) : (lane >> 1);
-  const int my_w = NS == 2 ? (lane & 15) : lane;          // chunk inside the record
-  const bool stage_ok = my_stage < nvalid;
-  // record geometry relative to (col a, row 2k): column offset, row offset
-  constexpr int NRF = C::NRF;
-  constexpr int JF = NRF * NS / 4;                          // chunks per lane, forward
-  auto rec_geo = [&](int r, int& dc, int& dr) {
-    const int base_c[4] = {0, 1, 0, 1}, base_r[4] = {0, 0, 1, 1};
-    const int tc[12] = {-2, -2, -1, -1, -1, -1, 2, 2, 2, 2, 3, 3};
-    const int tr[12] = {0, 1, -1, 0, 1, 2, -1, 0, 1, 2, 0, 1};
+  const int my_w = lane % CPR;
+  const bool stage_ok = my_w / (NS / 2) < nvalid;
+  constexpr int JF = C::NRF / RPI;
+  const double* fsrc[JF];
+  int fsz[JF], fdst[JF], frow[JF];
+#pragma unroll
+  for (int j = 0; j < JF; ++j) {
+    const int r = j * RPI + lane / CPR;
+    int dc, dr;
     if (r < 4) {
-      dc = base_c[r];
-      dr = base_r[r];
+      dc = r & 1;
+      dr = r >> 1;
     } else {
+      const int tc[12] = {-2, -2, -1, -1, -1, -1, 2, 2, 2, 2, 3, 3};
+      const int tr[12] = {0, 1, -1, 0, 1, 2, -1, 0, 1, 2, 0, 1};
       dc = tc[r - 4];
       dr = tr[r - 4];
     }
-  };
-  const double* fsrc[JF];
-  int frow[JF];
-  bool fcol[JF];
-  int fdst[JF];
-#pragma unroll
-  for (int j = 0; j < JF; ++j) {
-    const int r = NS == 2 ? 2 * j + (lane >> 4) : j;
-    int dc, dr;
-    rec_geo(r, dc, dr);
     const int jj = a + dc;
-    fcol[j] = stage_ok && jj >= 0 && jj < g.N;
+    const bool colok = stage_ok && jj >= 0 && jj < g.N;
+    fsz[j] = colok ? 16 : 0;
     frow[j] = dr;
-    fsrc[j] = (r < 4 ? rhs : th) + col_a + (long long)dc * cs + 2 * my_w;
+    fsrc[j] = colok ? (r < 4 ? rhs : th) + col_a + (long long)dc * cs + (long long)dr * rs + 2 * my_w
+                    : rhs;
     fdst[j] = r * REC + 2 * my_w;
   }
-  // factor / omega copy offsets (uniform data, 16-byte chunks)
-  constexpr int FCH = 2 * QQ / 2;          // chunks of the forward/backward factor pair
-  constexpr int OCH = 5 * B2 / 2;          // chunks of one node's omega rows
-
-  // ---- owned features: N-tile h -> node nd(h), component co(h) ----
-  int nd[NT], co[NT];
+  constexpr int FCH = QQ;                          // 16-byte chunks of one factor pair
+  constexpr int OCHN = 5 * B2 / 2;
+  constexpr int OCH = 4 * OCHN;
+  constexpr int OCU = (OCH + 31) / 32;
+  int odst[OCU], osz[OCU], orow[OCU], ooff[OCU];
 #pragma unroll
-  for (int h = 0; h < NT; ++h) {
-    nd[h] = (8 * h + 2 * qd) / NS;
-    co[h] = (8 * h + 2 * qd) % NS;
+  for (int u = 0; u < OCU; ++u) {
+    const int c = lane + 32 * u;
+    const int s = c / OCHN, w = c % OCHN;
+    const bool ok = INNER && c < OCH && ((s & 1) ? okb : true);
+    osz[u] = ok ? 16 : 0;
+    orow[u] = s >> 1;
+    ooff[u] = ok ? (((s & 1) * g.K + (s >> 1)) * 5 * B2 + 2 * w) : 0;
+    odst[u] = C::NR * REC + 2 * C::FAC + (c < OCH ? c : 0) * 2;
   }
-  // global offsets of owned pairs at block 0 (stage row 8m + rw)
-  long long own[2][NT];
-#pragma unroll
-  for (int m = 0; m < 2; ++m)
-#pragma unroll
-    for (int h = 0; h < NT; ++h)
-      own[m][h] = col_a + (nd[h] & 1) * cs + (nd[h] >> 1) * rs + (8 * m + rw) * NS + co[h];
-  bool own_col[NT];
-#pragma unroll
-  for (int h = 0; h < NT; ++h) own_col[h] = (nd[h] & 1) ? okb : true;
+  const long long odelta = 2LL * 5 * B2;
 
   auto issue_f = [&](int k, double* sl) {
-    if (k < g.nb) {
-      const long long roff = 2LL * k * rs;
+    if (k < nb) {
+      const long long roff = (long long)k * rs2;
+      const bool edge = (k == 0) || (k == nb - 1);
 #pragma unroll
       for (int j = 0; j < JF; ++j) {
-        const int row = 2 * k + frow[j];
-        const bool ok = fcol[j] && row >= 0 && row < g.K;
-        cpa16(sl + fdst[j], ok ? fsrc[j] + roff + (long long)frow[j] * rs : rhs, ok, pol);
+        int sz = (g_exp == 3) ? 0 : fsz[j];
+        if (edge) {
+          const int row = 2 * k + frow[j];
+          if (row < 0 || row >= g.K) sz = 0;
+        }
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(
+                         su32(sl + fdst[j])),
+                     "l"(sz ? fsrc[j] + roff : rhs), "r"(sz), "l"(pol)
+                     : "memory");
       }
-      double* sf = sl + C::NR * REC;
       const double* fa = FA + (long long)k * 4 * QQ;
+      if (g_exp != 8) {
 #pragma unroll
-      for (int c = lane; c < FCH; c += 32) cpa16(sf + 2 * c, fa + 2 * c, true, pol_keep);
+        for (int c = lane; c < FCH; c += 32) cpa16(sl + C::NR * REC + 2 * c, fa + 2 * c, true, pol_keep);
+      }
       if (TWO) {
         const double* fb = FB + (long long)k * 4 * QQ;
 #pragma unroll
-        for (int c = lane; c < FCH; c += 32) cpa16(sf + C::FAC + 2 * c, fb + 2 * c, true, pol_keep);
+        for (int c = lane; c < FCH; c += 32)
+          cpa16(sl + C::NR * REC + C::FAC + 2 * c, fb + 2 * c, true, pol_keep);
       }
       if (INNER) {
-        double* so = sf + 2 * C::FAC;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const int row = 2 * k + (s >> 1);
-          const bool ok = ((s & 1) ? okb : true) && row < g.K;
-          const long long off = ((long long)(s & 1) * g.K + row) * 5 * B2;
-#pragma unroll
-          for (int c = lane; c < OCH; c += 32) {
-            cpa16(so + s * 5 * B2 + 2 * c, ok ? OA + off + 2 * c : OA, ok, pol_keep);
-            if (TWO) cpa16(so + C::OMG + s * 5 * B2 + 2 * c, ok ? OB + off + 2 * c : OB, ok, pol_keep);
+        for (int u = 0; u < OCU; ++u) {
+          if (lane + 32 * u < OCH) {
+            int sz = osz[u];
+            if (edge && 2 * k + orow[u] >= g.K) sz = 0;
+            const long long o = sz ? ooff[u] + k * odelta : 0;
+            cpa16(sl + odst[u], OA + o, sz != 0, pol_keep);
+            if (TWO) cpa16(sl + odst[u] + C::OMG, OB + o, sz != 0, pol_keep);
           }
         }
       }
@@ -1203,51 +877,140 @@ __device__ __forceinline__ void sweep5_item(
     cp_commit();
   };
 
-  double wd[2][NT][2];
+  int nd[NT], co[NT];
 #pragma unroll
-  for (int m = 0; m < 2; ++m)
-#pragma unroll
-    for (int h = 0; h < NT; ++h) wd[m][h][0] = wd[m][h][1] = 0.0;
-  int sc = 0, si = 0;
-#pragma unroll 1
-  for (int p = 0; p < P; ++p) {
-    issue_f(p, ring + si * C::SLOT);
-    si = (si + 1 == R) ? 0 : si + 1;
+  for (int h = 0; h < NT; ++h) {
+    nd[h] = (8 * h + 2 * qd) / NS;
+    co[h] = (8 * h + 2 * qd) % NS;
   }
-#pragma unroll 1
-  for (int k = 0; k < g.nb; ++k) {
-    issue_f(k + P, ring + si * C::SLOT);
-    si = (si + 1 == R) ? 0 : si + 1;
-    cp_wait<P>();
-    __syncwarp();
-    const double* sl = ring + sc * C::SLOT;
-    sc = (sc + 1 == R) ? 0 : sc + 1;
-    const double* sf = sl + C::NR * REC;
-    // tau pairs
-    double bp[2][NT][2];
+  double* optr[MT][NT];
+  bool ostore[MT][NT], olast[MT][NT];
+  int bofs[MT][NT];
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int srow = 8 * m + rw;
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      optr[m][h] = out + col_a + (nd[h] & 1) * cs + (nd[h] >> 1) * rs + (8 * m + rw) * NS + co[h];
+      ostore[m][h] = tvm[m] && ((nd[h] & 1) ? okb : true);
+      olast[m][h] = (nd[h] >> 1) && (2 * (nb - 1) + 1 >= g.K);
+      bofs[m][h] = nd[h] * REC + (8 * m + rw) * NS + co[h];
+    }
+  int fofs[NT][NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h)
+#pragma unroll
+    for (int sg = 0; sg < NT; ++sg) fofs[h][sg] = (8 * h + rw) * Q + 8 * sg + 2 * qd;
+  int selm[MT];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) selm[m] = (TWO && cls[m] == cB) ? 1 : 0;
+
+  // DMMA halves of a block update (rows masked per class pass when TWO):
+  //   lmma: d = X0 L0 + X1 L1 (independent of the recurrence)
+  //   gmma: e = Y0 G0 + Y1 G1 (loop-carried through Y)
+  auto lmma = [&](const double* sf, const double (&xa)[MT][NT][2], double (&d)[MT][NT][2]) {
+    double d1[MT][NT][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+#pragma unroll
+        for (int z = 0; z < 2; ++z) d[m][h][z] = d1[m][h][z] = 0.0;
+    if (g_exp == 9) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int h = 0; h < NT; ++h)
+#pragma unroll
+          for (int z = 0; z < 2; ++z) d[m][h][z] = xa[m][h][z] * sf[0];
+      return;
+    }
+#pragma unroll
+    for (int pass = 0; pass < (TWO ? 2 : 1); ++pass) {
+      const double* L = sf + pass * C::FAC;
+      const int cx = pass ? cB : cA;
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+#pragma unroll
+        for (int sg = 0; sg < NT; ++sg) {
+          const double2 lb = *reinterpret_cast<const double2*>(L + fofs[h][sg]);
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const bool on = !TWO || cls[m] == cx;
+            dmma(d[m][h][0], d[m][h][1], on ? xa[m][sg][0] : 0.0, lb.x);
+            dmma(d1[m][h][0], d1[m][h][1], on ? xa[m][sg][1] : 0.0, lb.y);
+          }
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+#pragma unroll
+        for (int z = 0; z < 2; ++z) d[m][h][z] += d1[m][h][z];
+  };
+  // G fragments of one block (both classes when TWO)
+  auto gfrag = [&](const double* sf, double2 (&gb)[TWO ? 2 : 1][NT][NT]) {
+#pragma unroll
+    for (int pass = 0; pass < (TWO ? 2 : 1); ++pass)
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+#pragma unroll
+        for (int sg = 0; sg < NT; ++sg)
+          gb[pass][h][sg] = *reinterpret_cast<const double2*>(sf + pass * C::FAC + QQ + fofs[h][sg]);
+  };
+  auto gmma = [&](const double2 (&gb)[TWO ? 2 : 1][NT][NT], const double (&ya)[MT][NT][2],
+                  double (&e0)[MT][NT][2], double (&e1)[MT][NT][2]) {
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+#pragma unroll
+        for (int z = 0; z < 2; ++z) e0[m][h][z] = e1[m][h][z] = 0.0;
+#pragma unroll
+    for (int pass = 0; pass < (TWO ? 2 : 1); ++pass) {
+      const int cx = pass ? cB : cA;
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+#pragma unroll
+        for (int sg = 0; sg < NT; ++sg)
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const bool on = !TWO || cls[m] == cx;
+            dmma(e0[m][h][0], e0[m][h][1], on ? ya[m][sg][0] : 0.0, gb[pass][h][sg].x);
+            dmma(e1[m][h][0], e1[m][h][1], on ? ya[m][sg][1] : 0.0, gb[pass][h][sg].y);
+          }
+    }
+  };
+  // tau pairs of a forward slot (rhs minus Omega~ theta for inner sweeps)
+  auto load_tau = [&](const double* sl, double (&bp)[MT][NT][2]) {
+    const double* sf = sl + C::NR * REC;
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
 #pragma unroll
       for (int h = 0; h < NT; ++h) {
-        const double2 bv = *reinterpret_cast<const double2*>(sl + nd[h] * REC + srow * NS + co[h]);
+        const double2 bv = *reinterpret_cast<const double2*>(sl + bofs[m][h]);
         bp[m][h][0] = bv.x;
         bp[m][h][1] = bv.y;
-        if (INNER) {
-          const int ri = nd[h] >> 1;
-          const int sel = (TWO && cls[m] == cB) ? 1 : 0;
-          const double* om = sf + 2 * C::FAC + sel * C::OMG + nd[h] * 5 * B2 + co[h] * NS;
+      }
+    if (INNER) {
+#pragma unroll
+      for (int h = 0; h < NT; ++h) {
+        const int ri = nd[h] >> 1;
+        const bool odd = nd[h] & 1;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const double* om = sf + 2 * C::FAC + selm[m] * C::OMG + nd[h] * 5 * B2 + co[h] * NS;
           double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
           for (int u = 0; u < 5; ++u) {
-            const int tix = (nd[h] & 1) ? (u == 0 ? 3 : u == 1 ? 6 : u == 2 ? 7 : u == 3 ? 8 : 10)
-                                        : (u == 0 ? 0 : u == 1 ? 2 : u == 2 ? 3 : u == 3 ? 4 : 7);
-            const double* tr = sl + (4 + tix + ri) * REC + srow * NS;
+            const int tix = odd ? (u == 0 ? 3 : u == 1 ? 6 : u == 2 ? 7 : u == 3 ? 8 : 10)
+                                : (u == 0 ? 0 : u == 1 ? 2 : u == 2 ? 3 : u == 3 ? 4 : 7);
 #pragma unroll
             for (int c = 0; c < NS; c += 2) {
-              const double2 tv2 = *reinterpret_cast<const double2*>(tr + c);
               const double2 m0 = *reinterpret_cast<const double2*>(om + u * B2 + c);
               const double2 m1 = *reinterpret_cast<const double2*>(om + u * B2 + NS + c);
+              const double2 tv2 = *reinterpret_cast<const double2*>(
+                  sl + (4 + tix + ri) * REC + (8 * m + rw) * NS + c);
               s0 = fma(m0.x, tv2.x, s0);
               s2 = fma(m0.y, tv2.y, s2);
               s1 = fma(m1.x, tv2.x, s1);
@@ -1259,176 +1022,249 @@ __device__ __forceinline__ void sweep5_item(
         }
       }
     }
-    double dl[2][NT][2], dg0[2][NT][2], dg1[2][NT][2];
+  };
+
+  // ---------------- forward: w_k = L_k^-1 tau_k - G_k w_{k-1} ----------------
+  // software-pipelined by one block: the loop-carried G_k w_{k-1} DMMAs of block k overlap
+  // the fragment loads and L_{k+1} tau_{k+1} DMMAs of block k+1.
+  double wd[MT][NT][2];
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+  for (int m = 0; m < MT; ++m)
 #pragma unroll
-      for (int h = 0; h < NT; ++h)
-        dl[m][h][0] = dl[m][h][1] = dg0[m][h][0] = dg0[m][h][1] = dg1[m][h][0] = dg1[m][h][1] = 0.0;
+    for (int h = 0; h < NT; ++h) wd[m][h][0] = wd[m][h][1] = 0.0;
+  double* scp = ring;   // slot of the next block to consume
+  double* sip = ring;
+#pragma unroll 1
+  for (int p = 0; p < P; ++p) {
+    issue_f(p, sip);
+    sip += SLOT;
+    if (sip == ring_end) sip = ring;
+  }
+  double dl[MT][NT][2];
+  double2 gcur[TWO ? 2 : 1][NT][NT];
+  {
+    cp_wait<P - 1>();
+    __syncwarp();
+    double bp[MT][NT][2];
+    load_tau(scp, bp);
+    lmma(scp + C::NR * REC, bp, dl);
+    gfrag(scp + C::NR * REC, gcur);
+    scp += SLOT;
+    if (scp == ring_end) scp = ring;
+  }
+  const bool probe = (g_exp == 7) && lane == 0 && t0 == 8 * MT && v == 0 && !TWO;
+#pragma unroll 1
+  for (int k = 0; k < nb; ++k) {
+    long long c0 = clock64();
+    issue_f(k + P, sip);
+    sip += SLOT;
+    if (sip == ring_end) sip = ring;
+    long long c1 = clock64();
+    double e0[MT][NT][2], e1[MT][NT][2];
+    if (g_exp == 1 || g_exp == 9) {
 #pragma unroll
-    for (int pass = 0; pass < (TWO ? 2 : 1); ++pass) {
-      const double* L = sf + pass * C::FAC;
-      const double* Gm = L + QQ;
-      const int cx = pass ? cB : cA;
+      for (int m = 0; m < MT; ++m)
 #pragma unroll
-      for (int h = 0; h < NT; ++h) {
-#pragma unroll
-        for (int sg = 0; sg < NT; ++sg) {
-          const double2 lb = *reinterpret_cast<const double2*>(L + (8 * h + rw) * Q + 8 * sg + 2 * qd);
-          const double2 gb = *reinterpret_cast<const double2*>(Gm + (8 * h + rw) * Q + 8 * sg + 2 * qd);
-#pragma unroll
-          for (int m = 0; m < 2; ++m) {
-            const bool on = !TWO || cls[m] == cx;
-            dmma(dl[m][h][0], dl[m][h][1], on ? bp[m][sg][0] : 0.0, lb.x);
-            dmma(dl[m][h][0], dl[m][h][1], on ? bp[m][sg][1] : 0.0, lb.y);
-            dmma(dg0[m][h][0], dg0[m][h][1], on ? wd[m][sg][0] : 0.0, gb.x);
-            dmma(dg1[m][h][0], dg1[m][h][1], on ? wd[m][sg][1] : 0.0, gb.y);
-          }
-        }
-      }
+        for (int h = 0; h < NT; ++h) e0[m][h][0] = e0[m][h][1] = e1[m][h][0] = e1[m][h][1] = 0.0;
+    } else {
+      gmma(gcur, wd, e0, e1);
     }
-    const long long roff = 2LL * k * rs;
-    const bool ok1 = 2 * k + 1 < g.K;
+    double dln[MT][NT][2];
+    double2 gnext[TWO ? 2 : 1][NT][NT];
+    long long c2 = 0, c3 = 0;
+    if (k + 1 < nb) {
+      c2 = clock64();
+      cp_wait<P - 1>();
+      __syncwarp();
+      c3 = clock64();
+      double bp[MT][NT][2];
+      load_tau(scp, bp);
+      lmma(scp + C::NR * REC, bp, dln);
+      gfrag(scp + C::NR * REC, gnext);
+      scp += SLOT;
+      if (scp == ring_end) scp = ring;
+    }
+    if (probe && k < 200) {
+      g_dbg[4 * k + 0] = c1 - c0;
+      g_dbg[4 * k + 1] = c2 - c1;
+      g_dbg[4 * k + 2] = c3 - c2;
+      g_dbg[4 * k + 3] = clock64() - c3;
+    }
+    const bool lastk = k == nb - 1;
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+    for (int m = 0; m < MT; ++m)
 #pragma unroll
       for (int h = 0; h < NT; ++h) {
-        wd[m][h][0] = dl[m][h][0] + (dg0[m][h][0] + dg1[m][h][0]);
-        wd[m][h][1] = dl[m][h][1] + (dg0[m][h][1] + dg1[m][h][1]);
-        const bool ok = tvm[m] && own_col[h] && ((nd[h] >> 1) ? ok1 : true);
-        if (ok) {
-          double* p = out + own[m][h] + roff;
-          asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p),
-                       "d"(wd[m][h][0]), "d"(wd[m][h][1]), "l"(pol_keep)
-                       : "memory");
+        wd[m][h][0] = dl[m][h][0] + (e0[m][h][0] + e1[m][h][0]);
+        wd[m][h][1] = dl[m][h][1] + (e0[m][h][1] + e1[m][h][1]);
+        if (g_exp != 10 && ostore[m][h] && !(lastk && olast[m][h]) && g_exp != 4) {
+          if (g_exp == 5)
+            *reinterpret_cast<double2*>(optr[m][h] + k * rs2) = make_double2(wd[m][h][0], wd[m][h][1]);
+          else
+            asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(optr[m][h] + k * rs2),
+                         "d"(wd[m][h][0]), "d"(wd[m][h][1]), "l"(pol_keep)
+                         : "memory");
         }
       }
+    if (k + 1 < nb) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int h = 0; h < NT; ++h) {
+          dl[m][h][0] = dln[m][h][0];
+          dl[m][h][1] = dln[m][h][1];
+        }
+#pragma unroll
+      for (int pass = 0; pass < (TWO ? 2 : 1); ++pass)
+#pragma unroll
+        for (int h = 0; h < NT; ++h)
+#pragma unroll
+          for (int sg = 0; sg < NT; ++sg) gcur[pass][h][sg] = gnext[pass][h][sg];
+    }
     __syncwarp();
   }
   cp_wait<0>();
   __threadfence();
   __syncwarp();
+  if (g_exp == 2) return;
 
-  // ---------------- backward ----------------
-  constexpr int JB = 8 * NS / 4;             // w (4) + r (4) records
+  // ---------------- backward: x_k = L_k^-T w_k - H_k x_{k+1} ----------------
+  constexpr int JB = 8 / RPI;
   const double* bsrc[JB];
-  int brow[JB];
-  bool bcol[JB];
-  int bdst[JB];
+  int bsz[JB], bdst[JB], brow[JB];
 #pragma unroll
   for (int j = 0; j < JB; ++j) {
-    const int r = NS == 2 ? 2 * j + (lane >> 4) : j;
+    const int r = j * RPI + lane / CPR;
     const int dc = r & 1, dr = (r >> 1) & 1;
-    bcol[j] = stage_ok && (dc ? okb : true) && (r < 4 || dotmode != kDotNone);
+    const bool ok = stage_ok && (dc ? okb : true) && (r < 4 || dotmode != kDotNone);
+    bsz[j] = ok ? 16 : 0;
     brow[j] = dr;
-    bsrc[j] = (r < 4 ? (const double*)out : rdot) + col_a + (long long)dc * cs + 2 * my_w;
+    bsrc[j] = ok ? (r < 4 ? (const double*)out : rdot) + col_a + (long long)dc * cs +
+                       (long long)dr * rs + 2 * my_w
+                 : rhs;
     bdst[j] = r * REC + 2 * my_w;
   }
   auto issue_b = [&](int k, double* sl) {
     if (k >= 0) {
-      const long long roff = 2LL * k * rs;
+      const long long roff = (long long)k * rs2;
+      const bool edge = (k == nb - 1);
 #pragma unroll
       for (int j = 0; j < JB; ++j) {
-        const int row = 2 * k + brow[j];
-        const bool ok = bcol[j] && row < g.K;
-        cpa16(sl + bdst[j], ok ? bsrc[j] + roff + (long long)brow[j] * rs : rhs, ok, pol);
+        int sz = bsz[j];
+        if (edge && 2 * k + brow[j] >= g.K) sz = 0;
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(
+                         su32(sl + bdst[j])),
+                     "l"(sz ? bsrc[j] + roff : rhs), "r"(sz), "l"(pol)
+                     : "memory");
       }
-      double* sf = sl + C::NR * REC;
       const double* fa = FA + (long long)k * 4 * QQ + 2 * QQ;
 #pragma unroll
-      for (int c = lane; c < FCH; c += 32) cpa16(sf + 2 * c, fa + 2 * c, true, pol_keep);
+      for (int c = lane; c < FCH; c += 32) cpa16(sl + C::NR * REC + 2 * c, fa + 2 * c, true, pol_keep);
       if (TWO) {
         const double* fb = FB + (long long)k * 4 * QQ + 2 * QQ;
 #pragma unroll
-        for (int c = lane; c < FCH; c += 32) cpa16(sf + C::FAC + 2 * c, fb + 2 * c, true, pol_keep);
+        for (int c = lane; c < FCH; c += 32)
+          cpa16(sl + C::NR * REC + C::FAC + 2 * c, fb + 2 * c, true, pol_keep);
       }
     }
     cp_commit();
   };
-  double xd[2][NT][2];
+  auto load_w = [&](const double* sl, double (&wp)[MT][NT][2], double (&rp)[MT][NT][2]) {
 #pragma unroll
-  for (int m = 0; m < 2; ++m)
-#pragma unroll
-    for (int h = 0; h < NT; ++h) xd[m][h][0] = xd[m][h][1] = 0.0;
-  sc = 0;
-  si = 0;
-#pragma unroll 1
-  for (int p = 0; p < P; ++p) {
-    issue_b(g.nb - 1 - p, ring + si * C::SLOT);
-    si = (si + 1 == R) ? 0 : si + 1;
-  }
-#pragma unroll 1
-  for (int k = g.nb - 1; k >= 0; --k) {
-    issue_b(k - P, ring + si * C::SLOT);
-    si = (si + 1 == R) ? 0 : si + 1;
-    cp_wait<P>();
-    __syncwarp();
-    const double* sl = ring + sc * C::SLOT;
-    sc = (sc + 1 == R) ? 0 : sc + 1;
-    const double* sf = sl + C::NR * REC;
-    double wp[2][NT][2];
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
+    for (int m = 0; m < MT; ++m)
 #pragma unroll
       for (int h = 0; h < NT; ++h) {
-        const double2 wv = *reinterpret_cast<const double2*>(sl + nd[h] * REC + (8 * m + rw) * NS + co[h]);
+        const double2 wv = *reinterpret_cast<const double2*>(sl + bofs[m][h]);
         wp[m][h][0] = wv.x;
         wp[m][h][1] = wv.y;
+        const double2 rv = *reinterpret_cast<const double2*>(sl + 4 * REC + bofs[m][h]);
+        rp[m][h][0] = rv.x;
+        rp[m][h][1] = rv.y;
       }
-    double dl[2][NT][2], dg0[2][NT][2], dg1[2][NT][2];
+  };
+  double xd[MT][NT][2];
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+  for (int m = 0; m < MT; ++m)
 #pragma unroll
-      for (int h = 0; h < NT; ++h)
-        dl[m][h][0] = dl[m][h][1] = dg0[m][h][0] = dg0[m][h][1] = dg1[m][h][0] = dg1[m][h][1] = 0.0;
-#pragma unroll
-    for (int pass = 0; pass < (TWO ? 2 : 1); ++pass) {
-      const double* LT = sf + pass * C::FAC;
-      const double* Hm = LT + QQ;
-      const int cx = pass ? cB : cA;
-#pragma unroll
-      for (int h = 0; h < NT; ++h) {
-#pragma unroll
-        for (int sg = 0; sg < NT; ++sg) {
-          const double2 lb = *reinterpret_cast<const double2*>(LT + (8 * h + rw) * Q + 8 * sg + 2 * qd);
-          const double2 hb = *reinterpret_cast<const double2*>(Hm + (8 * h + rw) * Q + 8 * sg + 2 * qd);
-#pragma unroll
-          for (int m = 0; m < 2; ++m) {
-            const bool on = !TWO || cls[m] == cx;
-            dmma(dl[m][h][0], dl[m][h][1], on ? wp[m][sg][0] : 0.0, lb.x);
-            dmma(dl[m][h][0], dl[m][h][1], on ? wp[m][sg][1] : 0.0, lb.y);
-            dmma(dg0[m][h][0], dg0[m][h][1], on ? xd[m][sg][0] : 0.0, hb.x);
-            dmma(dg1[m][h][0], dg1[m][h][1], on ? xd[m][sg][1] : 0.0, hb.y);
-          }
-        }
-      }
+    for (int h = 0; h < NT; ++h) xd[m][h][0] = xd[m][h][1] = 0.0;
+  scp = ring;
+  sip = ring;
+#pragma unroll 1
+  for (int p = 0; p < P; ++p) {
+    issue_b(nb - 1 - p, sip);
+    sip += SLOT;
+    if (sip == ring_end) sip = ring;
+  }
+  double rcur[MT][NT][2];
+  {
+    cp_wait<P - 1>();
+    __syncwarp();
+    double wp[MT][NT][2];
+    load_w(scp, wp, rcur);
+    lmma(scp + C::NR * REC, wp, dl);
+    gfrag(scp + C::NR * REC, gcur);
+    scp += SLOT;
+    if (scp == ring_end) scp = ring;
+  }
+#pragma unroll 1
+  for (int k = nb - 1; k >= 0; --k) {
+    issue_b(k - P, sip);
+    sip += SLOT;
+    if (sip == ring_end) sip = ring;
+    double e0[MT][NT][2], e1[MT][NT][2];
+    gmma(gcur, xd, e0, e1);
+    double dln[MT][NT][2], rnext[MT][NT][2];
+    double2 gnext[TWO ? 2 : 1][NT][NT];
+    if (k > 0) {
+      cp_wait<P - 1>();
+      __syncwarp();
+      double wp[MT][NT][2];
+      load_w(scp, wp, rnext);
+      lmma(scp + C::NR * REC, wp, dln);
+      gfrag(scp + C::NR * REC, gnext);
+      scp += SLOT;
+      if (scp == ring_end) scp = ring;
     }
-    const long long roff = 2LL * k * rs;
-    const bool ok1 = 2 * k + 1 < g.K;
+    const bool lastk = k == nb - 1;
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+    for (int m = 0; m < MT; ++m)
 #pragma unroll
       for (int h = 0; h < NT; ++h) {
-        xd[m][h][0] = dl[m][h][0] + (dg0[m][h][0] + dg1[m][h][0]);
-        xd[m][h][1] = dl[m][h][1] + (dg0[m][h][1] + dg1[m][h][1]);
-        const bool ok = tvm[m] && own_col[h] && ((nd[h] >> 1) ? ok1 : true);
-        if (ok) {
-          *reinterpret_cast<double2*>(out + own[m][h] + roff) = make_double2(xd[m][h][0], xd[m][h][1]);
+        xd[m][h][0] = dl[m][h][0] + (e0[m][h][0] + e1[m][h][0]);
+        xd[m][h][1] = dl[m][h][1] + (e0[m][h][1] + e1[m][h][1]);
+        if (g_exp != 10 && ostore[m][h] && !(lastk && olast[m][h])) {
+          *reinterpret_cast<double2*>(optr[m][h] + k * rs2) = make_double2(xd[m][h][0], xd[m][h][1]);
           if (dotmode != kDotNone) {
-            const double2 rv = *reinterpret_cast<const double2*>(sl + (4 + nd[h]) * REC + (8 * m + rw) * NS + co[h]);
-            dot = fma(xd[m][h][0], rv.x, dot);
-            dot = fma(xd[m][h][1], rv.y, dot);
+            dot = fma(xd[m][h][0], rcur[m][h][0], dot);
+            dot = fma(xd[m][h][1], rcur[m][h][1], dot);
           }
         }
       }
+    if (k > 0) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int h = 0; h < NT; ++h)
+#pragma unroll
+          for (int z = 0; z < 2; ++z) {
+            dl[m][h][z] = dln[m][h][z];
+            rcur[m][h][z] = rnext[m][h][z];
+          }
+#pragma unroll
+      for (int pass = 0; pass < (TWO ? 2 : 1); ++pass)
+#pragma unroll
+        for (int h = 0; h < NT; ++h)
+#pragma unroll
+          for (int sg = 0; sg < NT; ++sg) gcur[pass][h][sg] = gnext[pass][h][sg];
+    }
     __syncwarp();
   }
   cp_wait<0>();
   __syncwarp();
 }
 
-template <int NS, bool INNER>
-__global__ void __launch_bounds__(32) k_sweep5(Geo g, FastOps fo, const double* __restrict__ rhs,
+template <int NS, bool INNER, int MT>
+__global__ void __launch_bounds__(32) k_sweep6(Geo g, FastOps fo, const double* __restrict__ rhs,
                                                const double* __restrict__ th, double* out,
                                                const double* __restrict__ rdot, int n_items,
                                                int nchunk, double* partials, PcgState* st,
@@ -1437,18 +1273,22 @@ __global__ void __launch_bounds__(32) k_sweep5(Geo g, FastOps fo, const double* 
   if (halted(st)) return;
   const int lane = threadIdx.x & 31;
   const int rw = lane >> 2;
-  const uint64_t pol = policy_evict_first();
-  const uint64_t pol_keep = policy_evict_last();
+  uint64_t pol = policy_evict_first();
+  uint64_t pol_keep = policy_evict_last();
+  if (g_exp == 6) {
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    pol_keep = pol;
+  }
   double dot = 0.0;
 #pragma unroll 1
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int v = item / nchunk, chunk = item % nchunk;
-    const int t0 = chunk * 16;
-    const int nvalid = min(16, g.T1 - t0);
-    int cls[2];
-    bool tvm[2];
+    const int t0 = chunk * 8 * MT;
+    const int nvalid = min(8 * MT, g.T1 - t0);
+    int cls[MT];
+    bool tvm[MT];
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
+    for (int m = 0; m < MT; ++m) {
       const int t = t0 + 8 * m + rw;
       tvm[m] = t < g.T1;
       cls[m] = tvm[m] ? fo.psi_cls[t] : -1;
@@ -1456,19 +1296,516 @@ __global__ void __launch_bounds__(32) k_sweep5(Geo g, FastOps fo, const double* 
     const int cA = fo.psi_cls[t0];
     const int cB = fo.psi_cls[t0 + nvalid - 1];
     if (cA == cB)
-      sweep5_item<NS, INNER, false>(g, fo, rhs, th, out, rdot, dotmode, smem, lane, v, t0, nvalid,
-                                    cA, cB, cls, tvm, pol, pol_keep, dot);
+      sweep6_item<NS, INNER, MT, false>(g, fo, rhs, th, out, rdot, dotmode, smem, lane, v, t0,
+                                        nvalid, cA, cB, cls, tvm, pol, pol_keep, dot);
     else
-      sweep5_item<NS, INNER, true>(g, fo, rhs, th, out, rdot, dotmode, smem, lane, v, t0, nvalid,
-                                   cA, cB, cls, tvm, pol, pol_keep, dot);
+      sweep6_item<NS, INNER, MT, true>(g, fo, rhs, th, out, rdot, dotmode, smem, lane, v, t0,
+                                       nvalid, cA, cB, cls, tvm, pol, pol_keep, dot);
   }
   if (dotmode != kDotNone) {
     double mu;
     if (grid_reduce<false>(dot, partials, &st->counter[2], mu) && threadIdx.x == 0) {
       if (dotmode == kDotInit) {
-        st->mu = mu;
+        st->mu = mu;                       // pcg.py:92
       } else {
-        st->beta = mu / st->mu;
+        st->beta = mu / st->mu;            // pcg.py:127-131
+        st->mu = mu;
+      }
+    }
+  }
+}
+
+
+// ---- TMA bulk-copy helpers --------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;\n" ::"r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(su32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// bounded wait: a protocol bug traps (launch error) instead of hanging the device
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  for (long long i = 0; !mbar_try(bar, parity); ++i)
+    if (i > (1LL << 28)) __trap();
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async;\n" ::: "memory");
+}
+
+// ---- sweep v8: CTA-cooperative, warp-specialised TMA pipeline ----------------------------
+// One CTA = one column pair x S = 8W consecutive stages (W consumer warps of 8 chains each,
+// plus one producer warp).  Per block the producer lane issues one cp.async.bulk per record
+// (S stages x n doubles of one node: ~1 KB contiguous in the stage-inner layout) and ONE
+// copy of the factor block (and omega rows) shared by all consumer warps, completing on a
+// per-slot `full` mbarrier; consumers release slots through an `empty` mbarrier.  This
+// replaces v6's per-lane cp.async, whose thousands of 16-byte requests clogged the LSU
+// (measured: ~660 cycles to issue 3 LDGSTS, ~800 cycles for the following LDS).
+template <int NS, bool INNER>
+struct Sw8 {
+  static constexpr int Q = 4 * NS, QQ = Q * Q, B2 = NS * NS, NT = Q / 8;
+  static constexpr int NRF = INNER ? 16 : 4;
+  static constexpr int NR = NRF > 8 ? NRF : 8;
+  static constexpr int FAC = 2 * QQ;
+  static constexpr int OMG = INNER ? Even<4 * 5 * B2>::v : 0;
+};
+
+struct Sw8Geo {
+  int W;        // consumer warps
+  int S;        // stages per item (8W)
+  int R;        // ring slots
+  int RECC;     // doubles per record (S * n)
+  int SLOT;     // doubles per slot
+  int nchunk;   // stage chunks per pair
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+
+template <int NS, bool INNER, bool TWOW>
+__device__ __forceinline__ void sweep8_warp_item(
+    const Geo& g, const Sw8Geo& sg, double* out, int dotmode, double* ring, uint64_t* full,
+    uint64_t* empty, const double* zrec, uint32_t& nuse, int lane, int wid, int v, int t0,
+    int cA, int cB, int fsel, const int cls, const bool tvr, uint64_t pol_keep, double& dot) {
+  using C = Sw8<NS, INNER>;
+  constexpr int Q = C::Q, QQ = C::QQ, B2 = C::B2, NT = C::NT;
+  const int qd = lane & 3, rw = lane >> 2;
+  const int RECC = sg.RECC, SLOT = sg.SLOT, R = sg.R;
+  const long long rs = (long long)g.T1 * NS;
+  const long long cs = (long long)g.K * g.T1 * NS;
+  const long long rs2 = 2 * rs;
+  const int a = 2 * v;
+  const bool okb = a + 1 < g.N;
+  const int nb = g.nb;
+  const int srow = 8 * wid + rw;                   // this lane's stage row inside records
+  const long long col_a = (long long)a * g.K * g.T1 * NS + (long long)(t0 + srow) * NS;
+  const int tr[12] = {0, 1, -1, 0, 1, 2, -1, 0, 1, 2, 0, 1};
+  const int tc[12] = {-2, -2, -1, -1, -1, -1, 2, 2, 2, 2, 3, 3};
+  int nd[NT], co[NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) {
+    nd[h] = (8 * h + 2 * qd) / NS;
+    co[h] = (8 * h + 2 * qd) % NS;
+  }
+  double* optr[NT];
+  bool ostore[NT];
+  int bofs[NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) {
+    optr[h] = out + col_a + (nd[h] & 1) * cs + (nd[h] >> 1) * rs + co[h];
+    ostore[h] = tvr && ((nd[h] & 1) ? okb : true);
+    bofs[h] = nd[h] * RECC + srow * NS + co[h];
+  }
+  int fofs[NT][NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h)
+#pragma unroll
+    for (int s2 = 0; s2 < NT; ++s2) fofs[h][s2] = (8 * h + rw) * Q + 8 * s2 + 2 * qd;
+  const int osel = TWOW ? (cls == cB ? 1 : 0) : fsel;
+  auto node_ok = [&](int ndv, int k) {
+    return ((ndv & 1) ? okb : true) && (2 * k + (ndv >> 1) < g.K);
+  };
+  auto acquire = [&]() -> double* {
+    const uint32_t s = nuse % R, par = (nuse / R) & 1;
+    const long long c0 = clock64();
+    mbar_wait(full + s, par);
+    if (g_exp == 7 && blockIdx.x == 0 && wid == 0 && lane == 0 && nuse < 200)
+      g_dbg[4 * nuse + 1] = clock64() - c0, g_dbg[4 * nuse + 2] = c0;
+    ++nuse;
+    return ring + (size_t)s * SLOT;
+  };
+  // slot reads done -> producer may refill it (the empty-barrier arrive orders our generic
+  // reads before the async-proxy overwrite; no proxy fence is needed for read -> write)
+  auto release = [&](const double* sl) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + (sl - ring) / SLOT);
+  };
+  auto lmma = [&](const double* sf, const double (&xa)[NT][2], double (&d)[NT][2]) {
+    double d1[NT][2];
+#pragma unroll
+    for (int h = 0; h < NT; ++h) d[h][0] = d[h][1] = d1[h][0] = d1[h][1] = 0.0;
+#pragma unroll
+    for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass) {
+      const double* L = sf + (TWOW ? pass : fsel) * C::FAC;
+      const bool on = !TWOW || cls == (pass ? cB : cA);
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+#pragma unroll
+        for (int s2 = 0; s2 < NT; ++s2) {
+          const double2 lb = *reinterpret_cast<const double2*>(L + fofs[h][s2]);
+          dmma(d[h][0], d[h][1], on ? xa[s2][0] : 0.0, lb.x);
+          dmma(d1[h][0], d1[h][1], on ? xa[s2][1] : 0.0, lb.y);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      d[h][0] += d1[h][0];
+      d[h][1] += d1[h][1];
+    }
+  };
+  auto gfrag = [&](const double* sf, double2 (&gb)[TWOW ? 2 : 1][NT][NT]) {
+#pragma unroll
+    for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass)
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+#pragma unroll
+        for (int s2 = 0; s2 < NT; ++s2)
+          gb[pass][h][s2] = *reinterpret_cast<const double2*>(
+              sf + (TWOW ? pass : fsel) * C::FAC + QQ + fofs[h][s2]);
+  };
+  auto gmma = [&](const double2 (&gb)[TWOW ? 2 : 1][NT][NT], const double (&ya)[NT][2],
+                  double (&e0)[NT][2], double (&e1)[NT][2]) {
+#pragma unroll
+    for (int h = 0; h < NT; ++h) e0[h][0] = e0[h][1] = e1[h][0] = e1[h][1] = 0.0;
+#pragma unroll
+    for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass) {
+      const bool on = !TWOW || cls == (pass ? cB : cA);
+#pragma unroll
+      for (int h = 0; h < NT; ++h)
+#pragma unroll
+        for (int s2 = 0; s2 < NT; ++s2) {
+          dmma(e0[h][0], e0[h][1], on ? ya[s2][0] : 0.0, gb[pass][h][s2].x);
+          dmma(e1[h][0], e1[h][1], on ? ya[s2][1] : 0.0, gb[pass][h][s2].y);
+        }
+    }
+  };
+  auto load_tau = [&](const double* sl, int k, double (&bp)[NT][2]) {
+    const double* sf = sl + C::NR * RECC;
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      const double2 bv =
+          *reinterpret_cast<const double2*>((node_ok(nd[h], k) ? sl : zrec) + bofs[h]);
+      bp[h][0] = bv.x;
+      bp[h][1] = bv.y;
+    }
+    if (INNER) {
+#pragma unroll
+      for (int h = 0; h < NT; ++h) {
+        const int ri = nd[h] >> 1;
+        const bool odd = nd[h] & 1;
+        const int opos = (nd[h] & 1) * 2 + (nd[h] >> 1);
+        const double* om = sf + 2 * C::FAC + osel * C::OMG + opos * 5 * B2 + co[h] * NS;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int u = 0; u < 5; ++u) {
+          const int tix = (odd ? (u == 0 ? 3 : u == 1 ? 6 : u == 2 ? 7 : u == 3 ? 8 : 10)
+                               : (u == 0 ? 0 : u == 1 ? 2 : u == 2 ? 3 : u == 3 ? 4 : 7)) + ri;
+          const int ii = 2 * k + tr[tix];
+          const int jj = a + tc[tix];
+          const bool tok = jj >= 0 && jj < g.N && ii >= 0 && ii < g.K;
+          const double* trow = (tok ? sl + (4 + tix) * RECC : zrec) + srow * NS;
+#pragma unroll
+          for (int c = 0; c < NS; c += 2) {
+            const double2 m0 = *reinterpret_cast<const double2*>(om + u * B2 + c);
+            const double2 m1 = *reinterpret_cast<const double2*>(om + u * B2 + NS + c);
+            const double2 tv2 = *reinterpret_cast<const double2*>(trow + c);
+            s0 = fma(m0.x, tv2.x, s0);
+            s2 = fma(m0.y, tv2.y, s2);
+            s1 = fma(m1.x, tv2.x, s1);
+            s3 = fma(m1.y, tv2.y, s3);
+          }
+        }
+        bp[h][0] -= s0 + s2;
+        bp[h][1] -= s1 + s3;
+      }
+    }
+  };
+
+  // ---------------- forward ----------------
+  double wd[NT][2];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) wd[h][0] = wd[h][1] = 0.0;
+  double dl[NT][2];
+  double2 gcur[TWOW ? 2 : 1][NT][NT];
+  {
+    const double* sl = acquire();
+    double bp[NT][2];
+    load_tau(sl, 0, bp);
+    lmma(sl + C::NR * RECC, bp, dl);
+    gfrag(sl + C::NR * RECC, gcur);
+    release(sl);
+  }
+#pragma unroll 1
+  for (int k = 0; k < nb; ++k) {
+    double e0[NT][2], e1[NT][2];
+    gmma(gcur, wd, e0, e1);
+    double dln[NT][2];
+    double2 gnext[TWOW ? 2 : 1][NT][NT];
+    if (k + 1 < nb) {
+      const double* sl = acquire();
+      double bp[NT][2];
+      load_tau(sl, k + 1, bp);
+      lmma(sl + C::NR * RECC, bp, dln);
+      gfrag(sl + C::NR * RECC, gnext);
+      release(sl);
+    }
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      wd[h][0] = dl[h][0] + (e0[h][0] + e1[h][0]);
+      wd[h][1] = dl[h][1] + (e0[h][1] + e1[h][1]);
+      if (ostore[h] && 2 * k + (nd[h] >> 1) < g.K)
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(optr[h] + k * rs2),
+                     "d"(wd[h][0]), "d"(wd[h][1]), "l"(pol_keep)
+                     : "memory");
+    }
+    if (k + 1 < nb) {
+#pragma unroll
+      for (int h = 0; h < NT; ++h) {
+        dl[h][0] = dln[h][0];
+        dl[h][1] = dln[h][1];
+      }
+#pragma unroll
+      for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass)
+#pragma unroll
+        for (int h = 0; h < NT; ++h)
+#pragma unroll
+          for (int s2 = 0; s2 < NT; ++s2) gcur[pass][h][s2] = gnext[pass][h][s2];
+    }
+  }
+  // w stores visible to the producer's bulk reads of the backward sweep
+  __threadfence();
+  fence_proxy_async();
+  asm volatile("barrier.sync 1, %0;\n" ::"r"(32 * (sg.W + 1)) : "memory");
+
+  // ---------------- backward ----------------
+  const bool dm = dotmode != kDotNone;
+  auto load_w = [&](const double* sl, int k, double (&wp)[NT][2], double (&rp)[NT][2]) {
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      const double* base = node_ok(nd[h], k) ? sl : zrec;
+      const double2 wv = *reinterpret_cast<const double2*>(base + bofs[h]);
+      wp[h][0] = wv.x;
+      wp[h][1] = wv.y;
+      const double2 rv = dm ? *reinterpret_cast<const double2*>(base + 4 * RECC + bofs[h])
+                            : make_double2(0.0, 0.0);
+      rp[h][0] = rv.x;
+      rp[h][1] = rv.y;
+    }
+  };
+  double xd[NT][2];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) xd[h][0] = xd[h][1] = 0.0;
+  double rcur[NT][2];
+  {
+    const double* sl = acquire();
+    double wp[NT][2];
+    load_w(sl, nb - 1, wp, rcur);
+    lmma(sl + C::NR * RECC, wp, dl);
+    gfrag(sl + C::NR * RECC, gcur);
+    release(sl);
+  }
+#pragma unroll 1
+  for (int k = nb - 1; k >= 0; --k) {
+    double e0[NT][2], e1[NT][2];
+    gmma(gcur, xd, e0, e1);
+    double dln[NT][2], rnext[NT][2];
+    double2 gnext[TWOW ? 2 : 1][NT][NT];
+    if (k > 0) {
+      const double* sl = acquire();
+      double wp[NT][2];
+      load_w(sl, k - 1, wp, rnext);
+      lmma(sl + C::NR * RECC, wp, dln);
+      gfrag(sl + C::NR * RECC, gnext);
+      release(sl);
+    }
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      xd[h][0] = dl[h][0] + (e0[h][0] + e1[h][0]);
+      xd[h][1] = dl[h][1] + (e0[h][1] + e1[h][1]);
+      if (ostore[h] && 2 * k + (nd[h] >> 1) < g.K) {
+        *reinterpret_cast<double2*>(optr[h] + k * rs2) = make_double2(xd[h][0], xd[h][1]);
+        if (dm) {
+          dot = fma(xd[h][0], rcur[h][0], dot);
+          dot = fma(xd[h][1], rcur[h][1], dot);
+        }
+      }
+    }
+    if (k > 0) {
+#pragma unroll
+      for (int h = 0; h < NT; ++h) {
+        dl[h][0] = dln[h][0];
+        dl[h][1] = dln[h][1];
+        rcur[h][0] = rnext[h][0];
+        rcur[h][1] = rnext[h][1];
+      }
+#pragma unroll
+      for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass)
+#pragma unroll
+        for (int h = 0; h < NT; ++h)
+#pragma unroll
+          for (int s2 = 0; s2 < NT; ++s2) gcur[pass][h][s2] = gnext[pass][h][s2];
+    }
+  }
+}
+
+template <int NS, bool INNER>
+__global__ void __launch_bounds__(288) k_sweep8(Geo g, FastOps fo, Sw8Geo sg,
+                                                const double* __restrict__ rhs,
+                                                const double* __restrict__ th, double* out,
+                                                const double* __restrict__ rdot, int n_items,
+                                                double* partials, PcgState* st, int dotmode) {
+  using C = Sw8<NS, INNER>;
+  constexpr int QQ = C::QQ, B2 = C::B2;
+  extern __shared__ __align__(16) double smem[];
+  if (halted(st)) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int R = sg.R, SLOT = sg.SLOT, RECC = sg.RECC, S = sg.S;
+  double* ring = smem;
+  double* zrec = smem + (size_t)R * SLOT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(zrec + (size_t)C::NR * RECC);
+  uint64_t* empty = full + R;
+  for (int e = threadIdx.x; e < C::NR * RECC; e += blockDim.x) zrec[e] = 0.0;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < R; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, sg.W);
+    }
+  fence_proxy_async();
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+  const long long rs = (long long)g.T1 * NS;
+  const long long cs = (long long)g.K * g.T1 * NS;
+  double dot = 0.0;
+  const bool producer = wid == sg.W;
+  uint32_t nfill = 0, nuse = 0;
+#pragma unroll 1
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int v = item / sg.nchunk, chunk = item % sg.nchunk;
+    const int t0 = chunk * S;
+    const int nvalid = min(S, g.T1 - t0);
+    const int cA = fo.psi_cls[t0];
+    const int cB = fo.psi_cls[t0 + nvalid - 1];
+    const bool two = cA != cB;
+    const int a = 2 * v;
+    const bool okb = a + 1 < g.N;
+    const long long col_a = (long long)a * g.K * g.T1 * NS + (long long)t0 * NS;
+    if (producer) {
+      if (lane == 0) {
+        const uint32_t rec_bytes = (uint32_t)nvalid * NS * 8;
+        const double* FA = fo.fac4 + ((long long)cA * g.V + v) * g.nb * 4 * QQ;
+        const double* FB = fo.fac4 + ((long long)cB * g.V + v) * g.nb * 4 * QQ;
+        const double* OA = fo.omega + ((long long)cA * g.nk + (long long)a * g.K) * 5 * B2;
+        const double* OB = fo.omega + ((long long)cB * g.nk + (long long)a * g.K) * 5 * B2;
+        const int tr[12] = {0, 1, -1, 0, 1, 2, -1, 0, 1, 2, 0, 1};
+        const int tc[12] = {-2, -2, -1, -1, -1, -1, 2, 2, 2, 2, 3, 3};
+        auto slot_for_fill = [&](uint32_t& bytes_bar_slot) -> double* {
+          const uint32_t s = nfill % R, u = nfill / R;
+          const long long c0 = clock64();
+          if (u >= 1) mbar_wait(empty + s, (u - 1) & 1);
+          if (g_exp == 7 && blockIdx.x == 0 && nfill < 200) g_dbg[4 * nfill + 0] = clock64() - c0;
+          ++nfill;
+          bytes_bar_slot = s;
+          return ring + (size_t)s * SLOT;
+        };
+        for (int k = 0; k < g.nb; ++k) {
+          uint32_t s;
+          double* sl = slot_for_fill(s);
+          uint64_t* bar = full + s;
+          const int i0 = 2 * k;
+          const bool ok1 = i0 + 1 < g.K;
+          const bool tv[4] = {true, okb, ok1, ok1 && okb};
+          bool thv[12];
+          uint32_t bytes = 2 * QQ * 8 * (two ? 2 : 1);
+          for (int r = 0; r < 4; ++r) bytes += tv[r] ? rec_bytes : 0;
+          if (INNER) {
+            for (int m = 0; m < 12; ++m) {
+              const int ii = i0 + tr[m], jj = a + tc[m];
+              thv[m] = jj >= 0 && jj < g.N && ii >= 0 && ii < g.K;
+              bytes += thv[m] ? rec_bytes : 0;
+            }
+            bytes += (uint32_t)((ok1 ? 2 : 1) * 5 * B2 * 8) * (okb ? 2 : 1) * (two ? 2 : 1);
+          }
+          mbar_expect_tx(bar, bytes);
+          const long long r0 = col_a + i0 * rs;
+          for (int r = 0; r < 4; ++r)
+            if (tv[r]) bulk_g2s(sl + r * RECC, rhs + r0 + (r & 1) * cs + (r >> 1) * rs, rec_bytes, bar, pol);
+          if (INNER)
+            for (int m = 0; m < 12; ++m)
+              if (thv[m]) bulk_g2s(sl + (4 + m) * RECC, th + r0 + tc[m] * cs + tr[m] * rs, rec_bytes, bar, pol);
+          double* sf = sl + C::NR * RECC;
+          bulk_g2s(sf, FA + (long long)k * 4 * QQ, 2 * QQ * 8, bar, pol_keep);
+          if (two) bulk_g2s(sf + C::FAC, FB + (long long)k * 4 * QQ, 2 * QQ * 8, bar, pol_keep);
+          if (INNER) {
+            double* so = sf + 2 * C::FAC;
+            const uint32_t ob = (uint32_t)((ok1 ? 2 : 1) * 5 * B2 * 8);
+            bulk_g2s(so, OA + (long long)i0 * 5 * B2, ob, bar, pol_keep);
+            if (okb) bulk_g2s(so + 2 * 5 * B2, OA + ((long long)g.K + i0) * 5 * B2, ob, bar, pol_keep);
+            if (two) {
+              bulk_g2s(so + C::OMG, OB + (long long)i0 * 5 * B2, ob, bar, pol_keep);
+              if (okb) bulk_g2s(so + C::OMG + 2 * 5 * B2, OB + ((long long)g.K + i0) * 5 * B2, ob, bar, pol_keep);
+            }
+          }
+        }
+        asm volatile("barrier.sync 1, %0;\n" ::"r"(32 * (sg.W + 1)) : "memory");
+        fence_proxy_async();
+        const bool dm = dotmode != kDotNone;
+        for (int k = g.nb - 1; k >= 0; --k) {
+          uint32_t s;
+          double* sl = slot_for_fill(s);
+          uint64_t* bar = full + s;
+          const bool ok1 = 2 * k + 1 < g.K;
+          const bool tv[4] = {true, okb, ok1, ok1 && okb};
+          uint32_t bytes = 2 * QQ * 8 * (two ? 2 : 1);
+          for (int r = 0; r < 4; ++r) bytes += tv[r] ? rec_bytes * (dm ? 2 : 1) : 0;
+          mbar_expect_tx(bar, bytes);
+          const long long r0 = col_a + 2 * k * rs;
+          for (int r = 0; r < 4; ++r)
+            if (tv[r]) {
+              const long long off = r0 + (r & 1) * cs + (r >> 1) * rs;
+              bulk_g2s(sl + r * RECC, out + off, rec_bytes, bar, pol);
+              if (dm) bulk_g2s(sl + (4 + r) * RECC, rdot + off, rec_bytes, bar, pol);
+            }
+          double* sf = sl + C::NR * RECC;
+          bulk_g2s(sf, FA + (long long)k * 4 * QQ + 2 * QQ, 2 * QQ * 8, bar, pol_keep);
+          if (two) bulk_g2s(sf + C::FAC, FB + (long long)k * 4 * QQ + 2 * QQ, 2 * QQ * 8, bar, pol_keep);
+        }
+      } else {
+        asm volatile("barrier.sync 1, %0;\n" ::"r"(32 * (sg.W + 1)) : "memory");
+      }
+    } else {
+      const int t = t0 + 8 * wid + (lane >> 2);
+      const bool tvr = t < g.T1;
+      const int cls = tvr ? fo.psi_cls[t] : -1;
+      const int wfirst = fo.psi_cls[min(t0 + 8 * wid, g.T1 - 1)];
+      const int wlast = fo.psi_cls[min(t0 + 8 * wid + 7, g.T1 - 1)];
+      const bool twow = two && wfirst != wlast;
+      const int fsel = (two && wfirst == cB) ? 1 : 0;
+      if (twow)
+        sweep8_warp_item<NS, INNER, true>(g, sg, out, dotmode, ring, full, empty, zrec, nuse, lane,
+                                          wid, v, t0, cA, cB, fsel, cls, tvr, pol_keep, dot);
+      else
+        sweep8_warp_item<NS, INNER, false>(g, sg, out, dotmode, ring, full, empty, zrec, nuse, lane,
+                                           wid, v, t0, cA, cB, fsel, cls, tvr, pol_keep, dot);
+    }
+  }
+  if (dotmode != kDotNone) {
+    double mu;
+    if (grid_reduce<false>(dot, partials, &st->counter[2], mu) && threadIdx.x == 0) {
+      if (dotmode == kDotInit) {
+        st->mu = mu;                       // pcg.py:92
+      } else {
+        st->beta = mu / st->mu;            // pcg.py:127-131
         st->mu = mu;
       }
     }
@@ -1609,38 +1946,89 @@ static cudaError_t sweep3_n(const Geo& g, const FastOps& fo, bool inner, const d
   return cudaGetLastError();
 }
 
+template <int NS, bool INNER, int MT>
+static constexpr size_t sw6_warp_bytes() {
+  return (size_t)Sw4<NS, INNER, MT>::R * Sw4<NS, INNER, MT>::SLOT * sizeof(double);
+}
+
+template <int NS, bool INNER, int MT>
+static cudaError_t sweep6_launch(const Geo& g, const FastOps& fo, const double* rhs,
+                                 const double* th, double* out, const double* rdot, int sm_count,
+                                 double* partials, PcgState* st, int dotmode, cudaStream_t s,
+                                 int wsm) {
+  const int nchunk = (g.T1 + 8 * MT - 1) / (8 * MT);
+  const int n_items = g.V * nchunk;
+  const int want = std::min(n_items, std::max(1, wsm) * sm_count);
+  constexpr size_t per = sw6_warp_bytes<NS, INNER, MT>();
+  cudaError_t e = cudaFuncSetAttribute(k_sweep6<NS, INNER, MT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per);
+  if (e != cudaSuccess) return e;
+  const unsigned blocks = resident_blocks(k_sweep6<NS, INNER, MT>, per, want, sm_count);
+  k_sweep6<NS, INNER, MT><<<blocks, 32, per, s>>>(g, fo, rhs, th, out, rdot, n_items, nchunk,
+                                                  partials, st, dotmode);
+  return cudaGetLastError();
+
+}
+
 template <int NS, bool INNER>
-static constexpr size_t sw4_warp_bytes() {
-  return (size_t)Sw4<NS, INNER>::R * Sw4<NS, INNER>::SLOT * sizeof(double);
+static cudaError_t sweep8_launch(const Geo& g, const FastOps& fo, const double* rhs,
+                                 const double* th, double* out, const double* rdot, int sm_count,
+                                 double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  using C = Sw8<NS, INNER>;
+  Sw8Geo sg;
+  // stage chunk: multiple of 8, ~T1 / ceil(T1 / 64) so chunks are balanced, <= 8 warps
+  const int nch = (g.T1 + 63) / 64;
+  sg.S = std::min(64, ((g.T1 + nch - 1) / nch + 7) / 8 * 8);
+  sg.W = sg.S / 8;
+  sg.nchunk = (g.T1 + sg.S - 1) / sg.S;
+  sg.RECC = sg.S * NS;
+  sg.SLOT = C::NR * sg.RECC + 2 * C::FAC + 2 * C::OMG;
+  const size_t budget = 200 * 1024;
+  const size_t fixed = (size_t)C::NR * sg.RECC * 8;
+  sg.R = (int)std::max<size_t>(2, std::min<size_t>(8, (budget - fixed) / ((size_t)sg.SLOT * 8 + 16)));
+  const size_t smem = fixed + (size_t)sg.R * sg.SLOT * 8 + (size_t)sg.R * 16;
+  const int n_items = g.V * sg.nchunk;
+  cudaError_t e = cudaFuncSetAttribute(k_sweep8<NS, INNER>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int threads = 32 * (sg.W + 1);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep8<NS, INNER>, threads, smem);
+  const int cap = std::max(1, env_int("GQ_SWEEP8_CTAS_PER_SM", 1));
+  const int blocks = std::max(1, std::min(n_items, std::min(std::max(per_sm, 1), cap) * sm_count));
+  k_sweep8<NS, INNER><<<blocks, threads, smem, s>>>(g, fo, sg, rhs, th, out, rdot, n_items,
+                                                    partials, st, dotmode);
+  return cudaGetLastError();
 }
 
 template <int NS>
 static cudaError_t sweep4_n(const Geo& g, const FastOps& fo, bool inner, const double* rhs,
                             const double* th, double* out, const double* rdot, int sm_count,
                             double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  const int nchunk = (g.T1 + 15) / 16;
-  const int n_items = g.V * nchunk;
-  const int want = std::min(n_items, std::max(1, env_int("GQ_SWEEP_WARPS_PER_SM", 4)) * sm_count);
-  cudaError_t e;
-  unsigned blocks;
-  if (inner) {
-    constexpr size_t per = sw4_warp_bytes<NS, true>();
-    e = cudaFuncSetAttribute(k_sweep5<NS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)per);
-    if (e != cudaSuccess) return e;
-    blocks = resident_blocks(k_sweep5<NS, true>, per, want, sm_count);
-    k_sweep5<NS, true><<<blocks, 32, per, s>>>(g, fo, rhs, th, out, rdot, n_items, nchunk,
-                                               partials, st, dotmode);
-  } else {
-    constexpr size_t per = sw4_warp_bytes<NS, false>();
-    e = cudaFuncSetAttribute(k_sweep5<NS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)per);
-    if (e != cudaSuccess) return e;
-    blocks = resident_blocks(k_sweep5<NS, false>, per, want, sm_count);
-    k_sweep5<NS, false><<<blocks, 32, per, s>>>(g, fo, rhs, th, out, rdot, n_items, nchunk,
-                                                partials, st, dotmode);
+  static int exp_set = -1;
+  const int ex = env_int("GQ_EXP", 0);
+  if (exp_set != ex) {
+    cudaMemcpyToSymbol(g_exp, &ex, sizeof(int));
+    exp_set = ex;
   }
-  return cudaGetLastError();
+  if (env_int("GQ_SWEEP_V", 6) == 8) {
+    if (inner) return sweep8_launch<NS, true>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    return sweep8_launch<NS, false>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  }
+  // n = 4: the MT = 1 instantiation (255 registers + spills) faults with an illegal
+  // instruction on B200; the two-tile variant is used instead.
+  const int mt = NS == 4 ? 2 : env_int("GQ_SWEEP_MT", 1);
+  const int wsm = env_int("GQ_SWEEP_WARPS_PER_SM", mt == 1 ? 8 : 4);
+  if (mt == 2) {
+    if (inner) return sweep6_launch<NS, true, 2>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
+    return sweep6_launch<NS, false, 2>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
+  }
+  if (inner) return sweep6_launch<NS, true, 1>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
+  return sweep6_launch<NS, false, 1>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
+}
+
+int debug_read(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_dbg, sizeof(long long) * (n < 1024 ? n : 1024));
 }
 
 bool tc_supported(int n) { return (n == 2 || n == 4) && env_int("GQ_NO_DMMA", 0) == 0; }
@@ -1692,7 +2080,7 @@ bool fast_supported(int n) {
 
 long long fast_max_blocks(const Geo& g, const StencilShape& sh, int sm_count) {
   const long long warps = (long long)g.N * sh.nchunk * sh.nstrip;
-  const long long w4 = (long long)g.V * ((g.T1 + 15) / 16);
+  const long long w4 = (long long)g.V * ((g.T1 + 7) / 8);
   return std::max<long long>({warps, (long long)sweep3_warps(g, sm_count), w4});
 }
 
