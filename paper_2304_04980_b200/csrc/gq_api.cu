@@ -49,6 +49,10 @@ struct gq_ctx {
   double* rs = nullptr;        // r + Xi~ delta of the current outer sweep (fast path)
   double *oprow = nullptr, *omega = nullptr, *fac3 = nullptr, *fac4 = nullptr;
   FastOps fo{};
+  double *cff = nullptr, *cfb = nullptr;
+  int4* seg = nullptr;
+  ChainOps co{};
+  bool chain = false;          // lean DMMA chain sweeps (n in {2, 4})
   bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
   double* partials = nullptr;
   PcgState* st = nullptr;
@@ -67,8 +71,6 @@ struct gq_ctx {
 };
 
 extern "C" const char* gq_last_error(void) { return g_err.c_str(); }
-namespace gq { int debug_read(long long* out, int n); }
-extern "C" int gq_debug_read(long long* out, int n) { return gq::debug_read(out, n); }
 extern "C" const char* gq_version(void) { return "gridlq_b200 0.1.0 (sm_100a, fp64)"; }
 
 static bool is_device_ptr(const void* p) {
@@ -92,7 +94,7 @@ static void release(gq_ctx* c) {
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
                   c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
                   c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->partials, c->st, c->hist, c->err};
+                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -315,6 +317,24 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
     CKB(launch_build_fast(g, c->npc, c->op, c->oprow, c->omega, c->fac3, c->fac4, c->stream));
     CKB(cudaStreamSynchronize(c->stream));
     c->fo = FastOps{c->oprow, c->omega, c->fac3, c->psi_cls, c->fac4};
+    if (chain_supported(g.n)) {
+      // class-pure chunks of <= 8 stages: runs of equal Psi class split into 8s
+      std::vector<int4> segs;
+      for (int t = 0; t < g.T1;) {
+        int e = t + 1;
+        while (e < g.T1 && e - t < 8 && pcls[e] == pcls[t]) ++e;
+        segs.push_back(make_int4(t, e - t, pcls[t], 0));
+        t = e;
+      }
+      CKB(dalloc(&c->cff, chain_ff_doubles(g, c->npc)));
+      CKB(dalloc(&c->cfb, chain_fb_doubles(g, c->npc)));
+      CKB(dalloc(&c->seg, segs.size()));
+      CKB(cudaMemcpy(c->seg, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice));
+      CKB(launch_build_chain(g, c->npc, c->fac, c->omega, c->cff, c->cfb, c->stream));
+      CKB(cudaStreamSynchronize(c->stream));
+      c->co = ChainOps{c->cff, c->cfb, c->seg, (int)segs.size()};
+      c->chain = true;
+    }
   }
 
   // work vectors (stage-inner layout) and the reference-layout staging buffers
@@ -331,7 +351,8 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   long long maxb = std::max({(long long)c->sh_delta.blocks, (long long)c->sw.blocks,
                              (long long)c->sw_outer.blocks, (long long)c->vblocks,
                              fast_max_blocks(g, c->sh_delta, c->sm_count),
-                             fast_max_blocks(g, c->sh_outer, c->sm_count)});
+                             fast_max_blocks(g, c->sh_outer, c->sm_count),
+                             c->chain ? chain_max_blocks(g, c->co.nseg, c->sm_count) : 0LL});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));
   CKB(dalloc(&c->st, 1));
   CKB(cudaMemset(c->st, 0, sizeof(PcgState)));
@@ -388,7 +409,10 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
       const double* tp = l > 0 ? c->th[(l - 1) % 2] : nullptr;
       const double* dp = s > 0 ? c->dl[(s - 1) % 2] : nullptr;
       const int dm = (last && s == c->S - 1) ? dotmode : kDotNone;
-      if (c->fast) {
+      if (c->chain) {
+        CK(launch_chain(c->g, c->co, l > 0, s > 0 ? c->rs : rin, tp, ob, rin, c->sm_count,
+                        c->partials, st, dm, c->stream));
+      } else if (c->fast) {
         CK(launch_sweep3(c->g, c->fo, l > 0, s > 0 ? c->rs : rin, tp, ob, rin, c->sm_count,
                          c->partials, st, dm, c->stream));
       } else {

@@ -1,0 +1,605 @@
+// Pair-chain sweeps on the fp64 tensor cores, lean edition ("chain" kernels).
+//
+// One warp owns 8 chains: 8 consecutive stages (one stage class) of one column pair v, and
+// walks the nb = ceil(K/2) two-row blocks of the pair forward then backward
+// (block_linalg.py:336-358, nested_jacobi.py:85-103):
+//
+//   forward   w_k = L_k^-1 tau_k  - (L_k^-1 Omega~_k) theta  - G_k w_{k-1}
+//   backward  x_k = L_k^-T w_k    - H_k x_{k+1}
+//
+// with tau_k the block's right-hand side, theta the previous inner iterate (inner sweeps
+// only), G_k = L_k^-1 C_k and H_k = L_k^-T C_{k+1}^T.  Every product is an m8n8k4 DMMA with
+// the 8 chains on M: the right-hand side, the 12 theta neighbour records and the carried
+// iterate are three A operands of ONE accumulation, so the cross-pair coupling that v6 ran
+// on the FMA pipe (5 blocks x 4 nodes of Omega~ per lane) becomes 2*12n/8 DMMAs against the
+// precomputed M_k = L_k^-1 Omega~_k.  Only the G_k w_{k-1} term is loop-carried.
+//
+// Data movement: per block a warp stages its records (8 stages x n doubles, contiguous in the
+// stage-inner layout) and the block's factor tiles into a ring of P+1 shared-memory slots
+// with cp.async P blocks ahead.  Each lane owns fixed 16-byte chunks; its global source is a
+// running pointer advanced by one block stride, validity (off-grid column, stage past T) is
+// folded into a loop-invariant src-size, and only the first/last block test rows -- the
+// steady-state loop carries no bounds logic.  Items never straddle a stage-class boundary
+// (the host splits chunks at class changes), so a slot holds one class's factors.
+//
+// Factor tiles: every Q x Kc matrix is stored as 8x8 tiles (tile (h,p) = rows 8h.., cols
+// 8p.., row-major inside), so a B fragment is one conflict-free LDS.128 per lane
+// (row rw, columns 2qd, 2qd+1 -> the two k-steps of a k-pair).
+#include <algorithm>
+#include <cstdlib>
+
+#include "gq_internal.h"
+
+namespace gq {
+
+namespace {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void ldgsts(unsigned dst, const double* src, int sz, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(dst),
+               "l"(src), "r"(sz), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void wait_groups() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void dmma(double2& d, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d.x), "+d"(d.y)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double2 lds2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ void stg2_keep(double* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x),
+               "d"(v.y), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ double2 add2(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+
+// theta neighbour records of a block, relative to (column a, row 2k): the twelve nodes
+// outside the pair that the 13-point Psi diamond of its four nodes reaches
+__host__ __device__ constexpr int th_dc(int r) {
+  return r < 2 ? -2 : r < 6 ? -1 : r < 10 ? 2 : 3;
+}
+__host__ __device__ constexpr int th_dr(int r) {
+  return (r == 0 || r == 3 || r == 7 || r == 10) ? 0
+       : (r == 1 || r == 4 || r == 8 || r == 11) ? 1
+       : (r == 2 || r == 6) ? -1 : 2;
+}
+// omega slot u of a node in the pair's left (dc = 0) / right (dc = 1) column -> record index
+// (before adding the node's row offset); matches the u order of k_build_rows
+__host__ __device__ constexpr int th_rec(int dc, int u) {
+  return dc == 0 ? (u == 0 ? 0 : u == 1 ? 2 : u == 2 ? 3 : u == 3 ? 4 : 7)
+                 : (u == 0 ? 3 : u == 1 ? 6 : u == 2 ? 7 : u == 3 ? 8 : 10);
+}
+
+// ---- Warp reduction for one-warp CTAs (deterministic last-block pattern) -------------------
+__device__ bool warp_grid_sum(double v, double* partials, unsigned int* counter, double& out) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  int last = 0;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = v;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return false;
+  __threadfence();
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + b);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  out = acc;
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
+}  // namespace
+
+template <int NS, bool INNER>
+struct Ch {
+  static constexpr int Q = 4 * NS, QQ = Q * Q, NT = Q / 8;
+  static constexpr int TC = 12 * NS;                  // theta feature count
+  static constexpr int KT = TC / 8;                   // theta k-pairs
+  static constexpr int FFS = 2 * QQ + Q * TC;         // forward factor doubles per block
+  static constexpr int FF = INNER ? FFS : 2 * QQ;     // ... staged by this variant
+  static constexpr int FB = 2 * QQ;                   // backward factor doubles per block
+  static constexpr int REC = 8 * NS;                  // record: 8 stages x NS
+  static constexpr int CPR = REC / 2;                 // 16-byte chunks per record
+  static constexpr int RPI = 32 / CPR;                // records per warp instruction
+  static constexpr int NRF = INNER ? 16 : 4;          // forward records: tau(4) + theta(12)
+  static constexpr int JF = NRF / RPI, JB = 8 / RPI;  // record instructions fwd / bwd (w + r)
+  static constexpr int CFF = FF / 64, CFB = FB / 64;  // factor instructions (32 x 16 B each)
+  static constexpr int SLOT = (NRF * REC + FF) > (8 * REC + FB) ? (NRF * REC + FF) : (8 * REC + FB);
+  static_assert(NS == 2 || NS == 4, "chain sweep needs n in {2, 4}");
+  static_assert(FF % 64 == 0 && FB % 64 == 0, "factor blocks must be whole warp copies");
+};
+
+template <int NS, bool INNER, int P>
+__device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
+                                           const double* __restrict__ rhs,
+                                           const double* __restrict__ th, double* out,
+                                           const double* __restrict__ rdot, bool dotting,
+                                           double* ring, int v, int t0, int nvalid, int cls,
+                                           uint64_t pol_s, uint64_t pol_k, double& dot) {
+  using C = Ch<NS, INNER>;
+  constexpr int Q = C::Q, QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::REC, R = P + 1;
+  const int lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
+  const long long rs = (long long)g.T1 * NS;
+  const long long cs = (long long)g.K * rs;
+  const long long rs2 = 2 * rs;
+  const int nb = g.nb, K = g.K;
+  const int a = 2 * v;
+  const bool okb = a + 1 < g.N;
+  const long long col_a = (long long)a * cs + (long long)t0 * NS;
+  const int wch = lane % C::CPR;                         // my 16-byte chunk of a record
+  const int wst = wch / (NS / 2);                        // ... and the stage it belongs to
+  const bool stage_ok = wst < nvalid;
+  const int wofs = stage_ok ? 2 * wch : 0;               // stage-invalid lanes read stage 0
+  const unsigned ring_u = smem_u32(ring);
+
+  // ---------------- forward ----------------
+  const double* fsrc[C::JF];
+  int fsz[C::JF], frow[C::JF];
+#pragma unroll
+  for (int j = 0; j < C::JF; ++j) {
+    const int r = j * C::RPI + lane / C::CPR;
+    const int dc = r < 4 ? (r & 1) : th_dc(r - 4);
+    const int dr = r < 4 ? (r >> 1) : th_dr(r - 4);
+    const bool colok = a + dc >= 0 && a + dc < g.N;
+    fsz[j] = (colok && stage_ok) ? 16 : 0;
+    frow[j] = dr;
+    // off-grid columns are redirected to the pair's own column (never read: size 0)
+    fsrc[j] = (r < 4 ? rhs : th) + col_a + (long long)(colok ? dc : 0) * cs +
+              (long long)dr * rs + wofs;
+  }
+  const unsigned rec_dst = ring_u + (unsigned)(((lane / C::CPR) * REC + 2 * wch) * 8);
+  const double* ffb = co.ff + ((long long)cls * g.V + v) * nb * C::FFS + 2 * lane;
+  constexpr unsigned FOFS = (unsigned)(C::NRF * REC * 8);
+
+  // checked issue (first/last blocks and the prologue): rows outside [0, K) zero-fill
+  auto issue_f_chk = [&](int k, int slot) {
+    const unsigned sb = (unsigned)(slot * C::SLOT * 8);
+#pragma unroll
+    for (int j = 0; j < C::JF; ++j) {
+      const int row = 2 * k + frow[j];
+      const bool ok = fsz[j] && row >= 0 && row < K;
+      ldgsts(rec_dst + sb + j * C::RPI * REC * 8, ok ? fsrc[j] + k * rs2 : rhs, ok ? 16 : 0,
+             pol_s);
+    }
+    const double* fp = ffb + (long long)k * C::FFS;
+#pragma unroll
+    for (int i = 0; i < C::CFF; ++i)
+      ldgsts(ring_u + sb + FOFS + (unsigned)((2 * lane + 64 * i) * 8), fp + 64 * i, 16, pol_k);
+  };
+
+  double2 wd[NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) wd[h] = make_double2(0.0, 0.0);
+
+  // output fragment addressing: lane holds features 8h + 2qd, +1 of chain (stage) rw
+  long long oofs[NT];
+  bool ook[NT];
+  int orow[NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) {
+    const int f0 = 8 * h + 2 * qd, nd = f0 / NS, cc = f0 % NS;
+    oofs[h] = col_a + (long long)(nd & 1) * cs + (long long)(nd >> 1) * rs + rw * NS + cc;
+    ook[h] = rw < nvalid && ((nd & 1) ? okb : true);
+    orow[h] = nd >> 1;
+  }
+
+  {
+    const int pro = P < nb ? P : nb;
+#pragma unroll 1
+    for (int p = 0; p < pro; ++p) {
+      issue_f_chk(p, p);
+      commit();
+    }
+#pragma unroll 1
+    for (int p = pro; p < P; ++p) commit();
+  }
+  // running sources of block k + P
+  const double* fcur[C::JF];
+#pragma unroll
+  for (int j = 0; j < C::JF; ++j) fcur[j] = fsz[j] ? fsrc[j] + (long long)P * rs2 : rhs;
+  const long long fstep = rs2;
+  const double* fpc = ffb + (long long)P * C::FFS;
+
+  int slot = 0, islot = P % R;
+#pragma unroll 1
+  for (int k = 0; k < nb; ++k) {
+    const int kk = k + P;
+    if (kk < nb) {
+      if (kk == nb - 1) {
+        issue_f_chk(kk, islot);
+      } else {
+        const unsigned sb = (unsigned)(islot * C::SLOT * 8);
+#pragma unroll
+        for (int j = 0; j < C::JF; ++j)
+          ldgsts(rec_dst + sb + j * C::RPI * REC * 8, fcur[j], fsz[j], pol_s);
+#pragma unroll
+        for (int i = 0; i < C::CFF; ++i)
+          ldgsts(ring_u + sb + FOFS + (unsigned)((2 * lane + 64 * i) * 8), fpc + 64 * i, 16, pol_k);
+      }
+    }
+    commit();
+#pragma unroll
+    for (int j = 0; j < C::JF; ++j)
+      if (fsz[j]) fcur[j] += fstep;
+    fpc += C::FFS;
+    wait_groups<P>();
+    __syncwarp();
+
+    const double* sl = ring + slot * C::SLOT;
+    const double* sf = sl + C::NRF * REC;
+    // A operands: tau k-pairs and theta k-pairs (feature pair 8p + 2qd of chain rw)
+    double2 tv[NT];
+#pragma unroll
+    for (int p = 0; p < NT; ++p) {
+      const int f0 = 8 * p + 2 * qd;
+      tv[p] = lds2(sl + (f0 / NS) * REC + rw * NS + (f0 % NS));
+    }
+    double2 thv[INNER ? KT : 1];
+    if (INNER) {
+#pragma unroll
+      for (int p = 0; p < KT; ++p) {
+        const int f0 = 8 * p + 2 * qd;
+        thv[p] = lds2(sl + (4 + f0 / NS) * REC + rw * NS + (f0 % NS));
+      }
+    }
+    double2 wn[NT];
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0, g0 = a0, g1 = a0;
+      double2 m0 = a0, m1 = a0, m2 = a0, m3 = a0;
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const double2 b = lds2(sf + (h * NT + p) * 64 + rw * 8 + 2 * qd);
+        dmma(a0, tv[p].x, b.x);
+        dmma(a1, tv[p].y, b.y);
+      }
+      if (INNER) {
+#pragma unroll
+        for (int p = 0; p < KT; ++p) {
+          const double2 b = lds2(sf + 2 * QQ + (h * KT + p) * 64 + rw * 8 + 2 * qd);
+          if (p & 1) {
+            dmma(m2, thv[p].x, b.x);
+            dmma(m3, thv[p].y, b.y);
+          } else {
+            dmma(m0, thv[p].x, b.x);
+            dmma(m1, thv[p].y, b.y);
+          }
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const double2 b = lds2(sf + QQ + (h * NT + p) * 64 + rw * 8 + 2 * qd);
+        dmma(g0, wd[p].x, b.x);
+        dmma(g1, wd[p].y, b.y);
+      }
+      double2 s = add2(a0, a1);
+      if (INNER) s = add2(s, add2(add2(m0, m1), add2(m2, m3)));
+      wn[h] = add2(s, add2(g0, g1));
+    }
+    const bool lastk = k == nb - 1;
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      wd[h] = wn[h];
+      if (ook[h] && !(lastk && 2 * k + orow[h] >= K))
+        stg2_keep(out + oofs[h] + (long long)k * rs2, wn[h], pol_k);
+    }
+    slot = slot + 1 == R ? 0 : slot + 1;
+    islot = islot + 1 == R ? 0 : islot + 1;
+    __syncwarp();
+  }
+  wait_groups<0>();
+  __threadfence();
+  __syncwarp();
+
+  // ---------------- backward ----------------
+  const double* bsrc[C::JB];
+  int bsz[C::JB], brow[C::JB];
+#pragma unroll
+  for (int j = 0; j < C::JB; ++j) {
+    const int r = j * C::RPI + lane / C::CPR;
+    const int dc = r & 1, dr = (r >> 1) & 1;
+    const bool ok = stage_ok && (dc ? okb : true) && (r < 4 || dotting);
+    bsz[j] = ok ? 16 : 0;
+    brow[j] = dr;
+    bsrc[j] = (r < 4 ? (const double*)out : (dotting ? rdot : rhs)) + col_a +
+              (long long)(dc && okb ? 1 : 0) * cs + (long long)dr * rs + wofs;
+  }
+  const double* fbb = co.fb + ((long long)cls * g.V + v) * nb * C::FB + 2 * lane;
+  constexpr unsigned BOFS = (unsigned)(8 * REC * 8);
+  auto issue_b_chk = [&](int k, int slot_) {
+    const unsigned sb = (unsigned)(slot_ * C::SLOT * 8);
+#pragma unroll
+    for (int j = 0; j < C::JB; ++j) {
+      const bool ok = bsz[j] && 2 * k + brow[j] < K;
+      ldgsts(rec_dst + sb + j * C::RPI * REC * 8, ok ? bsrc[j] + k * rs2 : rhs, ok ? 16 : 0,
+             pol_s);
+    }
+    const double* fp = fbb + (long long)k * C::FB;
+#pragma unroll
+    for (int i = 0; i < C::CFB; ++i)
+      ldgsts(ring_u + sb + BOFS + (unsigned)((2 * lane + 64 * i) * 8), fp + 64 * i, 16, pol_k);
+  };
+  {
+    const int pro = P < nb ? P : nb;
+#pragma unroll 1
+    for (int p = 0; p < pro; ++p) {
+      issue_b_chk(nb - 1 - p, p);
+      commit();
+    }
+#pragma unroll 1
+    for (int p = pro; p < P; ++p) commit();
+  }
+  const double* bcur[C::JB];
+#pragma unroll
+  for (int j = 0; j < C::JB; ++j)
+    bcur[j] = bsz[j] ? bsrc[j] + (long long)(nb - 1 - P) * rs2 : rhs;
+  const double* fbc = fbb + (long long)(nb - 1 - P) * C::FB;
+
+  double2 xd[NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) xd[h] = make_double2(0.0, 0.0);
+  slot = 0;
+  islot = P % R;
+#pragma unroll 1
+  for (int k = nb - 1; k >= 0; --k) {
+    const int kk = k - P;
+    if (kk >= 0) {
+      const unsigned sb = (unsigned)(islot * C::SLOT * 8);
+#pragma unroll
+      for (int j = 0; j < C::JB; ++j)
+        if (j * C::RPI < 4 || dotting) ldgsts(rec_dst + sb + j * C::RPI * REC * 8, bcur[j], bsz[j], pol_s);
+#pragma unroll
+      for (int i = 0; i < C::CFB; ++i)
+        ldgsts(ring_u + sb + BOFS + (unsigned)((2 * lane + 64 * i) * 8), fbc + 64 * i, 16, pol_k);
+    }
+    commit();
+#pragma unroll
+    for (int j = 0; j < C::JB; ++j)
+      if (bsz[j]) bcur[j] -= rs2;
+    fbc -= C::FB;
+    wait_groups<P>();
+    __syncwarp();
+
+    const double* sl = ring + slot * C::SLOT;
+    const double* sf = sl + 8 * REC;
+    double2 wv[NT];
+#pragma unroll
+    for (int p = 0; p < NT; ++p) {
+      const int f0 = 8 * p + 2 * qd;
+      wv[p] = lds2(sl + (f0 / NS) * REC + rw * NS + (f0 % NS));
+    }
+    double2 xn[NT];
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0, g0 = a0, g1 = a0;
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const double2 b = lds2(sf + (h * NT + p) * 64 + rw * 8 + 2 * qd);
+        dmma(a0, wv[p].x, b.x);
+        dmma(a1, wv[p].y, b.y);
+      }
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const double2 b = lds2(sf + QQ + (h * NT + p) * 64 + rw * 8 + 2 * qd);
+        dmma(g0, xd[p].x, b.x);
+        dmma(g1, xd[p].y, b.y);
+      }
+      xn[h] = add2(add2(a0, a1), add2(g0, g1));
+    }
+    const bool lastk = k == nb - 1;
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      xd[h] = xn[h];
+      if (ook[h] && !(lastk && 2 * k + orow[h] >= K)) {
+        *reinterpret_cast<double2*>(out + oofs[h] + (long long)k * rs2) = xn[h];
+        if (dotting) {
+          const int f0 = 8 * h + 2 * qd;
+          const double2 rv = lds2(sl + (4 + f0 / NS) * REC + rw * NS + (f0 % NS));
+          dot = fma(xn[h].x, rv.x, dot);
+          dot = fma(xn[h].y, rv.y, dot);
+        }
+      }
+    }
+    slot = slot + 1 == R ? 0 : slot + 1;
+    islot = islot + 1 == R ? 0 : islot + 1;
+    __syncwarp();
+  }
+  wait_groups<0>();
+  __syncwarp();
+}
+
+template <int NS, bool INNER, int P>
+__global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* __restrict__ rhs,
+                                              const double* __restrict__ th, double* out,
+                                              const double* __restrict__ rdot, int n_items,
+                                              double* partials, PcgState* st, int dotmode) {
+  extern __shared__ __align__(16) double ring[];
+  if (halted(st)) return;
+  const uint64_t pol_s = pol_first(), pol_k = pol_last();
+  const bool dotting = dotmode != kDotNone;
+  double dot = 0.0;
+#pragma unroll 1
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int v = item / co.nseg;
+    const int4 sg = co.seg[item - v * co.nseg];
+    chain_item<NS, INNER, P>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x, sg.y, sg.z,
+                             pol_s, pol_k, dot);
+  }
+  if (dotting) {
+    double mu;
+    if (warp_grid_sum(dot, partials, &st->counter[2], mu) && threadIdx.x == 0) {
+      if (dotmode == kDotInit) {
+        st->mu = mu;                       // pcg.py:92
+      } else {
+        st->beta = mu / st->mu;            // pcg.py:127-131
+        st->mu = mu;
+      }
+    }
+  }
+}
+
+// ---- factor tiles ---------------------------------------------------------------------
+// ff[pc][v][k] = L^-1 | -G | -M (M = L^-1 Omega~, Q x 12n), fb[pc][v][k] = L^-T | -H, all as
+// 8x8 tiles; one thread per (block, row).
+__host__ __device__ __forceinline__ int tile_at(int r, int c, int kc) {
+  return ((r >> 3) * (kc >> 3) + (c >> 3)) * 64 + (r & 7) * 8 + (c & 7);
+}
+
+template <int NS>
+__global__ void k_build_chain(Geo g, int npc, const double* __restrict__ fac,
+                              const double* __restrict__ omega, double* __restrict__ ff,
+                              double* __restrict__ fb) {
+  using C = Ch<NS, true>;
+  constexpr int Q = C::Q, QQ = C::QQ, TC = C::TC, B2 = NS * NS;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)npc * g.V * g.nb * Q) return;
+  const int p = (int)(gid % Q);
+  const long long idx = gid / Q;                    // (pc, v, k)
+  const int k = (int)(idx % g.nb);
+  const int v = (int)((idx / g.nb) % g.V);
+  const int pc = (int)(idx / ((long long)g.nb * g.V));
+  const double* L = fac + idx * 2 * QQ;
+  const double* Cm = L + QQ;
+  const double* Cn = (k + 1 < g.nb) ? fac + (idx + 1) * 2 * QQ + QQ : nullptr;
+  double* F = ff + idx * C::FFS;
+  double* B = fb + idx * C::FB;
+  for (int c = 0; c < Q; ++c) {
+    double s = 0.0;
+    for (int m = 0; m <= p; ++m) s = fma(L[p * Q + m], Cm[m * Q + c], s);
+    F[tile_at(p, c, Q)] = L[p * Q + c];
+    F[QQ + tile_at(p, c, Q)] = -s;
+    B[tile_at(p, c, Q)] = L[c * Q + p];
+    double h = 0.0;
+    if (Cn)
+      for (int m = p; m < Q; ++m) h = fma(L[m * Q + p], Cn[c * Q + m], h);
+    B[QQ + tile_at(p, c, Q)] = -h;
+  }
+  // row p of M = L^-1 Omega~: Omega~[f][rec*NS + c] = Psi_u(node f/NS)[f%NS][c]
+  const int a = 2 * v;
+  double mrow[TC];
+  for (int c = 0; c < TC; ++c) mrow[c] = 0.0;
+  for (int f = 0; f <= p; ++f) {
+    const double l = L[p * Q + f];
+    if (l == 0.0) continue;
+    const int nd = f / NS, fc = f % NS, dc = nd & 1, dr = nd >> 1;
+    const int col = a + dc, row = 2 * k + dr;
+    if (col >= g.N || row >= g.K) continue;
+    const double* W = omega + ((long long)pc * g.nk + (long long)col * g.K + row) * 5 * B2;
+    for (int u = 0; u < 5; ++u) {
+      const int rec = th_rec(dc, u) + dr;
+      for (int c = 0; c < NS; ++c) mrow[rec * NS + c] = fma(l, W[u * B2 + fc * NS + c], mrow[rec * NS + c]);
+    }
+  }
+  for (int c = 0; c < TC; ++c) F[2 * QQ + tile_at(p, c, TC)] = -mrow[c];
+}
+
+// ---- host side -----------------------------------------------------------------------------
+
+static int env_or(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return (s && *s) ? atoi(s) : dflt;
+}
+
+bool chain_supported(int n) {
+  return (n == 2 || n == 4) && env_or("GQ_NO_CHAIN", 0) == 0;
+}
+
+size_t chain_ff_doubles(const Geo& g, int npc) {
+  return g.n == 2 ? (size_t)npc * g.V * g.nb * Ch<2, true>::FFS
+                  : (size_t)npc * g.V * g.nb * Ch<4, true>::FFS;
+}
+size_t chain_fb_doubles(const Geo& g, int npc) {
+  return g.n == 2 ? (size_t)npc * g.V * g.nb * Ch<2, true>::FB
+                  : (size_t)npc * g.V * g.nb * Ch<4, true>::FB;
+}
+
+cudaError_t launch_build_chain(const Geo& g, int npc, const double* fac, const double* omega,
+                               double* ff, double* fb, cudaStream_t s) {
+  const long long n = (long long)npc * g.V * g.nb * 4 * g.n;
+  const unsigned blocks = (unsigned)((n + 127) / 128);
+  if (g.n == 2)
+    k_build_chain<2><<<blocks, 128, 0, s>>>(g, npc, fac, omega, ff, fb);
+  else if (g.n == 4)
+    k_build_chain<4><<<blocks, 128, 0, s>>>(g, npc, fac, omega, ff, fb);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+template <int NS, bool INNER, int P>
+static cudaError_t chain_launch(const Geo& g, const ChainOps& co, const double* rhs,
+                                const double* th, double* out, const double* rdot, int sm_count,
+                                double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  constexpr size_t smem = (size_t)(P + 1) * Ch<NS, INNER>::SLOT * sizeof(double);
+  const int n_items = g.V * co.nseg;
+  static int attr_done = 0;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(k_chain<NS, INNER, P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_done = 1;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain<NS, INNER, P>, 32, smem);
+  const int want = env_or("GQ_CHAIN_WARPS", 0);
+  if (want > 0) per_sm = std::min(per_sm, want);
+  const int blocks = std::max(1, std::min(n_items, std::max(per_sm, 1) * sm_count));
+  k_chain<NS, INNER, P><<<blocks, 32, smem, s>>>(g, co, rhs, th, out, rdot, n_items, partials,
+                                                  st, dotmode);
+  return cudaGetLastError();
+}
+
+template <int NS, bool INNER>
+static cudaError_t chain_p(const Geo& g, const ChainOps& co, const double* rhs, const double* th,
+                           double* out, const double* rdot, int sm_count, double* partials,
+                           PcgState* st, int dotmode, cudaStream_t s) {
+  switch (env_or("GQ_CHAIN_P", NS == 2 ? 3 : 2)) {
+    case 1: return chain_launch<NS, INNER, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    case 2: return chain_launch<NS, INNER, 2>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    case 4: return chain_launch<NS, INNER, 4>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    default: return chain_launch<NS, INNER, 3>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  }
+}
+
+cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
+                         const double* th, double* out, const double* rdot, int sm_count,
+                         double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  if (g.n == 2)
+    return inner ? chain_p<2, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                 : chain_p<2, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  if (g.n == 4)
+    return inner ? chain_p<4, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                 : chain_p<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  return cudaErrorInvalidValue;
+}
+
+long long chain_max_blocks(const Geo& g, int nseg, int sm_count) {
+  return std::min<long long>((long long)g.V * nseg, 32LL * sm_count);
+}
+
+}  // namespace gq

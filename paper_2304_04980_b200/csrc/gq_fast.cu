@@ -131,8 +131,6 @@ __device__ __forceinline__ void st_rec_pol(double* p, const Vec<NS>& x, uint64_t
 __device__ __forceinline__ int first_lane(unsigned mask) { return mask ? __ffs(mask) - 1 : 0; }
 __device__ __forceinline__ int last_lane(unsigned mask) { return mask ? 31 - __clz(mask) : 0; }
 
-__device__ int g_exp = 0;       // experiment switches (bisecting performance; 0 = normal)
-__device__ long long g_dbg[1024];
 
 constexpr int kStencilP = 5;   // rows in flight per warp
 constexpr int kSweepP = 4;     // blocks in flight per warp
@@ -250,13 +248,13 @@ __global__ void __launch_bounds__(128) k_stencil3(Geo g, FastOps fo, const doubl
   const int pc = tv ? fo.psi_cls[t] : 0;
   const int cA = __shfl_sync(0xffffffffu, pc, first_lane(vmask));
   const int cB = __shfl_sync(0xffffffffu, pc, last_lane(vmask));
-  const double msel = (pc == cA) ? 0.0 : 1.0;
-  const int psel = (pc == cA) ? 0 : 1;
-  const double ke = (tv && t < g.T) ? 1.0 : 0.0;   // e_t exists (Xi_t, t < T)
-  const double kf = (tv && t >= 1) ? 1.0 : 0.0;    // f_t exists (Xi_{t-1})
-  const double ku = (t >= 1) ? 1.0 : 0.0;          // receives e_{t-1}
-  const double kd = (t < g.T) ? 1.0 : 0.0;         // receives f_{t+1}
-  (void)msel;
+  // off-range lanes read class A's operator slot (always staged); their zero-filled
+  // records keep every product finite and the masks below select them away
+  const int psel = (tv && pc != cA) ? 1 : 0;
+  const bool ke = tv && t < g.T;    // e_t exists (Xi_t, t < T)
+  const bool kf = tv && t >= 1;     // f_t exists (Xi_{t-1})
+  const bool ku = t >= 1;           // receives e_{t-1}
+  const bool kd = t < g.T;          // receives f_{t+1}
   const uint64_t pol = policy_evict_first();
   const uint64_t pol_op = policy_evict_last();
   double dot = 0.0;
@@ -359,18 +357,23 @@ __global__ void __launch_bounds__(128) k_stencil3(Geo g, FastOps fo, const doubl
       macs<NS>(f, E + 9 * B2, cp[1]);
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        e.v[k] *= ke;
-        f.v[k] *= kf;
+        e.v[k] = ke ? e.v[k] : 0.0;
+        f.v[k] = kf ? f.v[k] : 0.0;
       }
-      const Vec<NS> eu = shfl_up<NS>(e, 1);
-      const Vec<NS> fd = shfl_down<NS>(f, 1);
+      Vec<NS> eu = shfl_up<NS>(e, 1);
+      Vec<NS> fd = shfl_down<NS>(f, 1);
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        eu.v[k] = ku ? eu.v[k] : 0.0;
+        fd.v[k] = kd ? fd.v[k] : 0.0;
+      }
       if (MODE == kDelta) {
 #pragma unroll
-        for (int k = 0; k < NS; ++k) acc.v[k] = (acc.v[k] + ku * eu.v[k]) + kd * fd.v[k];
+        for (int k = 0; k < NS; ++k) acc.v[k] = (acc.v[k] + eu.v[k]) + fd.v[k];
       } else {   // y = r + (-(Xi_{t-1} x_{t-1}) - Xi_t' x_{t+1})
         const Vec<NS> rv = lds_rec<NS>(sl + 5 * REC + lane * NS);
 #pragma unroll
-        for (int k = 0; k < NS; ++k) acc.v[k] = rv.v[k] + ((0.0 - ku * eu.v[k]) - kd * fd.v[k]);
+        for (int k = 0; k < NS; ++k) acc.v[k] = rv.v[k] + ((0.0 - eu.v[k]) - fd.v[k]);
       }
       if (useful) {
         stv<NS>(y + ((long long)j * g.K * g.T1 + t) * NS + i * rs, acc);
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(32) k_sweep3(Geo g, FastOps fo, const double* 
     const int pc = tv ? fo.psi_cls[t] : 0;
     const int cA = __shfl_sync(0xffffffffu, pc, first_lane(vmask));
     const int cB = __shfl_sync(0xffffffffu, pc, last_lane(vmask));
-    const int psel = (pc == cA) ? 0 : 1;
+    const int psel = (tv && pc != cA) ? 1 : 0;
     const bool two = cB != cA;
     const int a = 2 * v;
     const bool okb = a + 1 < g.N;
@@ -840,7 +843,7 @@ __device__ __forceinline__ void sweep6_item(
       const bool edge = (k == 0) || (k == nb - 1);
 #pragma unroll
       for (int j = 0; j < JF; ++j) {
-        int sz = (g_exp == 3) ? 0 : fsz[j];
+        int sz = fsz[j];
         if (edge) {
           const int row = 2 * k + frow[j];
           if (row < 0 || row >= g.K) sz = 0;
@@ -851,10 +854,8 @@ __device__ __forceinline__ void sweep6_item(
                      : "memory");
       }
       const double* fa = FA + (long long)k * 4 * QQ;
-      if (g_exp != 8) {
 #pragma unroll
-        for (int c = lane; c < FCH; c += 32) cpa16(sl + C::NR * REC + 2 * c, fa + 2 * c, true, pol_keep);
-      }
+      for (int c = lane; c < FCH; c += 32) cpa16(sl + C::NR * REC + 2 * c, fa + 2 * c, true, pol_keep);
       if (TWO) {
         const double* fb = FB + (long long)k * 4 * QQ;
 #pragma unroll
@@ -915,15 +916,6 @@ __device__ __forceinline__ void sweep6_item(
       for (int h = 0; h < NT; ++h)
 #pragma unroll
         for (int z = 0; z < 2; ++z) d[m][h][z] = d1[m][h][z] = 0.0;
-    if (g_exp == 9) {
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-#pragma unroll
-        for (int h = 0; h < NT; ++h)
-#pragma unroll
-          for (int z = 0; z < 2; ++z) d[m][h][z] = xa[m][h][z] * sf[0];
-      return;
-    }
 #pragma unroll
     for (int pass = 0; pass < (TWO ? 2 : 1); ++pass) {
       const double* L = sf + pass * C::FAC;
@@ -1052,43 +1044,24 @@ __device__ __forceinline__ void sweep6_item(
     scp += SLOT;
     if (scp == ring_end) scp = ring;
   }
-  const bool probe = (g_exp == 7) && lane == 0 && t0 == 8 * MT && v == 0 && !TWO;
 #pragma unroll 1
   for (int k = 0; k < nb; ++k) {
-    long long c0 = clock64();
     issue_f(k + P, sip);
     sip += SLOT;
     if (sip == ring_end) sip = ring;
-    long long c1 = clock64();
     double e0[MT][NT][2], e1[MT][NT][2];
-    if (g_exp == 1 || g_exp == 9) {
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-#pragma unroll
-        for (int h = 0; h < NT; ++h) e0[m][h][0] = e0[m][h][1] = e1[m][h][0] = e1[m][h][1] = 0.0;
-    } else {
-      gmma(gcur, wd, e0, e1);
-    }
+    gmma(gcur, wd, e0, e1);
     double dln[MT][NT][2];
     double2 gnext[TWO ? 2 : 1][NT][NT];
-    long long c2 = 0, c3 = 0;
     if (k + 1 < nb) {
-      c2 = clock64();
       cp_wait<P - 1>();
       __syncwarp();
-      c3 = clock64();
       double bp[MT][NT][2];
       load_tau(scp, bp);
       lmma(scp + C::NR * REC, bp, dln);
       gfrag(scp + C::NR * REC, gnext);
       scp += SLOT;
       if (scp == ring_end) scp = ring;
-    }
-    if (probe && k < 200) {
-      g_dbg[4 * k + 0] = c1 - c0;
-      g_dbg[4 * k + 1] = c2 - c1;
-      g_dbg[4 * k + 2] = c3 - c2;
-      g_dbg[4 * k + 3] = clock64() - c3;
     }
     const bool lastk = k == nb - 1;
 #pragma unroll
@@ -1097,11 +1070,8 @@ __device__ __forceinline__ void sweep6_item(
       for (int h = 0; h < NT; ++h) {
         wd[m][h][0] = dl[m][h][0] + (e0[m][h][0] + e1[m][h][0]);
         wd[m][h][1] = dl[m][h][1] + (e0[m][h][1] + e1[m][h][1]);
-        if (g_exp != 10 && ostore[m][h] && !(lastk && olast[m][h]) && g_exp != 4) {
-          if (g_exp == 5)
-            *reinterpret_cast<double2*>(optr[m][h] + k * rs2) = make_double2(wd[m][h][0], wd[m][h][1]);
-          else
-            asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(optr[m][h] + k * rs2),
+        if (ostore[m][h] && !(lastk && olast[m][h])) {
+          asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(optr[m][h] + k * rs2),
                          "d"(wd[m][h][0]), "d"(wd[m][h][1]), "l"(pol_keep)
                          : "memory");
         }
@@ -1126,7 +1096,6 @@ __device__ __forceinline__ void sweep6_item(
   cp_wait<0>();
   __threadfence();
   __syncwarp();
-  if (g_exp == 2) return;
 
   // ---------------- backward: x_k = L_k^-T w_k - H_k x_{k+1} ----------------
   constexpr int JB = 8 / RPI;
@@ -1232,7 +1201,7 @@ __device__ __forceinline__ void sweep6_item(
       for (int h = 0; h < NT; ++h) {
         xd[m][h][0] = dl[m][h][0] + (e0[m][h][0] + e1[m][h][0]);
         xd[m][h][1] = dl[m][h][1] + (e0[m][h][1] + e1[m][h][1]);
-        if (g_exp != 10 && ostore[m][h] && !(lastk && olast[m][h])) {
+        if (ostore[m][h] && !(lastk && olast[m][h])) {
           *reinterpret_cast<double2*>(optr[m][h] + k * rs2) = make_double2(xd[m][h][0], xd[m][h][1]);
           if (dotmode != kDotNone) {
             dot = fma(xd[m][h][0], rcur[m][h][0], dot);
@@ -1275,10 +1244,6 @@ __global__ void __launch_bounds__(32) k_sweep6(Geo g, FastOps fo, const double* 
   const int rw = lane >> 2;
   uint64_t pol = policy_evict_first();
   uint64_t pol_keep = policy_evict_last();
-  if (g_exp == 6) {
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-    pol_keep = pol;
-  }
   double dot = 0.0;
 #pragma unroll 1
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -1427,10 +1392,7 @@ __device__ __forceinline__ void sweep8_warp_item(
   };
   auto acquire = [&]() -> double* {
     const uint32_t s = nuse % R, par = (nuse / R) & 1;
-    const long long c0 = clock64();
     mbar_wait(full + s, par);
-    if (g_exp == 7 && blockIdx.x == 0 && wid == 0 && lane == 0 && nuse < 200)
-      g_dbg[4 * nuse + 1] = clock64() - c0, g_dbg[4 * nuse + 2] = c0;
     ++nuse;
     return ring + (size_t)s * SLOT;
   };
@@ -1711,9 +1673,7 @@ __global__ void __launch_bounds__(288) k_sweep8(Geo g, FastOps fo, Sw8Geo sg,
         const int tc[12] = {-2, -2, -1, -1, -1, -1, 2, 2, 2, 2, 3, 3};
         auto slot_for_fill = [&](uint32_t& bytes_bar_slot) -> double* {
           const uint32_t s = nfill % R, u = nfill / R;
-          const long long c0 = clock64();
           if (u >= 1) mbar_wait(empty + s, (u - 1) & 1);
-          if (g_exp == 7 && blockIdx.x == 0 && nfill < 200) g_dbg[4 * nfill + 0] = clock64() - c0;
           ++nfill;
           bytes_bar_slot = s;
           return ring + (size_t)s * SLOT;
@@ -2005,12 +1965,6 @@ template <int NS>
 static cudaError_t sweep4_n(const Geo& g, const FastOps& fo, bool inner, const double* rhs,
                             const double* th, double* out, const double* rdot, int sm_count,
                             double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  static int exp_set = -1;
-  const int ex = env_int("GQ_EXP", 0);
-  if (exp_set != ex) {
-    cudaMemcpyToSymbol(g_exp, &ex, sizeof(int));
-    exp_set = ex;
-  }
   if (env_int("GQ_SWEEP_V", 6) == 8) {
     if (inner) return sweep8_launch<NS, true>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
     return sweep8_launch<NS, false>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
@@ -2027,9 +1981,6 @@ static cudaError_t sweep4_n(const Geo& g, const FastOps& fo, bool inner, const d
   return sweep6_launch<NS, false, 1>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
 }
 
-int debug_read(long long* out, int n) {
-  return (int)cudaMemcpyFromSymbol(out, g_dbg, sizeof(long long) * (n < 1024 ? n : 1024));
-}
 
 bool tc_supported(int n) { return (n == 2 || n == 4) && env_int("GQ_NO_DMMA", 0) == 0; }
 

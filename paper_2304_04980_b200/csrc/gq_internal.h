@@ -72,6 +72,23 @@ cudaError_t launch_sweep3(const Geo& g, const FastOps& fo, bool inner, const dou
 bool fast_supported(int n);
 long long fast_max_blocks(const Geo& g, const StencilShape& sh, int sm_count);
 
+// ---- lean DMMA pair-chain sweeps (gq_chain.cu) ----
+struct ChainOps {
+  const double* ff;    // [npc][V][nb] L^-1 | -G | -L^-1 Omega~   (8x8 tiles)
+  const double* fb;    // [npc][V][nb] L^-T | -H                  (8x8 tiles)
+  const int4* seg;     // [nseg] (t0, nvalid <= 8, psi class, 0): class-pure stage chunks
+  int nseg;
+};
+bool chain_supported(int n);
+size_t chain_ff_doubles(const Geo& g, int npc);
+size_t chain_fb_doubles(const Geo& g, int npc);
+cudaError_t launch_build_chain(const Geo& g, int npc, const double* fac, const double* omega,
+                               double* ff, double* fb, cudaStream_t s);
+cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
+                         const double* th, double* out, const double* rdot, int sm_count,
+                         double* partials, PcgState* st, int dotmode, cudaStream_t s);
+long long chain_max_blocks(const Geo& g, int nseg, int sm_count);
+
 // ---- vector kernels (gq_vec.cu) ----
 int vec_blocks(int sm_count);
 cudaError_t launch_update(const Geo& g, double* x, double* r, const double* d, const double* y,

@@ -1,4 +1,4 @@
-"""Time one preconditioner apply (4 sweeps + outer rhs) at the headline size."""
+"""Time one preconditioner apply (S=L=2: 4 sweeps + outer rhs) at the headline size."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -9,7 +9,9 @@ v = torch.randn(op.dim, device="cuda", dtype=torch.float64)
 for _ in range(2): pc.apply(v)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-e0.record(); n = 5
+n = 10
+e0.record()
 for _ in range(n): pc.apply(v)
 e1.record(); torch.cuda.synchronize()
-print(json.dumps({"exp": os.environ.get("GQ_EXP", "0"), "v": os.environ.get("GQ_SWEEP_V", "8"), "ms_per_apply": e0.elapsed_time(e1) / n}))
+env = {k: v for k, v in os.environ.items() if k.startswith("GQ_")}
+print(json.dumps({"env": env, "ms_per_apply": e0.elapsed_time(e1) / n}))
