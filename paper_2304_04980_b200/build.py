@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import glob
 import os
+import re
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
@@ -53,9 +54,33 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
         list(ex.map(run, jobs))
+    for job in jobs:
+        lint_sass(job[-1])
     if force or jobs or not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
         run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
     return LIB
+
+
+# LDGSTS whose shared destination ptxas split as [R + UR] (emitted next to an L2 cache-policy
+# operand) faults with "illegal instruction" on B200; refuse to ship such code.
+_BAD_LDGSTS = re.compile(r"LDGSTS[^;]*\[R\d+\+UR\d+")
+
+
+def lint_sass(obj: str) -> None:
+    cuobjdump = os.path.join(os.path.dirname(NVCC), "cuobjdump")
+    res = subprocess.run([cuobjdump, "-sass", obj], capture_output=True, text=True)
+    if res.returncode != 0:
+        return
+    func, bad = None, {}
+    for line in res.stdout.splitlines():
+        if "Function :" in line:
+            func = line.split("Function :")[1].strip()
+        elif _BAD_LDGSTS.search(line):
+            bad[func] = bad.get(func, 0) + 1
+    if bad:
+        os.remove(obj)
+        raise RuntimeError(f"{os.path.basename(obj)}: LDGSTS [R+UR] forms (fault on B200) in "
+                           + ", ".join(f"{k} x{v}" for k, v in bad.items()))
 
 
 if __name__ == "__main__":

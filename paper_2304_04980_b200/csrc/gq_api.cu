@@ -53,6 +53,8 @@ struct gq_ctx {
   int4* seg = nullptr;
   ChainOps co{};
   bool chain = false;          // lean DMMA chain sweeps (n in {2, 4})
+  bool grid = false;           // lean n = 2 grid stencils
+  GridShape gsh{};
   bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
   double* partials = nullptr;
   PcgState* st = nullptr;
@@ -343,6 +345,8 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                      &c->dl[0], &c->dl[1], &c->tmp0, &c->tmp1, &c->rs};
   for (double** p : vecs) CKB(dalloc(p, dim));
   c->sh_delta = stencil_shape(g, kDelta, c->sm_count);
+  c->grid = c->fast && grid_supported(g.n);
+  if (c->grid) c->gsh = grid_shape(g, c->sm_count);
   c->sh_outer = stencil_shape(g, kOuter, c->sm_count);
   c->sh_inner = stencil_shape(g, kInner, c->sm_count);
   c->sw = sweep_shape(g, false);
@@ -352,7 +356,8 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                              (long long)c->sw_outer.blocks, (long long)c->vblocks,
                              fast_max_blocks(g, c->sh_delta, c->sm_count),
                              fast_max_blocks(g, c->sh_outer, c->sm_count),
-                             c->chain ? chain_max_blocks(g, c->co.nseg, c->sm_count) : 0LL});
+                             c->chain ? chain_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
+                             c->grid ? (long long)c->gsh.blocks : 0LL});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));
   CKB(dalloc(&c->st, 1));
   CKB(cudaMemset(c->st, 0, sizeof(PcgState)));
@@ -395,8 +400,12 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
   for (int s = 0; s < c->S; ++s) {
     if (c->fast && s > 0) {
       // rhs_s = r + Xi~ delta_{s-1}, materialised once per outer sweep (nested_jacobi.py:119-121)
-      CK(launch_stencil3(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->sh_outer,
-                         c->partials, st, kDotNone, c->stream));
+      if (c->grid)
+        CK(launch_grid(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->gsh,
+                       c->partials, st, kDotNone, c->stream));
+      else
+        CK(launch_stencil3(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->sh_outer,
+                           c->partials, st, kDotNone, c->stream));
       if (names) names->push_back("outer_rhs_s" + std::to_string(s));
       if (mark) {
         const int rc = mark();
@@ -435,7 +444,10 @@ extern "C" int gq_apply_delta(gq_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, x, c->tmp0);
   if (rc) return rc;
-  if (c->fast)
+  if (c->grid)
+    CK(launch_grid(c->g, c->fo, kDelta, c->tmp0, nullptr, c->y, c->gsh, c->partials, nullptr,
+                   kDotNone, c->stream));
+  else if (c->fast)
     CK(launch_stencil3(c->g, c->fo, kDelta, c->tmp0, nullptr, c->y, c->sh_delta, c->partials,
                        nullptr, kDotNone, c->stream));
   else
@@ -494,7 +506,10 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
   };
   int rc = mark();
   if (rc) return rc;
-  if (c->fast)
+  if (c->grid)
+    CK(launch_grid(c->g, c->fo, kDelta, c->d, nullptr, c->y, c->gsh, c->partials, c->st,
+                   kDotStep, c->stream));
+  else if (c->fast)
     CK(launch_stencil3(c->g, c->fo, kDelta, c->d, nullptr, c->y, c->sh_delta, c->partials, c->st,
                        kDotStep, c->stream));
   else

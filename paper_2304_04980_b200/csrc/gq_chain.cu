@@ -28,50 +28,19 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "gq_async.cuh"
 #include "gq_internal.h"
 
 namespace gq {
 
 namespace {
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ uint64_t pol_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t pol_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void ldgsts(unsigned dst, const double* src, int sz, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(dst),
-               "l"(src), "r"(sz), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void wait_groups() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void dmma(double2& d, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d.x), "+d"(d.y)
-               : "d"(a), "d"(b));
-}
-__device__ __forceinline__ double2 lds2(const double* p) {
-  return *reinterpret_cast<const double2*>(p);
-}
+using namespace as;
+
 __device__ __forceinline__ void stg2_keep(double* p, double2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x),
                "d"(v.y), "l"(pol)
                : "memory");
-}
-__device__ __forceinline__ double2 add2(double2 a, double2 b) {
-  return make_double2(a.x + b.x, a.y + b.y);
 }
 
 // theta neighbour records of a block, relative to (column a, row 2k): the twelve nodes
@@ -134,6 +103,8 @@ struct Ch {
   static_assert(FF % 64 == 0 && FB % 64 == 0, "factor blocks must be whole warp copies");
 };
 
+using namespace as;
+
 template <int NS, bool INNER, int P>
 __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            const double* __restrict__ rhs,
@@ -142,7 +113,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            double* ring, int v, int t0, int nvalid, int cls,
                                            uint64_t pol_s, uint64_t pol_k, double& dot) {
   using C = Ch<NS, INNER>;
-  constexpr int Q = C::Q, QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::REC, R = P + 1;
+  constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::REC, R = P + 1;
   const int lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
   const long long rs = (long long)g.T1 * NS;
   const long long cs = (long long)g.K * rs;
@@ -172,13 +143,15 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     fsrc[j] = (r < 4 ? rhs : th) + col_a + (long long)(colok ? dc : 0) * cs +
               (long long)dr * rs + wofs;
   }
-  const unsigned rec_dst = ring_u + (unsigned)(((lane / C::CPR) * REC + 2 * wch) * 8);
+  // per-lane shared destinations, kept in vector registers (no [R + UR] LDGSTS forms)
+  const unsigned rec_dst = lane_opaque(ring_u + (unsigned)(((lane / C::CPR) * REC + 2 * wch) * 8));
+  const unsigned facf_dst = lane_opaque(ring_u + (unsigned)(C::NRF * REC * 8 + 16 * lane));
+  const unsigned facb_dst = lane_opaque(ring_u + (unsigned)(8 * REC * 8 + 16 * lane));
   const double* ffb = co.ff + ((long long)cls * g.V + v) * nb * C::FFS + 2 * lane;
-  constexpr unsigned FOFS = (unsigned)(C::NRF * REC * 8);
 
   // checked issue (first/last blocks and the prologue): rows outside [0, K) zero-fill
   auto issue_f_chk = [&](int k, int slot) {
-    const unsigned sb = (unsigned)(slot * C::SLOT * 8);
+    const unsigned sb = lane_opaque((unsigned)(slot * C::SLOT * 8));
 #pragma unroll
     for (int j = 0; j < C::JF; ++j) {
       const int row = 2 * k + frow[j];
@@ -189,7 +162,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     const double* fp = ffb + (long long)k * C::FFS;
 #pragma unroll
     for (int i = 0; i < C::CFF; ++i)
-      ldgsts(ring_u + sb + FOFS + (unsigned)((2 * lane + 64 * i) * 8), fp + 64 * i, 16, pol_k);
+      ldgsts(facf_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
   };
 
   double2 wd[NT];
@@ -233,13 +206,13 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       if (kk == nb - 1) {
         issue_f_chk(kk, islot);
       } else {
-        const unsigned sb = (unsigned)(islot * C::SLOT * 8);
+        const unsigned sb = lane_opaque((unsigned)(islot * C::SLOT * 8));
 #pragma unroll
         for (int j = 0; j < C::JF; ++j)
           ldgsts(rec_dst + sb + j * C::RPI * REC * 8, fcur[j], fsz[j], pol_s);
 #pragma unroll
         for (int i = 0; i < C::CFF; ++i)
-          ldgsts(ring_u + sb + FOFS + (unsigned)((2 * lane + 64 * i) * 8), fpc + 64 * i, 16, pol_k);
+          ldgsts(facf_dst + sb + 512 * i, fpc + 64 * i, 16, pol_k);
       }
     }
     commit();
@@ -330,9 +303,8 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
               (long long)(dc && okb ? 1 : 0) * cs + (long long)dr * rs + wofs;
   }
   const double* fbb = co.fb + ((long long)cls * g.V + v) * nb * C::FB + 2 * lane;
-  constexpr unsigned BOFS = (unsigned)(8 * REC * 8);
   auto issue_b_chk = [&](int k, int slot_) {
-    const unsigned sb = (unsigned)(slot_ * C::SLOT * 8);
+    const unsigned sb = lane_opaque((unsigned)(slot_ * C::SLOT * 8));
 #pragma unroll
     for (int j = 0; j < C::JB; ++j) {
       const bool ok = bsz[j] && 2 * k + brow[j] < K;
@@ -342,7 +314,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     const double* fp = fbb + (long long)k * C::FB;
 #pragma unroll
     for (int i = 0; i < C::CFB; ++i)
-      ldgsts(ring_u + sb + BOFS + (unsigned)((2 * lane + 64 * i) * 8), fp + 64 * i, 16, pol_k);
+      ldgsts(facb_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
   };
   {
     const int pro = P < nb ? P : nb;
@@ -369,13 +341,13 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   for (int k = nb - 1; k >= 0; --k) {
     const int kk = k - P;
     if (kk >= 0) {
-      const unsigned sb = (unsigned)(islot * C::SLOT * 8);
+      const unsigned sb = lane_opaque((unsigned)(islot * C::SLOT * 8));
 #pragma unroll
       for (int j = 0; j < C::JB; ++j)
-        if (j * C::RPI < 4 || dotting) ldgsts(rec_dst + sb + j * C::RPI * REC * 8, bcur[j], bsz[j], pol_s);
+        ldgsts(rec_dst + sb + j * C::RPI * REC * 8, bcur[j], bsz[j], pol_s);
 #pragma unroll
       for (int i = 0; i < C::CFB; ++i)
-        ldgsts(ring_u + sb + BOFS + (unsigned)((2 * lane + 64 * i) * 8), fbc + 64 * i, 16, pol_k);
+        ldgsts(facb_dst + sb + 512 * i, fbc + 64 * i, 16, pol_k);
     }
     commit();
 #pragma unroll

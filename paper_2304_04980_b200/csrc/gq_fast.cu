@@ -1977,8 +1977,11 @@ static cudaError_t sweep4_n(const Geo& g, const FastOps& fo, bool inner, const d
     if (inner) return sweep6_launch<NS, true, 2>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
     return sweep6_launch<NS, false, 2>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
   }
-  if (inner) return sweep6_launch<NS, true, 1>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
-  return sweep6_launch<NS, false, 1>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
+  if constexpr (NS == 2) {
+    if (inner) return sweep6_launch<NS, true, 1>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
+    return sweep6_launch<NS, false, 1>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
+  }
+  return cudaErrorInvalidValue;
 }
 
 

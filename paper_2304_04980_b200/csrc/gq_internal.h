@@ -89,6 +89,17 @@ cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const dou
                          double* partials, PcgState* st, int dotmode, cudaStream_t s);
 long long chain_max_blocks(const Geo& g, int nseg, int sm_count);
 
+// ---- lean n = 2 grid stencils (gq_grid.cu) ----
+struct GridShape {
+  int nchunk = 0, nstrip = 0, rows = 0, blocks = 0;
+};
+bool grid_supported(int n);
+GridShape grid_shape(const Geo& g, int sm_count);
+// modes kDelta (y = Delta x, optional curvature) and kOuterRhs (y = r + Xi~ x)
+cudaError_t launch_grid(const Geo& g, const FastOps& fo, int mode, const double* x,
+                        const double* rin, double* y, const GridShape& sh, double* partials,
+                        PcgState* st, int dotmode, cudaStream_t s);
+
 // ---- vector kernels (gq_vec.cu) ----
 int vec_blocks(int sm_count);
 cudaError_t launch_update(const Geo& g, double* x, double* r, const double* d, const double* y,

@@ -8,7 +8,15 @@
 
 namespace gq {
 
-int vec_blocks(int sm_count) { return sm_count * 4; }
+int vec_blocks(int sm_count) { return sm_count * 8; }
+
+// Streaming kernels: each thread keeps kVU independent 16-byte loads per operand in flight
+// (a 210 MB vector pass is pure HBM bandwidth), 8 x 256-thread blocks per SM.
+constexpr int kVU = 4;
+
+__device__ __forceinline__ double2 ld_stream(const double* p) {
+  return __ldcs(reinterpret_cast<const double2*>(p));
+}
 
 __global__ void __launch_bounds__(256) k_update(long long dim, double* __restrict__ x,
                                                 double* __restrict__ r,
@@ -18,12 +26,41 @@ __global__ void __launch_bounds__(256) k_update(long long dim, double* __restric
   if (halted(st)) return;
   const double alpha = st->alpha;
   double m = 0.0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride) {
-    x[e] = __dadd_rn(x[e], __dmul_rn(alpha, d[e]));          // pcg.py:109
-    const double rn = __dsub_rn(r[e], __dmul_rn(alpha, y[e]));  // pcg.py:111
+  const long long n2 = dim >> 1;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long b = tid; b < n2; b += nth * kVU) {
+    double2 xv[kVU], rv[kVU], dv[kVU], yv[kVU];
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        dv[u] = ld_stream(d + e);
+        yv[u] = ld_stream(y + e);
+        xv[u] = *reinterpret_cast<const double2*>(x + e);
+        rv[u] = *reinterpret_cast<const double2*>(r + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        xv[u].x = __dadd_rn(xv[u].x, __dmul_rn(alpha, dv[u].x));    // pcg.py:109
+        xv[u].y = __dadd_rn(xv[u].y, __dmul_rn(alpha, dv[u].y));
+        rv[u].x = __dsub_rn(rv[u].x, __dmul_rn(alpha, yv[u].x));    // pcg.py:111
+        rv[u].y = __dsub_rn(rv[u].y, __dmul_rn(alpha, yv[u].y));
+        __stcs(reinterpret_cast<double2*>(x + e), xv[u]);
+        *reinterpret_cast<double2*>(r + e) = rv[u];
+        m = nmax(m, nmax(fabs(rv[u].x), fabs(rv[u].y)));           // pcg.py:113
+      }
+    }
+  }
+  if ((dim & 1) && tid == 0) {
+    const long long e = dim - 1;
+    x[e] = __dadd_rn(x[e], __dmul_rn(alpha, d[e]));
+    const double rn = __dsub_rn(r[e], __dmul_rn(alpha, y[e]));
     r[e] = rn;
-    m = nmax(m, fabs(rn));                                     // pcg.py:113
+    m = nmax(m, fabs(rn));
   }
   double res;
   if (grid_reduce<true>(m, partials, &st->counter[1], res) && threadIdx.x == 0) {
@@ -41,9 +78,30 @@ __global__ void __launch_bounds__(256) k_dirupdate(long long dim, double* __rest
                                                    const double* __restrict__ q, PcgState* st) {
   if (halted(st)) return;
   const double beta = st->beta;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride)
-    d[e] = __dadd_rn(q[e], __dmul_rn(beta, d[e]));            // pcg.py:129
+  const long long n2 = dim >> 1;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long b = tid; b < n2; b += nth * kVU) {
+    double2 dv[kVU], qv[kVU];
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        qv[u] = ld_stream(q + e);
+        dv[u] = *reinterpret_cast<const double2*>(d + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        dv[u].x = __dadd_rn(qv[u].x, __dmul_rn(beta, dv[u].x));    // pcg.py:129
+        dv[u].y = __dadd_rn(qv[u].y, __dmul_rn(beta, dv[u].y));
+        *reinterpret_cast<double2*>(d + e) = dv[u];
+      }
+    }
+  }
+  if ((dim & 1) && tid == 0) d[dim - 1] = __dadd_rn(q[dim - 1], __dmul_rn(beta, d[dim - 1]));
 }
 
 __global__ void __launch_bounds__(256) k_dot(long long dim, const double* __restrict__ a,
