@@ -72,8 +72,8 @@ template <int MODE, int P>
 __global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __restrict__ x,
                                              const double* __restrict__ rin,
                                              double* __restrict__ y, int nchunk, int nstrip,
-                                             int rows, double* partials, PcgState* st,
-                                             int dotmode) {
+                                             int rows, int n_items, double* partials,
+                                             PcgState* st, int dotmode) {
   using C = Gd<MODE>;
   constexpr int R = P + 1, REC = C::REC, OPS = C::OPS;
   extern __shared__ __align__(16) double ring[];
@@ -87,8 +87,13 @@ __global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __
     }
   }
   const int lane = threadIdx.x;
-  const int strip = blockIdx.x % nstrip;
-  const int rest = blockIdx.x / nstrip;
+  const uint64_t pol_s = pol_first(), pol_k = pol_last();
+  const unsigned ring_u = lane_opaque(smem_u32(ring) + 16 * lane) - 16 * lane;
+  double dot = 0.0;
+#pragma unroll 1
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  const int strip = item % nstrip;
+  const int rest = item / nstrip;
   const int chunk = rest % nchunk;
   const int j = rest / nchunk;
   const int K = g.K;
@@ -105,9 +110,6 @@ __global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __
   const bool kf = tv && t >= 1;     // f_t exists (Xi_{t-1})
   const bool ku = t >= 1;           // receives e_{t-1}
   const bool kd = t < g.T;          // receives f_{t+1}
-  const uint64_t pol_s = pol_first(), pol_k = pol_last();
-  const unsigned ring_u = lane_opaque(smem_u32(ring) + 16 * lane) - 16 * lane;
-
   const long long rs = (long long)g.T1 * 2;
   const long long cs = (long long)K * rs;
   const long long toff = (long long)(tv ? t : 0) * 2;
@@ -125,7 +127,6 @@ __global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __
 
   const int i0 = strip * rows;
   const int i1 = min(K, i0 + rows);
-  double dot = 0.0;
 
   // records of row-step ii -> ring slot
   auto issue = [&](int ii, int slot) {
@@ -305,6 +306,8 @@ __global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __
     if (i + 4 < i1) stepS(std::integral_constant<int, 4>{}, i + 4);
   }
   wait_groups<0>();
+  __syncwarp();
+  }
   if (MODE == kDelta && dotmode != kDotNone) {
     double c;
     if (warp_grid_sum2(dot, partials, &st->counter[0], c) && threadIdx.x == 0) {
@@ -329,39 +332,60 @@ static int genv(const char* name, int dflt) {
 bool grid_supported(int n) { return n == 2 && genv("GQ_NO_GRID", 0) == 0; }
 
 GridShape grid_shape(const Geo& g, int sm_count) {
+  // upper bound (partials sizing); the launch picks the strip count per kernel occupancy
   GridShape sh;
   sh.nchunk = (g.T1 + kHaloChunk - 1) / kHaloChunk;
-  const long long cols = (long long)g.N * sh.nchunk;
-  const long long want = 12LL * sm_count;
-  int nstrip = (int)std::max<long long>(1, (want + cols - 1) / cols);
-  nstrip = std::min(nstrip, std::max(1, g.K / 8));
-  sh.rows = (g.K + nstrip - 1) / nstrip;
-  sh.nstrip = (g.K + sh.rows - 1) / sh.rows;
-  sh.blocks = (int)(cols * sh.nstrip);
+  sh.nstrip = std::max(1, std::min(8, g.K / 8));
+  sh.rows = (g.K + sh.nstrip - 1) / sh.nstrip;
+  sh.blocks = (int)std::min<long long>((long long)g.N * sh.nchunk * sh.nstrip, 32LL * sm_count);
   return sh;
 }
 
 template <int MODE, int P>
 static cudaError_t grid_launch(const Geo& g, const FastOps& fo, const double* x, const double* rin,
-                               double* y, const GridShape& sh, double* partials, PcgState* st,
+                               double* y, const GridShape& ub, double* partials, PcgState* st,
                                int dotmode, cudaStream_t s) {
   constexpr size_t smem = (size_t)(P + 1) * Gd<MODE>::SLOT * sizeof(double);
-  static int attr_done = 0;
+  static int attr_done = 0, per_sm = 0;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(k_grid<MODE, P>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid<MODE, P>, 32, smem);
+    per_sm = std::max(per_sm, 1);
     attr_done = 1;
   }
-  k_grid<MODE, P><<<sh.blocks, 32, smem, s>>>(g, fo, x, rin, y, sh.nchunk, sh.nstrip, sh.rows,
-                                              partials, st, dotmode);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // equal-cost items (column, 30-stage chunk, row strip) on a persistent grid: pick the
+  // strip count that minimises waves x (rows per strip + window warm-up)
+  const long long cols = (long long)g.N * ub.nchunk;
+  const long long slots = (long long)per_sm * sms;
+  int best = 1;
+  long long best_cost = -1;
+  for (int ns = 1; ns <= ub.nstrip; ++ns) {
+    const int rows = (g.K + ns - 1) / ns;
+    const long long items = cols * ((g.K + rows - 1) / rows);
+    const long long cost = ((items + slots - 1) / slots) * (rows + 4);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = ns;
+    }
+  }
+  const int rows = (g.K + best - 1) / best;
+  const int nstrip = (g.K + rows - 1) / rows;
+  const int n_items = (int)(cols * nstrip);
+  const int blocks = (int)std::min<long long>({(long long)n_items, slots, (long long)ub.blocks});
+  k_grid<MODE, P><<<blocks, 32, smem, s>>>(g, fo, x, rin, y, ub.nchunk, nstrip, rows, n_items,
+                                           partials, st, dotmode);
   return cudaGetLastError();
 }
 
 cudaError_t launch_grid(const Geo& g, const FastOps& fo, int mode, const double* x,
                         const double* rin, double* y, const GridShape& sh, double* partials,
                         PcgState* st, int dotmode, cudaStream_t s) {
-  const int p = genv("GQ_GRID_P", 3);
+  const int p = genv("GQ_GRID_P", 2);
   if (mode == kDelta) {
     if (p == 2) return grid_launch<kDelta, 2>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
     if (p == 4) return grid_launch<kDelta, 4>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
