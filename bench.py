@@ -52,7 +52,9 @@ def kernel_passes(name):
     if name == "delta":
         return 2                       # read d, write y (+ y.d)
     if name == "update":
-        return 6                       # read x, r, d, y; write x, r (+ max|r|)
+        return 3                       # read r, y; write r (+ max|r|)
+    if name == "update_x":
+        return 3                       # read x, d; write x (parallel graph branch)
     if name == "dirupdate":
         return 3                       # read q, d; write d
     if name == "dot":

@@ -39,6 +39,8 @@ struct gq_ctx {
   Geo g{};
   int m = 0, L = 2, S = 2, n_dyn = 0, n_cost = 0, npc = 0, nxc = 0, sm_count = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;          // parallel graph branch (x update)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double *A = nullptr, *B = nullptr, *R = nullptr, *C = nullptr, *Q = nullptr;
   double *qinv = nullptr, *rinv = nullptr, *brb = nullptr;
   double *psi = nullptr, *xi = nullptr, *xit = nullptr, *fac = nullptr;
@@ -100,6 +102,9 @@ static void release(gq_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   delete c;
 }
 
@@ -255,6 +260,9 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       return bail(fail(GQ_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_))); \
   } while (0)
   CKB(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CKB(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CKB(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CKB(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CKB(dalloc(&c->A, D.n_dyn * nk * nn));
   CKB(dalloc(&c->B, D.n_dyn * nk * n * m));
   CKB(dalloc(&c->R, D.n_dyn * nk * m * m));
@@ -320,21 +328,28 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
     CKB(cudaStreamSynchronize(c->stream));
     c->fo = FastOps{c->oprow, c->omega, c->fac3, c->psi_cls, c->fac4};
     if (chain_supported(g.n)) {
-      // class-pure chunks of <= 8 stages: runs of equal Psi class split into 8s
-      std::vector<int4> segs;
-      for (int t = 0; t < g.T1;) {
-        int e = t + 1;
-        while (e < g.T1 && e - t < 8 && pcls[e] == pcls[t]) ++e;
-        segs.push_back(make_int4(t, e - t, pcls[t], 0));
-        t = e;
-      }
+      // class-pure chunks of <= w stages: runs of equal Psi class split into w's
+      auto chunks = [&](int w) {
+        std::vector<int4> segs;
+        for (int t = 0; t < g.T1;) {
+          int e = t + 1;
+          while (e < g.T1 && e - t < w && pcls[e] == pcls[t]) ++e;
+          segs.push_back(make_int4(t, e - t, pcls[t], 0));
+          t = e;
+        }
+        return segs;
+      };
+      const std::vector<int4> s8 = chunks(8), s16 = chunks(16);
       CKB(dalloc(&c->cff, chain_ff_doubles(g, c->npc)));
       CKB(dalloc(&c->cfb, chain_fb_doubles(g, c->npc)));
-      CKB(dalloc(&c->seg, segs.size()));
-      CKB(cudaMemcpy(c->seg, segs.data(), segs.size() * sizeof(int4), cudaMemcpyHostToDevice));
+      CKB(dalloc(&c->seg, s8.size() + s16.size()));
+      CKB(cudaMemcpy(c->seg, s8.data(), s8.size() * sizeof(int4), cudaMemcpyHostToDevice));
+      CKB(cudaMemcpy(c->seg + s8.size(), s16.data(), s16.size() * sizeof(int4),
+                     cudaMemcpyHostToDevice));
       CKB(launch_build_chain(g, c->npc, c->fac, c->omega, c->cff, c->cfb, c->stream));
       CKB(cudaStreamSynchronize(c->stream));
-      c->co = ChainOps{c->cff, c->cfb, c->seg, (int)segs.size()};
+      c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
+                       (int)s16.size()};
       c->chain = true;
     }
   }
@@ -517,7 +532,25 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
                       kDotStep, c->stream));
   if (names) names->push_back("delta");
   if ((rc = mark())) return rc;
-  CK(launch_update(c->g, c->x, c->r, c->d, c->y, c->vblocks, c->partials, c->st, c->stream));
+  // x += alpha d only feeds the result: it runs on a parallel branch of the step graph,
+  // overlapping the r update and the sweeps, and joins before d is overwritten.  Profiled
+  // (evs != null) steps run it in line so it gets its own timing.
+  static const bool no_fork = [] {
+    const char* e = getenv("GQ_NO_FORK");
+    return e && *e == '1';
+  }();
+  const bool fork = evs == nullptr && !no_fork;
+  if (fork) {
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    CK(launch_update_x(c->g, c->x, c->d, c->vblocks, c->st, c->side));
+    CK(cudaEventRecord(c->ev_join, c->side));
+  } else {
+    CK(launch_update_x(c->g, c->x, c->d, c->vblocks, c->st, c->stream));
+    if (names) names->push_back("update_x");
+    if ((rc = mark())) return rc;
+  }
+  CK(launch_update_r(c->g, c->r, c->y, c->vblocks, c->partials, c->st, c->stream));
   if (names) names->push_back("update");
   if ((rc = mark())) return rc;
   const double* qv = c->q;
@@ -531,6 +564,7 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
     if ((rc = mark())) return rc;
     qv = c->r;
   }
+  if (fork) CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   CK(launch_dirupdate(c->g, c->d, qv, c->vblocks, c->st, c->stream));
   if (names) names->push_back("dirupdate");
   return mark();
@@ -538,8 +572,8 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
 
 extern "C" int gq_launches_per_step(gq_ctx* c) {
   if (!c) return -1;
-  if (!c->use_precond) return 4;
-  return 3 + c->S * c->L + (c->fast ? c->S - 1 : 0);
+  if (!c->use_precond) return 5;
+  return 4 + c->S * c->L + (c->fast ? c->S - 1 : 0);
 }
 
 extern "C" int gq_pcg_start(gq_ctx* c, const double* rhs, const double* x0, int32_t use_precond) {

@@ -84,7 +84,7 @@ __device__ bool warp_grid_sum(double v, double* partials, unsigned int* counter,
 
 }  // namespace
 
-template <int NS, bool INNER>
+template <int NS, bool INNER, int MT = 1>
 struct Ch {
   static constexpr int Q = 4 * NS, QQ = Q * Q, NT = Q / 8;
   static constexpr int TC = 12 * NS;                  // theta feature count
@@ -92,28 +92,33 @@ struct Ch {
   static constexpr int FFS = 2 * QQ + Q * TC;         // forward factor doubles per block
   static constexpr int FF = INNER ? FFS : 2 * QQ;     // ... staged by this variant
   static constexpr int FB = 2 * QQ;                   // backward factor doubles per block
-  static constexpr int REC = 8 * NS;                  // record: 8 stages x NS
+  static constexpr int ST = 8 * MT;                   // chains (stages) per warp
+  static constexpr int REC = ST * NS;                 // record: ST stages x NS
   static constexpr int CPR = REC / 2;                 // 16-byte chunks per record
   static constexpr int RPI = 32 / CPR;                // records per warp instruction
   static constexpr int NRF = INNER ? 16 : 4;          // forward records: tau(4) + theta(12)
   static constexpr int JF = NRF / RPI, JB = 8 / RPI;  // record instructions fwd / bwd (w + r)
   static constexpr int CFF = FF / 64, CFB = FB / 64;  // factor instructions (32 x 16 B each)
-  static constexpr int SLOT = (NRF * REC + FF) > (8 * REC + FB) ? (NRF * REC + FF) : (8 * REC + FB);
+  // record stride in shared memory: padded by 16*NS bytes so the A-fragment reads of a
+  // quarter warp (4 records x 2 chains) hit 8 distinct 16-byte bank groups
+  static constexpr int RSTR = REC + 2 * NS;
+  static constexpr int SLOT = (NRF * RSTR + FF) > (8 * RSTR + FB) ? (NRF * RSTR + FF) : (8 * RSTR + FB);
   static_assert(NS == 2 || NS == 4, "chain sweep needs n in {2, 4}");
+  static_assert(CPR <= 32 && 32 % CPR == 0, "a record must split evenly over the warp");
   static_assert(FF % 64 == 0 && FB % 64 == 0, "factor blocks must be whole warp copies");
 };
 
 using namespace as;
 
-template <int NS, bool INNER, int P>
+template <int NS, bool INNER, int P, int MT>
 __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            const double* __restrict__ rhs,
                                            const double* __restrict__ th, double* out,
                                            const double* __restrict__ rdot, bool dotting,
                                            double* ring, int v, int t0, int nvalid, int cls,
                                            uint64_t pol_s, uint64_t pol_k, double& dot) {
-  using C = Ch<NS, INNER>;
-  constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::REC, R = P + 1;
+  using C = Ch<NS, INNER, MT>;
+  constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::RSTR, R = P + 1;
   const int lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
   const long long rs = (long long)g.T1 * NS;
   const long long cs = (long long)g.K * rs;
@@ -127,6 +132,8 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   const bool stage_ok = wst < nvalid;
   const int wofs = stage_ok ? 2 * wch : 0;               // stage-invalid lanes read stage 0
   const unsigned ring_u = smem_u32(ring);
+  // A-fragment offset of feature pair f0 = 8p + 2qd for chain (8m + rw) inside a record slot
+  auto aofs = [&](int rec, int m, int f0) { return (rec + f0 / NS) * REC + (8 * m + rw) * NS + (f0 % NS); };
 
   // ---------------- forward ----------------
   const double* fsrc[C::JF];
@@ -165,20 +172,26 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       ldgsts(facf_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
   };
 
-  double2 wd[NT];
+  double2 wd[MT][NT];
 #pragma unroll
-  for (int h = 0; h < NT; ++h) wd[h] = make_double2(0.0, 0.0);
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int h = 0; h < NT; ++h) wd[m][h] = make_double2(0.0, 0.0);
 
-  // output fragment addressing: lane holds features 8h + 2qd, +1 of chain (stage) rw
-  long long oofs[NT];
-  bool ook[NT];
+  // output fragment addressing: lane holds features 8h + 2qd, +1 of chain (stage) 8m + rw
+  long long oofs[MT][NT];
+  bool ook[MT][NT];
   int orow[NT];
 #pragma unroll
   for (int h = 0; h < NT; ++h) {
     const int f0 = 8 * h + 2 * qd, nd = f0 / NS, cc = f0 % NS;
-    oofs[h] = col_a + (long long)(nd & 1) * cs + (long long)(nd >> 1) * rs + rw * NS + cc;
-    ook[h] = rw < nvalid && ((nd & 1) ? okb : true);
     orow[h] = nd >> 1;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      oofs[m][h] = col_a + (long long)(nd & 1) * cs + (long long)(nd >> 1) * rs +
+                   (8 * m + rw) * NS + cc;
+      ook[m][h] = 8 * m + rw < nvalid && ((nd & 1) ? okb : true);
+    }
   }
 
   {
@@ -195,7 +208,6 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   const double* fcur[C::JF];
 #pragma unroll
   for (int j = 0; j < C::JF; ++j) fcur[j] = fsz[j] ? fsrc[j] + (long long)P * rs2 : rhs;
-  const long long fstep = rs2;
   const double* fpc = ffb + (long long)P * C::FFS;
 
   int slot = 0, islot = P % R;
@@ -218,69 +230,77 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     commit();
 #pragma unroll
     for (int j = 0; j < C::JF; ++j)
-      if (fsz[j]) fcur[j] += fstep;
+      if (fsz[j]) fcur[j] += rs2;
     fpc += C::FFS;
     wait_groups<P>();
     __syncwarp();
 
     const double* sl = ring + slot * C::SLOT;
     const double* sf = sl + C::NRF * REC;
-    // A operands: tau k-pairs and theta k-pairs (feature pair 8p + 2qd of chain rw)
-    double2 tv[NT];
+    // A operands: tau k-pairs and theta k-pairs of every M-tile
+    double2 tv[MT][NT];
 #pragma unroll
-    for (int p = 0; p < NT; ++p) {
-      const int f0 = 8 * p + 2 * qd;
-      tv[p] = lds2(sl + (f0 / NS) * REC + rw * NS + (f0 % NS));
-    }
-    double2 thv[INNER ? KT : 1];
-    if (INNER) {
+    for (int m = 0; m < MT; ++m)
 #pragma unroll
-      for (int p = 0; p < KT; ++p) {
-        const int f0 = 8 * p + 2 * qd;
-        thv[p] = lds2(sl + (4 + f0 / NS) * REC + rw * NS + (f0 % NS));
-      }
-    }
-    double2 wn[NT];
+      for (int p = 0; p < NT; ++p) tv[m][p] = lds2(sl + aofs(0, m, 8 * p + 2 * qd));
+    double2 wn[MT][NT];
 #pragma unroll
     for (int h = 0; h < NT; ++h) {
-      double2 a0 = make_double2(0.0, 0.0), a1 = a0, g0 = a0, g1 = a0;
-      double2 m0 = a0, m1 = a0, m2 = a0, m3 = a0;
+      double2 a0[MT], a1[MT], g0[MT], g1[MT], m0[MT], m1[MT], m2[MT], m3[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+        a0[m] = a1[m] = g0[m] = g1[m] = m0[m] = m1[m] = m2[m] = m3[m] = make_double2(0.0, 0.0);
 #pragma unroll
       for (int p = 0; p < NT; ++p) {
         const double2 b = lds2(sf + (h * NT + p) * 64 + rw * 8 + 2 * qd);
-        dmma(a0, tv[p].x, b.x);
-        dmma(a1, tv[p].y, b.y);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          dmma(a0[m], tv[m][p].x, b.x);
+          dmma(a1[m], tv[m][p].y, b.y);
+        }
       }
       if (INNER) {
 #pragma unroll
         for (int p = 0; p < KT; ++p) {
           const double2 b = lds2(sf + 2 * QQ + (h * KT + p) * 64 + rw * 8 + 2 * qd);
-          if (p & 1) {
-            dmma(m2, thv[p].x, b.x);
-            dmma(m3, thv[p].y, b.y);
-          } else {
-            dmma(m0, thv[p].x, b.x);
-            dmma(m1, thv[p].y, b.y);
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const double2 tq = lds2(sl + aofs(4, m, 8 * p + 2 * qd));
+            if (p & 1) {
+              dmma(m2[m], tq.x, b.x);
+              dmma(m3[m], tq.y, b.y);
+            } else {
+              dmma(m0[m], tq.x, b.x);
+              dmma(m1[m], tq.y, b.y);
+            }
           }
         }
       }
 #pragma unroll
       for (int p = 0; p < NT; ++p) {
         const double2 b = lds2(sf + QQ + (h * NT + p) * 64 + rw * 8 + 2 * qd);
-        dmma(g0, wd[p].x, b.x);
-        dmma(g1, wd[p].y, b.y);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          dmma(g0[m], wd[m][p].x, b.x);
+          dmma(g1[m], wd[m][p].y, b.y);
+        }
       }
-      double2 s = add2(a0, a1);
-      if (INNER) s = add2(s, add2(add2(m0, m1), add2(m2, m3)));
-      wn[h] = add2(s, add2(g0, g1));
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        double2 sm = add2(a0[m], a1[m]);
+        if (INNER) sm = add2(sm, add2(add2(m0[m], m1[m]), add2(m2[m], m3[m])));
+        wn[m][h] = add2(sm, add2(g0[m], g1[m]));
+      }
     }
     const bool lastk = k == nb - 1;
 #pragma unroll
-    for (int h = 0; h < NT; ++h) {
-      wd[h] = wn[h];
-      if (ook[h] && !(lastk && 2 * k + orow[h] >= K))
-        stg2_keep(out + oofs[h] + (long long)k * rs2, wn[h], pol_k);
-    }
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int h = 0; h < NT; ++h) {
+        wd[m][h] = wn[m][h];
+        if (ook[m][h] && !(lastk && 2 * k + orow[h] >= K))
+          stg2_keep(out + oofs[m][h] + (long long)k * rs2, wn[m][h], pol_k);
+      }
     slot = slot + 1 == R ? 0 : slot + 1;
     islot = islot + 1 == R ? 0 : islot + 1;
     __syncwarp();
@@ -332,9 +352,11 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     bcur[j] = bsz[j] ? bsrc[j] + (long long)(nb - 1 - P) * rs2 : rhs;
   const double* fbc = fbb + (long long)(nb - 1 - P) * C::FB;
 
-  double2 xd[NT];
+  double2 xd[MT][NT];
 #pragma unroll
-  for (int h = 0; h < NT; ++h) xd[h] = make_double2(0.0, 0.0);
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int h = 0; h < NT; ++h) xd[m][h] = make_double2(0.0, 0.0);
   slot = 0;
   islot = P % R;
 #pragma unroll 1
@@ -359,44 +381,53 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
 
     const double* sl = ring + slot * C::SLOT;
     const double* sf = sl + 8 * REC;
-    double2 wv[NT];
+    double2 wv[MT][NT];
 #pragma unroll
-    for (int p = 0; p < NT; ++p) {
-      const int f0 = 8 * p + 2 * qd;
-      wv[p] = lds2(sl + (f0 / NS) * REC + rw * NS + (f0 % NS));
-    }
-    double2 xn[NT];
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int p = 0; p < NT; ++p) wv[m][p] = lds2(sl + aofs(0, m, 8 * p + 2 * qd));
+    double2 xn[MT][NT];
 #pragma unroll
     for (int h = 0; h < NT; ++h) {
-      double2 a0 = make_double2(0.0, 0.0), a1 = a0, g0 = a0, g1 = a0;
+      double2 a0[MT], a1[MT], g0[MT], g1[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) a0[m] = a1[m] = g0[m] = g1[m] = make_double2(0.0, 0.0);
 #pragma unroll
       for (int p = 0; p < NT; ++p) {
         const double2 b = lds2(sf + (h * NT + p) * 64 + rw * 8 + 2 * qd);
-        dmma(a0, wv[p].x, b.x);
-        dmma(a1, wv[p].y, b.y);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          dmma(a0[m], wv[m][p].x, b.x);
+          dmma(a1[m], wv[m][p].y, b.y);
+        }
       }
 #pragma unroll
       for (int p = 0; p < NT; ++p) {
         const double2 b = lds2(sf + QQ + (h * NT + p) * 64 + rw * 8 + 2 * qd);
-        dmma(g0, xd[p].x, b.x);
-        dmma(g1, xd[p].y, b.y);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          dmma(g0[m], xd[m][p].x, b.x);
+          dmma(g1[m], xd[m][p].y, b.y);
+        }
       }
-      xn[h] = add2(add2(a0, a1), add2(g0, g1));
+#pragma unroll
+      for (int m = 0; m < MT; ++m) xn[m][h] = add2(add2(a0[m], a1[m]), add2(g0[m], g1[m]));
     }
     const bool lastk = k == nb - 1;
 #pragma unroll
-    for (int h = 0; h < NT; ++h) {
-      xd[h] = xn[h];
-      if (ook[h] && !(lastk && 2 * k + orow[h] >= K)) {
-        *reinterpret_cast<double2*>(out + oofs[h] + (long long)k * rs2) = xn[h];
-        if (dotting) {
-          const int f0 = 8 * h + 2 * qd;
-          const double2 rv = lds2(sl + (4 + f0 / NS) * REC + rw * NS + (f0 % NS));
-          dot = fma(xn[h].x, rv.x, dot);
-          dot = fma(xn[h].y, rv.y, dot);
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int h = 0; h < NT; ++h) {
+        xd[m][h] = xn[m][h];
+        if (ook[m][h] && !(lastk && 2 * k + orow[h] >= K)) {
+          *reinterpret_cast<double2*>(out + oofs[m][h] + (long long)k * rs2) = xn[m][h];
+          if (dotting) {
+            const double2 rv = lds2(sl + aofs(4, m, 8 * h + 2 * qd));
+            dot = fma(xn[m][h].x, rv.x, dot);
+            dot = fma(xn[m][h].y, rv.y, dot);
+          }
         }
       }
-    }
     slot = slot + 1 == R ? 0 : slot + 1;
     islot = islot + 1 == R ? 0 : islot + 1;
     __syncwarp();
@@ -405,7 +436,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   __syncwarp();
 }
 
-template <int NS, bool INNER, int P>
+template <int NS, bool INNER, int P, int MT>
 __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* __restrict__ rhs,
                                               const double* __restrict__ th, double* out,
                                               const double* __restrict__ rdot, int n_items,
@@ -414,13 +445,15 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
   if (halted(st)) return;
   const uint64_t pol_s = pol_first(), pol_k = pol_last();
   const bool dotting = dotmode != kDotNone;
+  const int nseg = MT == 1 ? co.nseg : co.nseg16;
+  const int4* seg = MT == 1 ? co.seg : co.seg16;
   double dot = 0.0;
 #pragma unroll 1
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int v = item / co.nseg;
-    const int4 sg = co.seg[item - v * co.nseg];
-    chain_item<NS, INNER, P>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x, sg.y, sg.z,
-                             pol_s, pol_k, dot);
+    const int v = item / nseg;
+    const int4 sg = seg[item - v * nseg];
+    chain_item<NS, INNER, P, MT>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x, sg.y, sg.z,
+                                 pol_s, pol_k, dot);
   }
   if (dotting) {
     double mu;
@@ -523,50 +556,64 @@ cudaError_t launch_build_chain(const Geo& g, int npc, const double* fac, const d
   return cudaGetLastError();
 }
 
-template <int NS, bool INNER, int P>
+template <int NS, bool INNER, int P, int MT>
 static cudaError_t chain_launch(const Geo& g, const ChainOps& co, const double* rhs,
                                 const double* th, double* out, const double* rdot, int sm_count,
                                 double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  constexpr size_t smem = (size_t)(P + 1) * Ch<NS, INNER>::SLOT * sizeof(double);
-  const int n_items = g.V * co.nseg;
-  static int attr_done = 0;
+  constexpr size_t smem = (size_t)(P + 1) * Ch<NS, INNER, MT>::SLOT * sizeof(double);
+  const int n_items = g.V * (MT == 1 ? co.nseg : co.nseg16);
+  static int attr_done = 0, per_sm = 0;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_chain<NS, INNER, P>,
+    cudaError_t e = cudaFuncSetAttribute(k_chain<NS, INNER, P, MT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain<NS, INNER, P, MT>, 32, smem);
+    per_sm = std::max(per_sm, 1);
     attr_done = 1;
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain<NS, INNER, P>, 32, smem);
-  const int want = env_or("GQ_CHAIN_WARPS", 0);
-  if (want > 0) per_sm = std::min(per_sm, want);
-  const int blocks = std::max(1, std::min(n_items, std::max(per_sm, 1) * sm_count));
-  k_chain<NS, INNER, P><<<blocks, 32, smem, s>>>(g, co, rhs, th, out, rdot, n_items, partials,
-                                                  st, dotmode);
+  int cap = per_sm;
+  const int want = env_or(INNER ? "GQ_CHAIN_WARPS_INNER" : "GQ_CHAIN_WARPS_OUTER",
+                          env_or("GQ_CHAIN_WARPS", 0));
+  if (want > 0) cap = std::min(cap, want);
+  const int blocks = std::max(1, std::min(n_items, cap * sm_count));
+  k_chain<NS, INNER, P, MT><<<blocks, 32, smem, s>>>(g, co, rhs, th, out, rdot, n_items,
+                                                      partials, st, dotmode);
   return cudaGetLastError();
 }
 
-template <int NS, bool INNER>
+template <int NS, bool INNER, int MT>
 static cudaError_t chain_p(const Geo& g, const ChainOps& co, const double* rhs, const double* th,
                            double* out, const double* rdot, int sm_count, double* partials,
                            PcgState* st, int dotmode, cudaStream_t s) {
-  switch (env_or("GQ_CHAIN_P", NS == 2 ? 3 : 2)) {
-    case 1: return chain_launch<NS, INNER, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    case 2: return chain_launch<NS, INNER, 2>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    case 4: return chain_launch<NS, INNER, 4>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    default: return chain_launch<NS, INNER, 3>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  switch (env_or("GQ_CHAIN_P", 3)) {
+    case 2: return chain_launch<NS, INNER, 2, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    case 5: return chain_launch<NS, INNER, 5, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    case 7: return chain_launch<NS, INNER, 7, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    default: break;
   }
+  return chain_launch<NS, INNER, 3, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+}
+
+template <int NS, bool INNER>
+static cudaError_t chain_mt(const Geo& g, const ChainOps& co, const double* rhs, const double* th,
+                            double* out, const double* rdot, int sm_count, double* partials,
+                            PcgState* st, int dotmode, cudaStream_t s) {
+  if constexpr (NS == 2) {
+    if (env_or("GQ_CHAIN_MT", 1) == 2)
+      return chain_p<NS, INNER, 2>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  }
+  return chain_p<NS, INNER, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
 }
 
 cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
                          const double* th, double* out, const double* rdot, int sm_count,
                          double* partials, PcgState* st, int dotmode, cudaStream_t s) {
   if (g.n == 2)
-    return inner ? chain_p<2, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
-                 : chain_p<2, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    return inner ? chain_mt<2, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                 : chain_mt<2, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 4)
-    return inner ? chain_p<4, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
-                 : chain_p<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    return inner ? chain_mt<4, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                 : chain_mt<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   return cudaErrorInvalidValue;
 }
 

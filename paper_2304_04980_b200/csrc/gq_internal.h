@@ -78,6 +78,8 @@ struct ChainOps {
   const double* fb;    // [npc][V][nb] L^-T | -H                  (8x8 tiles)
   const int4* seg;     // [nseg] (t0, nvalid <= 8, psi class, 0): class-pure stage chunks
   int nseg;
+  const int4* seg16;   // [nseg16] the same with chunks of <= 16 stages (two M-tiles per warp)
+  int nseg16;
 };
 bool chain_supported(int n);
 size_t chain_ff_doubles(const Geo& g, int npc);
@@ -104,6 +106,10 @@ cudaError_t launch_grid(const Geo& g, const FastOps& fo, int mode, const double*
 int vec_blocks(int sm_count);
 cudaError_t launch_update(const Geo& g, double* x, double* r, const double* d, const double* y,
                           int blocks, double* partials, PcgState* st, cudaStream_t s);
+cudaError_t launch_update_r(const Geo& g, double* r, const double* y, int blocks,
+                            double* partials, PcgState* st, cudaStream_t s);
+cudaError_t launch_update_x(const Geo& g, double* x, const double* d, int blocks, PcgState* st,
+                            cudaStream_t s);
 cudaError_t launch_dirupdate(const Geo& g, double* d, const double* q, int blocks,
                              PcgState* st, cudaStream_t s);
 cudaError_t launch_dot(const Geo& g, const double* a, const double* b, int blocks,

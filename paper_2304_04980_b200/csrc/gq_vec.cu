@@ -74,6 +74,89 @@ __global__ void __launch_bounds__(256) k_update(long long dim, double* __restric
   }
 }
 
+// r = r - alpha y and ||r||_inf only (the x update runs on a parallel graph branch)
+__global__ void __launch_bounds__(256) k_update_r(long long dim, double* __restrict__ r,
+                                                  const double* __restrict__ y, double* partials,
+                                                  PcgState* st) {
+  if (halted(st)) return;
+  const double alpha = st->alpha;
+  double m = 0.0;
+  const long long n2 = dim >> 1;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long b = tid; b < n2; b += nth * kVU) {
+    double2 rv[kVU], yv[kVU];
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        yv[u] = ld_stream(y + e);
+        rv[u] = *reinterpret_cast<const double2*>(r + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        rv[u].x = __dsub_rn(rv[u].x, __dmul_rn(alpha, yv[u].x));    // pcg.py:111
+        rv[u].y = __dsub_rn(rv[u].y, __dmul_rn(alpha, yv[u].y));
+        *reinterpret_cast<double2*>(r + e) = rv[u];
+        m = nmax(m, nmax(fabs(rv[u].x), fabs(rv[u].y)));           // pcg.py:113
+      }
+    }
+  }
+  if ((dim & 1) && tid == 0) {
+    const long long e = dim - 1;
+    const double rn = __dsub_rn(r[e], __dmul_rn(alpha, y[e]));
+    r[e] = rn;
+    m = nmax(m, fabs(rn));
+  }
+  double res;
+  if (grid_reduce<true>(m, partials, &st->counter[1], res) && threadIdx.x == 0) {
+    st->res = res;
+    st->hist[st->step] = res;
+    st->step += 1;
+    if (res < st->tol) {            // pcg.py:119-121
+      st->converged = 1;
+      st->done = 1;
+    }
+  }
+}
+
+// x = x + alpha d (pcg.py:109).  Runs concurrently with the r update and the sweeps of the
+// same step, so it must not look at `done` (the r update may set it for this very step,
+// whose x update still belongs to the result); `skip` (set by the step's first kernel) and
+// `breakdown` (set by the curvature reduction before alpha) are the only stops.
+__global__ void __launch_bounds__(256) k_update_x(long long dim, double* __restrict__ x,
+                                                  const double* __restrict__ d, PcgState* st) {
+  if (st->skip || st->breakdown) return;
+  const double alpha = st->alpha;
+  const long long n2 = dim >> 1;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long b = tid; b < n2; b += nth * kVU) {
+    double2 xv[kVU], dv[kVU];
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        dv[u] = ld_stream(d + e);
+        xv[u] = ld_stream(x + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        xv[u].x = __dadd_rn(xv[u].x, __dmul_rn(alpha, dv[u].x));
+        xv[u].y = __dadd_rn(xv[u].y, __dmul_rn(alpha, dv[u].y));
+        __stcs(reinterpret_cast<double2*>(x + e), xv[u]);
+      }
+    }
+  }
+  if ((dim & 1) && tid == 0) x[dim - 1] = __dadd_rn(x[dim - 1], __dmul_rn(alpha, d[dim - 1]));
+}
+
 __global__ void __launch_bounds__(256) k_dirupdate(long long dim, double* __restrict__ d,
                                                    const double* __restrict__ q, PcgState* st) {
   if (halted(st)) return;
@@ -134,6 +217,18 @@ __global__ void __launch_bounds__(256) k_sub(long long dim, double* __restrict__
 cudaError_t launch_update(const Geo& g, double* x, double* r, const double* d, const double* y,
                           int blocks, double* partials, PcgState* st, cudaStream_t s) {
   k_update<<<blocks, 256, 0, s>>>(g.dim, x, r, d, y, partials, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_r(const Geo& g, double* r, const double* y, int blocks,
+                            double* partials, PcgState* st, cudaStream_t s) {
+  k_update_r<<<blocks, 256, 0, s>>>(g.dim, r, y, partials, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_x(const Geo& g, double* x, const double* d, int blocks, PcgState* st,
+                            cudaStream_t s) {
+  k_update_x<<<blocks, 256, 0, s>>>(g.dim, x, d, st);
   return cudaGetLastError();
 }
 
