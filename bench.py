@@ -142,6 +142,19 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(value, device, ws):
+    """Replica timing: every rank times its own solve; the job's time is the slowest rank
+    (device-timed values reduced with MAX over the process group)."""
+    if ws <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(value)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def traffic_from_profiles(kernel):
     """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -197,11 +210,8 @@ def run_ours(args, ws, rank, local):
         torch.cuda.synchronize()
     assert rc in (_lib.GQ_OK, _lib.GQ_MAX_ITER), _lib.last_error()
     assert steps.value == W + K, (steps.value, W + K)
-    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(e0.elapsed_time(e1), dev, ws)
     if ws > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.barrier()
     hist = np.empty(W + K)
     _lib.check(lib.gq_pcg_history(ctx.h, hist.ctypes.data, W + K))
@@ -236,10 +246,7 @@ def run_ours(args, ws, rank, local):
         x_out = exc.iterate
     e2e_s = time.perf_counter() - t0
     assert x_out.shape == (dim,)
-    if ws > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(e2e_s, dev, ws)
 
     line = {
         "metric": METRIC,
