@@ -57,7 +57,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     for job in jobs:
         lint_sass(job[-1])
     if force or jobs or not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
-        run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
+        run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread"])
     return LIB
 
 

@@ -64,6 +64,7 @@ struct PcgState {
   double* hist;
   int done, converged, breakdown;
   int skip;   // set by the first kernel of a step when the step budget is exhausted
+  int nonfinite;   // set by the rhs check of gq_pcg_start
   unsigned int counter[4];
 };
 

@@ -106,6 +106,8 @@ cudaError_t launch_grid(const Geo& g, const FastOps& fo, int mode, const double*
 int vec_blocks(int sm_count);
 cudaError_t launch_update(const Geo& g, double* x, double* r, const double* d, const double* y,
                           int blocks, double* partials, PcgState* st, cudaStream_t s);
+cudaError_t launch_nonfinite(const Geo& g, const double* v, int blocks, PcgState* st,
+                             cudaStream_t s);
 cudaError_t launch_update_r(const Geo& g, double* r, const double* y, int blocks,
                             double* partials, PcgState* st, cudaStream_t s);
 cudaError_t launch_update_x(const Geo& g, double* x, const double* d, int blocks, PcgState* st,

@@ -220,6 +220,23 @@ cudaError_t launch_update(const Geo& g, double* x, double* r, const double* d, c
   return cudaGetLastError();
 }
 
+// any non-finite entry -> st->nonfinite = 1 (pcg.py:65-66 check, done on the device so the
+// host never scans the 210 MB right-hand side)
+__global__ void __launch_bounds__(256) k_nonfinite(long long dim, const double* __restrict__ v,
+                                                   PcgState* st) {
+  bool bad = false;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride)
+    bad |= !isfinite(v[e]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) st->nonfinite = 1;
+}
+
+cudaError_t launch_nonfinite(const Geo& g, const double* v, int blocks, PcgState* st,
+                             cudaStream_t s) {
+  k_nonfinite<<<blocks, 256, 0, s>>>(g.dim, v, st);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_update_r(const Geo& g, double* r, const double* y, int blocks,
                             double* partials, PcgState* st, cudaStream_t s) {
   k_update_r<<<blocks, 256, 0, s>>>(g.dim, r, y, partials, st);
