@@ -323,10 +323,13 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   if (c->fast) {
     CKB(dalloc(&c->oprow, (size_t)c->npc * nk * 23 * nn));
     CKB(dalloc(&c->omega, (size_t)c->npc * nk * 5 * nn));
-    if (tc_supported(g.n))
-      CKB(dalloc(&c->fac4, (size_t)c->npc * g.V * g.nb * 4 * q * q));
-    else
-      CKB(dalloc(&c->fac3, (size_t)c->npc * g.V * g.nb * 3 * q * q));
+    // per-lane sweep factors: only needed when the chain kernel does not run the sweeps
+    if (!chain_supported(g.n)) {
+      if (tc_supported(g.n))
+        CKB(dalloc(&c->fac4, (size_t)c->npc * g.V * g.nb * 4 * q * q));
+      else
+        CKB(dalloc(&c->fac3, (size_t)c->npc * g.V * g.nb * 3 * q * q));
+    }
     CKB(launch_build_fast(g, c->npc, c->op, c->oprow, c->omega, c->fac3, c->fac4, c->stream));
     CKB(cudaStreamSynchronize(c->stream));
     c->fo = FastOps{c->oprow, c->omega, c->fac3, c->psi_cls, c->fac4};

@@ -1281,498 +1281,6 @@ __global__ void __launch_bounds__(32) k_sweep6(Geo g, FastOps fo, const double* 
 }
 
 
-// ---- TMA bulk-copy helpers --------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
-      "%2, [%3], %4;\n" ::"r"(su32(dst)),
-      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(su32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// bounded wait: a protocol bug traps (launch error) instead of hanging the device
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  for (long long i = 0; !mbar_try(bar, parity); ++i)
-    if (i > (1LL << 28)) __trap();
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async;\n" ::: "memory");
-}
-
-// ---- sweep v8: CTA-cooperative, warp-specialised TMA pipeline ----------------------------
-// One CTA = one column pair x S = 8W consecutive stages (W consumer warps of 8 chains each,
-// plus one producer warp).  Per block the producer lane issues one cp.async.bulk per record
-// (S stages x n doubles of one node: ~1 KB contiguous in the stage-inner layout) and ONE
-// copy of the factor block (and omega rows) shared by all consumer warps, completing on a
-// per-slot `full` mbarrier; consumers release slots through an `empty` mbarrier.  This
-// replaces v6's per-lane cp.async, whose thousands of 16-byte requests clogged the LSU
-// (measured: ~660 cycles to issue 3 LDGSTS, ~800 cycles for the following LDS).
-template <int NS, bool INNER>
-struct Sw8 {
-  static constexpr int Q = 4 * NS, QQ = Q * Q, B2 = NS * NS, NT = Q / 8;
-  static constexpr int NRF = INNER ? 16 : 4;
-  static constexpr int NR = NRF > 8 ? NRF : 8;
-  static constexpr int FAC = 2 * QQ;
-  static constexpr int OMG = INNER ? Even<4 * 5 * B2>::v : 0;
-};
-
-struct Sw8Geo {
-  int W;        // consumer warps
-  int S;        // stages per item (8W)
-  int R;        // ring slots
-  int RECC;     // doubles per record (S * n)
-  int SLOT;     // doubles per slot
-  int nchunk;   // stage chunks per pair
-};
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
-}
-
-template <int NS, bool INNER, bool TWOW>
-__device__ __forceinline__ void sweep8_warp_item(
-    const Geo& g, const Sw8Geo& sg, double* out, int dotmode, double* ring, uint64_t* full,
-    uint64_t* empty, const double* zrec, uint32_t& nuse, int lane, int wid, int v, int t0,
-    int cA, int cB, int fsel, const int cls, const bool tvr, uint64_t pol_keep, double& dot) {
-  using C = Sw8<NS, INNER>;
-  constexpr int Q = C::Q, QQ = C::QQ, B2 = C::B2, NT = C::NT;
-  const int qd = lane & 3, rw = lane >> 2;
-  const int RECC = sg.RECC, SLOT = sg.SLOT, R = sg.R;
-  const long long rs = (long long)g.T1 * NS;
-  const long long cs = (long long)g.K * g.T1 * NS;
-  const long long rs2 = 2 * rs;
-  const int a = 2 * v;
-  const bool okb = a + 1 < g.N;
-  const int nb = g.nb;
-  const int srow = 8 * wid + rw;                   // this lane's stage row inside records
-  const long long col_a = (long long)a * g.K * g.T1 * NS + (long long)(t0 + srow) * NS;
-  const int tr[12] = {0, 1, -1, 0, 1, 2, -1, 0, 1, 2, 0, 1};
-  const int tc[12] = {-2, -2, -1, -1, -1, -1, 2, 2, 2, 2, 3, 3};
-  int nd[NT], co[NT];
-#pragma unroll
-  for (int h = 0; h < NT; ++h) {
-    nd[h] = (8 * h + 2 * qd) / NS;
-    co[h] = (8 * h + 2 * qd) % NS;
-  }
-  double* optr[NT];
-  bool ostore[NT];
-  int bofs[NT];
-#pragma unroll
-  for (int h = 0; h < NT; ++h) {
-    optr[h] = out + col_a + (nd[h] & 1) * cs + (nd[h] >> 1) * rs + co[h];
-    ostore[h] = tvr && ((nd[h] & 1) ? okb : true);
-    bofs[h] = nd[h] * RECC + srow * NS + co[h];
-  }
-  int fofs[NT][NT];
-#pragma unroll
-  for (int h = 0; h < NT; ++h)
-#pragma unroll
-    for (int s2 = 0; s2 < NT; ++s2) fofs[h][s2] = (8 * h + rw) * Q + 8 * s2 + 2 * qd;
-  const int osel = TWOW ? (cls == cB ? 1 : 0) : fsel;
-  auto node_ok = [&](int ndv, int k) {
-    return ((ndv & 1) ? okb : true) && (2 * k + (ndv >> 1) < g.K);
-  };
-  auto acquire = [&]() -> double* {
-    const uint32_t s = nuse % R, par = (nuse / R) & 1;
-    mbar_wait(full + s, par);
-    ++nuse;
-    return ring + (size_t)s * SLOT;
-  };
-  // slot reads done -> producer may refill it (the empty-barrier arrive orders our generic
-  // reads before the async-proxy overwrite; no proxy fence is needed for read -> write)
-  auto release = [&](const double* sl) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + (sl - ring) / SLOT);
-  };
-  auto lmma = [&](const double* sf, const double (&xa)[NT][2], double (&d)[NT][2]) {
-    double d1[NT][2];
-#pragma unroll
-    for (int h = 0; h < NT; ++h) d[h][0] = d[h][1] = d1[h][0] = d1[h][1] = 0.0;
-#pragma unroll
-    for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass) {
-      const double* L = sf + (TWOW ? pass : fsel) * C::FAC;
-      const bool on = !TWOW || cls == (pass ? cB : cA);
-#pragma unroll
-      for (int h = 0; h < NT; ++h)
-#pragma unroll
-        for (int s2 = 0; s2 < NT; ++s2) {
-          const double2 lb = *reinterpret_cast<const double2*>(L + fofs[h][s2]);
-          dmma(d[h][0], d[h][1], on ? xa[s2][0] : 0.0, lb.x);
-          dmma(d1[h][0], d1[h][1], on ? xa[s2][1] : 0.0, lb.y);
-        }
-    }
-#pragma unroll
-    for (int h = 0; h < NT; ++h) {
-      d[h][0] += d1[h][0];
-      d[h][1] += d1[h][1];
-    }
-  };
-  auto gfrag = [&](const double* sf, double2 (&gb)[TWOW ? 2 : 1][NT][NT]) {
-#pragma unroll
-    for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass)
-#pragma unroll
-      for (int h = 0; h < NT; ++h)
-#pragma unroll
-        for (int s2 = 0; s2 < NT; ++s2)
-          gb[pass][h][s2] = *reinterpret_cast<const double2*>(
-              sf + (TWOW ? pass : fsel) * C::FAC + QQ + fofs[h][s2]);
-  };
-  auto gmma = [&](const double2 (&gb)[TWOW ? 2 : 1][NT][NT], const double (&ya)[NT][2],
-                  double (&e0)[NT][2], double (&e1)[NT][2]) {
-#pragma unroll
-    for (int h = 0; h < NT; ++h) e0[h][0] = e0[h][1] = e1[h][0] = e1[h][1] = 0.0;
-#pragma unroll
-    for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass) {
-      const bool on = !TWOW || cls == (pass ? cB : cA);
-#pragma unroll
-      for (int h = 0; h < NT; ++h)
-#pragma unroll
-        for (int s2 = 0; s2 < NT; ++s2) {
-          dmma(e0[h][0], e0[h][1], on ? ya[s2][0] : 0.0, gb[pass][h][s2].x);
-          dmma(e1[h][0], e1[h][1], on ? ya[s2][1] : 0.0, gb[pass][h][s2].y);
-        }
-    }
-  };
-  auto load_tau = [&](const double* sl, int k, double (&bp)[NT][2]) {
-    const double* sf = sl + C::NR * RECC;
-#pragma unroll
-    for (int h = 0; h < NT; ++h) {
-      const double2 bv =
-          *reinterpret_cast<const double2*>((node_ok(nd[h], k) ? sl : zrec) + bofs[h]);
-      bp[h][0] = bv.x;
-      bp[h][1] = bv.y;
-    }
-    if (INNER) {
-#pragma unroll
-      for (int h = 0; h < NT; ++h) {
-        const int ri = nd[h] >> 1;
-        const bool odd = nd[h] & 1;
-        const int opos = (nd[h] & 1) * 2 + (nd[h] >> 1);
-        const double* om = sf + 2 * C::FAC + osel * C::OMG + opos * 5 * B2 + co[h] * NS;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-        for (int u = 0; u < 5; ++u) {
-          const int tix = (odd ? (u == 0 ? 3 : u == 1 ? 6 : u == 2 ? 7 : u == 3 ? 8 : 10)
-                               : (u == 0 ? 0 : u == 1 ? 2 : u == 2 ? 3 : u == 3 ? 4 : 7)) + ri;
-          const int ii = 2 * k + tr[tix];
-          const int jj = a + tc[tix];
-          const bool tok = jj >= 0 && jj < g.N && ii >= 0 && ii < g.K;
-          const double* trow = (tok ? sl + (4 + tix) * RECC : zrec) + srow * NS;
-#pragma unroll
-          for (int c = 0; c < NS; c += 2) {
-            const double2 m0 = *reinterpret_cast<const double2*>(om + u * B2 + c);
-            const double2 m1 = *reinterpret_cast<const double2*>(om + u * B2 + NS + c);
-            const double2 tv2 = *reinterpret_cast<const double2*>(trow + c);
-            s0 = fma(m0.x, tv2.x, s0);
-            s2 = fma(m0.y, tv2.y, s2);
-            s1 = fma(m1.x, tv2.x, s1);
-            s3 = fma(m1.y, tv2.y, s3);
-          }
-        }
-        bp[h][0] -= s0 + s2;
-        bp[h][1] -= s1 + s3;
-      }
-    }
-  };
-
-  // ---------------- forward ----------------
-  double wd[NT][2];
-#pragma unroll
-  for (int h = 0; h < NT; ++h) wd[h][0] = wd[h][1] = 0.0;
-  double dl[NT][2];
-  double2 gcur[TWOW ? 2 : 1][NT][NT];
-  {
-    const double* sl = acquire();
-    double bp[NT][2];
-    load_tau(sl, 0, bp);
-    lmma(sl + C::NR * RECC, bp, dl);
-    gfrag(sl + C::NR * RECC, gcur);
-    release(sl);
-  }
-#pragma unroll 1
-  for (int k = 0; k < nb; ++k) {
-    double e0[NT][2], e1[NT][2];
-    gmma(gcur, wd, e0, e1);
-    double dln[NT][2];
-    double2 gnext[TWOW ? 2 : 1][NT][NT];
-    if (k + 1 < nb) {
-      const double* sl = acquire();
-      double bp[NT][2];
-      load_tau(sl, k + 1, bp);
-      lmma(sl + C::NR * RECC, bp, dln);
-      gfrag(sl + C::NR * RECC, gnext);
-      release(sl);
-    }
-#pragma unroll
-    for (int h = 0; h < NT; ++h) {
-      wd[h][0] = dl[h][0] + (e0[h][0] + e1[h][0]);
-      wd[h][1] = dl[h][1] + (e0[h][1] + e1[h][1]);
-      if (ostore[h] && 2 * k + (nd[h] >> 1) < g.K)
-        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(optr[h] + k * rs2),
-                     "d"(wd[h][0]), "d"(wd[h][1]), "l"(pol_keep)
-                     : "memory");
-    }
-    if (k + 1 < nb) {
-#pragma unroll
-      for (int h = 0; h < NT; ++h) {
-        dl[h][0] = dln[h][0];
-        dl[h][1] = dln[h][1];
-      }
-#pragma unroll
-      for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass)
-#pragma unroll
-        for (int h = 0; h < NT; ++h)
-#pragma unroll
-          for (int s2 = 0; s2 < NT; ++s2) gcur[pass][h][s2] = gnext[pass][h][s2];
-    }
-  }
-  // w stores visible to the producer's bulk reads of the backward sweep
-  __threadfence();
-  fence_proxy_async();
-  asm volatile("barrier.sync 1, %0;\n" ::"r"(32 * (sg.W + 1)) : "memory");
-
-  // ---------------- backward ----------------
-  const bool dm = dotmode != kDotNone;
-  auto load_w = [&](const double* sl, int k, double (&wp)[NT][2], double (&rp)[NT][2]) {
-#pragma unroll
-    for (int h = 0; h < NT; ++h) {
-      const double* base = node_ok(nd[h], k) ? sl : zrec;
-      const double2 wv = *reinterpret_cast<const double2*>(base + bofs[h]);
-      wp[h][0] = wv.x;
-      wp[h][1] = wv.y;
-      const double2 rv = dm ? *reinterpret_cast<const double2*>(base + 4 * RECC + bofs[h])
-                            : make_double2(0.0, 0.0);
-      rp[h][0] = rv.x;
-      rp[h][1] = rv.y;
-    }
-  };
-  double xd[NT][2];
-#pragma unroll
-  for (int h = 0; h < NT; ++h) xd[h][0] = xd[h][1] = 0.0;
-  double rcur[NT][2];
-  {
-    const double* sl = acquire();
-    double wp[NT][2];
-    load_w(sl, nb - 1, wp, rcur);
-    lmma(sl + C::NR * RECC, wp, dl);
-    gfrag(sl + C::NR * RECC, gcur);
-    release(sl);
-  }
-#pragma unroll 1
-  for (int k = nb - 1; k >= 0; --k) {
-    double e0[NT][2], e1[NT][2];
-    gmma(gcur, xd, e0, e1);
-    double dln[NT][2], rnext[NT][2];
-    double2 gnext[TWOW ? 2 : 1][NT][NT];
-    if (k > 0) {
-      const double* sl = acquire();
-      double wp[NT][2];
-      load_w(sl, k - 1, wp, rnext);
-      lmma(sl + C::NR * RECC, wp, dln);
-      gfrag(sl + C::NR * RECC, gnext);
-      release(sl);
-    }
-#pragma unroll
-    for (int h = 0; h < NT; ++h) {
-      xd[h][0] = dl[h][0] + (e0[h][0] + e1[h][0]);
-      xd[h][1] = dl[h][1] + (e0[h][1] + e1[h][1]);
-      if (ostore[h] && 2 * k + (nd[h] >> 1) < g.K) {
-        *reinterpret_cast<double2*>(optr[h] + k * rs2) = make_double2(xd[h][0], xd[h][1]);
-        if (dm) {
-          dot = fma(xd[h][0], rcur[h][0], dot);
-          dot = fma(xd[h][1], rcur[h][1], dot);
-        }
-      }
-    }
-    if (k > 0) {
-#pragma unroll
-      for (int h = 0; h < NT; ++h) {
-        dl[h][0] = dln[h][0];
-        dl[h][1] = dln[h][1];
-        rcur[h][0] = rnext[h][0];
-        rcur[h][1] = rnext[h][1];
-      }
-#pragma unroll
-      for (int pass = 0; pass < (TWOW ? 2 : 1); ++pass)
-#pragma unroll
-        for (int h = 0; h < NT; ++h)
-#pragma unroll
-          for (int s2 = 0; s2 < NT; ++s2) gcur[pass][h][s2] = gnext[pass][h][s2];
-    }
-  }
-}
-
-template <int NS, bool INNER>
-__global__ void __launch_bounds__(288) k_sweep8(Geo g, FastOps fo, Sw8Geo sg,
-                                                const double* __restrict__ rhs,
-                                                const double* __restrict__ th, double* out,
-                                                const double* __restrict__ rdot, int n_items,
-                                                double* partials, PcgState* st, int dotmode) {
-  using C = Sw8<NS, INNER>;
-  constexpr int QQ = C::QQ, B2 = C::B2;
-  extern __shared__ __align__(16) double smem[];
-  if (halted(st)) return;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int R = sg.R, SLOT = sg.SLOT, RECC = sg.RECC, S = sg.S;
-  double* ring = smem;
-  double* zrec = smem + (size_t)R * SLOT;
-  uint64_t* full = reinterpret_cast<uint64_t*>(zrec + (size_t)C::NR * RECC);
-  uint64_t* empty = full + R;
-  for (int e = threadIdx.x; e < C::NR * RECC; e += blockDim.x) zrec[e] = 0.0;
-  if (threadIdx.x == 0)
-    for (int s = 0; s < R; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, sg.W);
-    }
-  fence_proxy_async();
-  __syncthreads();
-  const uint64_t pol = policy_evict_first();
-  const uint64_t pol_keep = policy_evict_last();
-  const long long rs = (long long)g.T1 * NS;
-  const long long cs = (long long)g.K * g.T1 * NS;
-  double dot = 0.0;
-  const bool producer = wid == sg.W;
-  uint32_t nfill = 0, nuse = 0;
-#pragma unroll 1
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int v = item / sg.nchunk, chunk = item % sg.nchunk;
-    const int t0 = chunk * S;
-    const int nvalid = min(S, g.T1 - t0);
-    const int cA = fo.psi_cls[t0];
-    const int cB = fo.psi_cls[t0 + nvalid - 1];
-    const bool two = cA != cB;
-    const int a = 2 * v;
-    const bool okb = a + 1 < g.N;
-    const long long col_a = (long long)a * g.K * g.T1 * NS + (long long)t0 * NS;
-    if (producer) {
-      if (lane == 0) {
-        const uint32_t rec_bytes = (uint32_t)nvalid * NS * 8;
-        const double* FA = fo.fac4 + ((long long)cA * g.V + v) * g.nb * 4 * QQ;
-        const double* FB = fo.fac4 + ((long long)cB * g.V + v) * g.nb * 4 * QQ;
-        const double* OA = fo.omega + ((long long)cA * g.nk + (long long)a * g.K) * 5 * B2;
-        const double* OB = fo.omega + ((long long)cB * g.nk + (long long)a * g.K) * 5 * B2;
-        const int tr[12] = {0, 1, -1, 0, 1, 2, -1, 0, 1, 2, 0, 1};
-        const int tc[12] = {-2, -2, -1, -1, -1, -1, 2, 2, 2, 2, 3, 3};
-        auto slot_for_fill = [&](uint32_t& bytes_bar_slot) -> double* {
-          const uint32_t s = nfill % R, u = nfill / R;
-          if (u >= 1) mbar_wait(empty + s, (u - 1) & 1);
-          ++nfill;
-          bytes_bar_slot = s;
-          return ring + (size_t)s * SLOT;
-        };
-        for (int k = 0; k < g.nb; ++k) {
-          uint32_t s;
-          double* sl = slot_for_fill(s);
-          uint64_t* bar = full + s;
-          const int i0 = 2 * k;
-          const bool ok1 = i0 + 1 < g.K;
-          const bool tv[4] = {true, okb, ok1, ok1 && okb};
-          bool thv[12];
-          uint32_t bytes = 2 * QQ * 8 * (two ? 2 : 1);
-          for (int r = 0; r < 4; ++r) bytes += tv[r] ? rec_bytes : 0;
-          if (INNER) {
-            for (int m = 0; m < 12; ++m) {
-              const int ii = i0 + tr[m], jj = a + tc[m];
-              thv[m] = jj >= 0 && jj < g.N && ii >= 0 && ii < g.K;
-              bytes += thv[m] ? rec_bytes : 0;
-            }
-            bytes += (uint32_t)((ok1 ? 2 : 1) * 5 * B2 * 8) * (okb ? 2 : 1) * (two ? 2 : 1);
-          }
-          mbar_expect_tx(bar, bytes);
-          const long long r0 = col_a + i0 * rs;
-          for (int r = 0; r < 4; ++r)
-            if (tv[r]) bulk_g2s(sl + r * RECC, rhs + r0 + (r & 1) * cs + (r >> 1) * rs, rec_bytes, bar, pol);
-          if (INNER)
-            for (int m = 0; m < 12; ++m)
-              if (thv[m]) bulk_g2s(sl + (4 + m) * RECC, th + r0 + tc[m] * cs + tr[m] * rs, rec_bytes, bar, pol);
-          double* sf = sl + C::NR * RECC;
-          bulk_g2s(sf, FA + (long long)k * 4 * QQ, 2 * QQ * 8, bar, pol_keep);
-          if (two) bulk_g2s(sf + C::FAC, FB + (long long)k * 4 * QQ, 2 * QQ * 8, bar, pol_keep);
-          if (INNER) {
-            double* so = sf + 2 * C::FAC;
-            const uint32_t ob = (uint32_t)((ok1 ? 2 : 1) * 5 * B2 * 8);
-            bulk_g2s(so, OA + (long long)i0 * 5 * B2, ob, bar, pol_keep);
-            if (okb) bulk_g2s(so + 2 * 5 * B2, OA + ((long long)g.K + i0) * 5 * B2, ob, bar, pol_keep);
-            if (two) {
-              bulk_g2s(so + C::OMG, OB + (long long)i0 * 5 * B2, ob, bar, pol_keep);
-              if (okb) bulk_g2s(so + C::OMG + 2 * 5 * B2, OB + ((long long)g.K + i0) * 5 * B2, ob, bar, pol_keep);
-            }
-          }
-        }
-        asm volatile("barrier.sync 1, %0;\n" ::"r"(32 * (sg.W + 1)) : "memory");
-        fence_proxy_async();
-        const bool dm = dotmode != kDotNone;
-        for (int k = g.nb - 1; k >= 0; --k) {
-          uint32_t s;
-          double* sl = slot_for_fill(s);
-          uint64_t* bar = full + s;
-          const bool ok1 = 2 * k + 1 < g.K;
-          const bool tv[4] = {true, okb, ok1, ok1 && okb};
-          uint32_t bytes = 2 * QQ * 8 * (two ? 2 : 1);
-          for (int r = 0; r < 4; ++r) bytes += tv[r] ? rec_bytes * (dm ? 2 : 1) : 0;
-          mbar_expect_tx(bar, bytes);
-          const long long r0 = col_a + 2 * k * rs;
-          for (int r = 0; r < 4; ++r)
-            if (tv[r]) {
-              const long long off = r0 + (r & 1) * cs + (r >> 1) * rs;
-              bulk_g2s(sl + r * RECC, out + off, rec_bytes, bar, pol);
-              if (dm) bulk_g2s(sl + (4 + r) * RECC, rdot + off, rec_bytes, bar, pol);
-            }
-          double* sf = sl + C::NR * RECC;
-          bulk_g2s(sf, FA + (long long)k * 4 * QQ + 2 * QQ, 2 * QQ * 8, bar, pol_keep);
-          if (two) bulk_g2s(sf + C::FAC, FB + (long long)k * 4 * QQ + 2 * QQ, 2 * QQ * 8, bar, pol_keep);
-        }
-      } else {
-        asm volatile("barrier.sync 1, %0;\n" ::"r"(32 * (sg.W + 1)) : "memory");
-      }
-    } else {
-      const int t = t0 + 8 * wid + (lane >> 2);
-      const bool tvr = t < g.T1;
-      const int cls = tvr ? fo.psi_cls[t] : -1;
-      const int wfirst = fo.psi_cls[min(t0 + 8 * wid, g.T1 - 1)];
-      const int wlast = fo.psi_cls[min(t0 + 8 * wid + 7, g.T1 - 1)];
-      const bool twow = two && wfirst != wlast;
-      const int fsel = (two && wfirst == cB) ? 1 : 0;
-      if (twow)
-        sweep8_warp_item<NS, INNER, true>(g, sg, out, dotmode, ring, full, empty, zrec, nuse, lane,
-                                          wid, v, t0, cA, cB, fsel, cls, tvr, pol_keep, dot);
-      else
-        sweep8_warp_item<NS, INNER, false>(g, sg, out, dotmode, ring, full, empty, zrec, nuse, lane,
-                                           wid, v, t0, cA, cB, fsel, cls, tvr, pol_keep, dot);
-    }
-  }
-  if (dotmode != kDotNone) {
-    double mu;
-    if (grid_reduce<false>(dot, partials, &st->counter[2], mu) && threadIdx.x == 0) {
-      if (dotmode == kDotInit) {
-        st->mu = mu;                       // pcg.py:92
-      } else {
-        st->beta = mu / st->mu;            // pcg.py:127-131
-        st->mu = mu;
-      }
-    }
-  }
-}
-
-// fac4[pc][v][k] = L_k^-1 | -G_k | L_k^-T | -H_k  (row-major q x q each)
 template <int NS>
 __global__ void k_build_fac4(Geo g, int npc, const double* __restrict__ fac,
                              double* __restrict__ fac4) {
@@ -1930,45 +1438,10 @@ static cudaError_t sweep6_launch(const Geo& g, const FastOps& fo, const double* 
 
 }
 
-template <int NS, bool INNER>
-static cudaError_t sweep8_launch(const Geo& g, const FastOps& fo, const double* rhs,
-                                 const double* th, double* out, const double* rdot, int sm_count,
-                                 double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  using C = Sw8<NS, INNER>;
-  Sw8Geo sg;
-  // stage chunk: multiple of 8, ~T1 / ceil(T1 / 64) so chunks are balanced, <= 8 warps
-  const int nch = (g.T1 + 63) / 64;
-  sg.S = std::min(64, ((g.T1 + nch - 1) / nch + 7) / 8 * 8);
-  sg.W = sg.S / 8;
-  sg.nchunk = (g.T1 + sg.S - 1) / sg.S;
-  sg.RECC = sg.S * NS;
-  sg.SLOT = C::NR * sg.RECC + 2 * C::FAC + 2 * C::OMG;
-  const size_t budget = 200 * 1024;
-  const size_t fixed = (size_t)C::NR * sg.RECC * 8;
-  sg.R = (int)std::max<size_t>(2, std::min<size_t>(8, (budget - fixed) / ((size_t)sg.SLOT * 8 + 16)));
-  const size_t smem = fixed + (size_t)sg.R * sg.SLOT * 8 + (size_t)sg.R * 16;
-  const int n_items = g.V * sg.nchunk;
-  cudaError_t e = cudaFuncSetAttribute(k_sweep8<NS, INNER>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int threads = 32 * (sg.W + 1);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep8<NS, INNER>, threads, smem);
-  const int cap = std::max(1, env_int("GQ_SWEEP8_CTAS_PER_SM", 1));
-  const int blocks = std::max(1, std::min(n_items, std::min(std::max(per_sm, 1), cap) * sm_count));
-  k_sweep8<NS, INNER><<<blocks, threads, smem, s>>>(g, fo, sg, rhs, th, out, rdot, n_items,
-                                                    partials, st, dotmode);
-  return cudaGetLastError();
-}
-
 template <int NS>
 static cudaError_t sweep4_n(const Geo& g, const FastOps& fo, bool inner, const double* rhs,
                             const double* th, double* out, const double* rdot, int sm_count,
                             double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  if (env_int("GQ_SWEEP_V", 6) == 8) {
-    if (inner) return sweep8_launch<NS, true>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    return sweep8_launch<NS, false>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-  }
   // n = 4: the MT = 1 instantiation (255 registers + spills) faults with an illegal
   // instruction on B200; the two-tile variant is used instead.
   const int mt = NS == 4 ? 2 : env_int("GQ_SWEEP_MT", 1);
