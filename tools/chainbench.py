@@ -20,4 +20,4 @@ for L in (2, 4):
 # L4 - L2 = 2 inner sweeps
 res["inner_sweep_est"] = round((res["L4"] - res["L2"]) / 2, 4)
 res["outer_sweep_est"] = round(res["L2"] - res["inner_sweep_est"], 4)   # + transposes
-print(json.dumps({"exp": os.environ.get("GQ_CHAIN_EXP", "0"), **res}))
+print(json.dumps({"exp": os.environ.get("GQ_CHAIN_EX", os.environ.get("GQ_CHAIN_EXP", "0")), **res}))
