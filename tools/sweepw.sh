@@ -1,1 +1,1 @@
-for ex in 0 3 7 11 4 8 12; do GQ_CHAIN_EX=$ex python tools/chainbench.py; done
+for ex in 0 1 2 4 5 8 13 15; do GQ_GRID_EX=$ex python tools/gridbench.py; done
