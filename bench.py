@@ -237,6 +237,10 @@ def run_ours(args, ws, rank, local):
 
     # end to end through the public API with host buffers (H2D rhs, D2H x + history)
     rhs_host = torch.from_numpy(ga.offset.copy()).pin_memory().numpy()
+    try:        # warm-up solve of W steps through the same path (not timed)
+        pcg_solve(op, pc, rhs_host, tol=tol, max_steps=max(W, 1))
+    except MaxIterationsExceeded:
+        pass
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     try:
