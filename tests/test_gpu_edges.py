@@ -1,0 +1,47 @@
+"""Edge shapes through the fast n = 2 / n = 4 kernels against the CPU oracle: single row or
+column grids, odd sizes (padded pair blocks), a horizon of one stage, and T + 1 not a
+multiple of the stencil / chain stage chunks.  20 PCG steps, iterates to 1e-9."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    (1, 1, 1, 2), (1, 5, 3, 2), (5, 1, 3, 2), (2, 3, 1, 2), (3, 2, 7, 2),
+    (7, 9, 31, 2), (4, 6, 30, 2), (9, 4, 61, 2), (6, 5, 8, 4), (3, 3, 2, 4),
+]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("K,N,T,n", SHAPES)
+def test_edge_shape_pcg(K, N, T, n):
+    from oracle.gridlq_oracle import Oracle, pcg
+    from paper_2304_04980_b200 import (GpuNestedJacobiPreconditioner, GpuSchurOperator,
+                                       MaxIterationsExceeded, generators, pcg_solve)
+
+    ga = generators.random_case(K, N, T, n, 1, seed=K * 100 + N * 10 + T, coupling_std=0.1)
+    op = GpuSchurOperator(ga, 2, 2)
+    pc = GpuNestedJacobiPreconditioner(op, 2, 2)
+    orc = Oracle(ga, 2, 2)
+    v = np.random.default_rng(0).standard_normal(op.dim)
+    assert rel_err(op.apply(v), orc.apply_delta(v)) < 1e-12
+    assert rel_err(pc.apply(v), orc.apply_precond(v)) < 1e-11
+    steps = 20
+    x_ref, hist_ref, k_ref, conv_ref, _ = pcg(orc, ga.offset, tol=1e-13, max_steps=steps)
+    try:
+        x, rep = pcg_solve(op, pc, ga.offset, tol=1e-13, max_steps=steps)
+    except MaxIterationsExceeded as exc:
+        x, rep = exc.iterate, exc.report
+    assert rep.steps == k_ref
+    assert rel_err(x, x_ref) < 1e-9
+    h, hr = np.array(rep.residual_inf_history), np.array(hist_ref)
+    assert np.all(np.abs(h - hr) <= 1e-9 * hr + 1e-14 * hr[0])
