@@ -1,1 +1,1 @@
-for ex in 0 1 2 4 5 8 13 15; do GQ_GRID_EX=$ex python tools/gridbench.py; done
+for i in 1 2; do for ex in 0 1 2 3; do GQ_CHAIN_EX=$ex python tools/chainbench.py; done; done
