@@ -562,15 +562,10 @@ static cudaError_t chain_launch(const Geo& g, const ChainOps& co, const double* 
                                 double* partials, PcgState* st, int dotmode, cudaStream_t s) {
   constexpr size_t smem = (size_t)(P + 1) * Ch<NS, INNER, MT>::SLOT * sizeof(double);
   const int n_items = g.V * (MT == 1 ? co.nseg : co.nseg16);
-  static int attr_done = 0, per_sm = 0;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_chain<NS, INNER, P, MT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chain<NS, INNER, P, MT>, 32, smem);
-    per_sm = std::max(per_sm, 1);
-    attr_done = 1;
-  }
+  static int cache[64] = {0};
+  int per_sm = 1;
+  cudaError_t e = kernel_occupancy(k_chain<NS, INNER, P, MT>, 32, smem, cache, per_sm);
+  if (e != cudaSuccess) return e;
   int cap = per_sm;
   const int want = env_or(INNER ? "GQ_CHAIN_WARPS_INNER" : "GQ_CHAIN_WARPS_OUTER",
                           env_or("GQ_CHAIN_WARPS", 0));

@@ -346,15 +346,10 @@ static cudaError_t grid_launch(const Geo& g, const FastOps& fo, const double* x,
                                double* y, const GridShape& ub, double* partials, PcgState* st,
                                int dotmode, cudaStream_t s) {
   constexpr size_t smem = (size_t)(P + 1) * Gd<MODE>::SLOT * sizeof(double);
-  static int attr_done = 0, per_sm = 0;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_grid<MODE, P>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid<MODE, P>, 32, smem);
-    per_sm = std::max(per_sm, 1);
-    attr_done = 1;
-  }
+  static int cache[64] = {0};
+  int per_sm = 1;
+  cudaError_t e = kernel_occupancy(k_grid<MODE, P>, 32, smem, cache, per_sm);
+  if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

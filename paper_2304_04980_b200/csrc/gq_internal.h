@@ -7,6 +7,26 @@
 
 namespace gq {
 
+// Per-device one-time kernel configuration (max dynamic shared memory, resident blocks per
+// SM).  `cache` is a zero-initialised static int[64] owned by the call site.
+template <typename Kern>
+inline cudaError_t kernel_occupancy(Kern kernel, int threads, size_t smem, int* cache,
+                                    int& per_sm) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 63;
+  if (!cache[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+    cache[dev] = n > 0 ? n : 1;
+  }
+  per_sm = cache[dev];
+  return cudaSuccess;
+}
+
 enum StencilMode { kDelta = 0, kOuter = 1, kInner = 2, kOuterRhs = 3 };
 
 struct SetupErr {
