@@ -47,7 +47,7 @@ def c_factor(S, L):
     return 10 + (3 * L - 1) + (S - 1) * (4 * L - 1)
 
 
-def kernel_passes(name):
+def kernel_passes(name, S=2, L=2):
     """Algorithmic full-vector reads+writes of one launch of each step kernel."""
     if name == "delta":
         return 2                       # read d, write y (+ y.d)
@@ -62,8 +62,12 @@ def kernel_passes(name):
     if name.startswith("outer_rhs"):
         return 3                       # read delta, r; write r + Xi~ delta
     if name.startswith("sweep_s"):
+        # read rhs, write the sweep output; + theta for inner sweeps; + r for the q.r dot
+        # fused into the last sweep; + delta for the v1 path's on-the-fly Xi~ delta
+        s_ = int(name[len("sweep_s"):].split("_")[0])
         l_ = int(name.split("_l")[1].split("_")[0])
-        return 2 + (1 if l_ > 0 else 0) + (1 if name.endswith("_xi") else 0)
+        last = s_ == S - 1 and l_ == L - 1
+        return 2 + (1 if l_ > 0 else 0) + (1 if last else 0) + (1 if name.endswith("_xi") else 0)
     return 0
 
 
@@ -228,7 +232,7 @@ def run_ours(args, ws, rank, local):
     vec_bytes = 8 * dim
     peak, peak_src = load_peaks()
     top = max(kms, key=kms.get)
-    top_bytes = kernel_passes(top) * vec_bytes
+    top_bytes = kernel_passes(top, S, L) * vec_bytes
     achieved = top_bytes / (kms[top] * 1e-3) / 1e9
     step_bytes = 8 * dim * c_factor(S, L)
     step_ms = ms / K
