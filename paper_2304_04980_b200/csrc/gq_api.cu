@@ -56,6 +56,9 @@ struct gq_ctx {
   int4* seg = nullptr;
   ChainOps co{};
   bool chain = false;          // lean DMMA chain sweeps (n in {2, 4})
+  bool dd = false;             // domain-decomposed chain sweeps (n = 2)
+  double* ddarena = nullptr;
+  DDOps ddo{};
   bool grid = false;           // lean n = 2 grid stencils
   GridShape gsh{};
   bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
@@ -100,7 +103,7 @@ static void release(gq_ctx* c) {
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
                   c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
                   c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->partials, c->st, c->hist, c->err};
+                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -357,6 +360,15 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
       c->chain = true;
+      if (dd_supported(g)) {
+        const DDShape sh = dd_shape(g);
+        CKB(dalloc(&c->ddarena, dd_doubles(g, c->npc)));
+        CKB(launch_build_dd(g, c->npc, c->psi, c->omega, c->ddarena, c->stream));
+        const size_t blocks = (size_t)c->npc * g.V * g.nb;
+        c->ddo = DDOps{c->ddarena, c->ddarena + blocks * 320, c->ddarena + blocks * (320 + 128),
+                       c->ddarena + blocks * (320 + 128 + 128), sh.m, sh.ns};
+        c->dd = true;
+      }
     }
   }
 
@@ -495,7 +507,10 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
       const double* tp = l > 0 ? c->th[(l - 1) % 2] : nullptr;
       const double* dp = s > 0 ? c->dl[(s - 1) % 2] : nullptr;
       const int dm = (last && s == c->S - 1) ? dotmode : kDotNone;
-      if (c->chain) {
+      if (c->dd) {
+        CK(launch_chain_dd(c->g, c->co, c->ddo, l > 0, s > 0 ? c->rs : rin, tp, ob, rin,
+                           c->sm_count, c->partials, st, dm, c->stream));
+      } else if (c->chain) {
         CK(launch_chain(c->g, c->co, l > 0, s > 0 ? c->rs : rin, tp, ob, rin, c->sm_count,
                         c->partials, st, dm, c->stream));
       } else if (c->fast) {

@@ -116,7 +116,10 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            const double* __restrict__ th, double* out,
                                            const double* __restrict__ rdot, bool dotting,
                                            double* ring, int v, int t0, int nvalid, int cls,
-                                           uint64_t pol_s, uint64_t pol_k, double& dot) {
+                                           uint64_t pol_s, uint64_t pol_k, double& dot,
+                                           int kb, int ke, const double* __restrict__ ffbase,
+                                           const double* __restrict__ fbbase,
+                                           double2* ucap = nullptr) {
   using C = Ch<NS, INNER, MT>;
   constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::RSTR, R = P + 1;
   const int lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
@@ -154,7 +157,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   const unsigned rec_dst = lane_opaque(ring_u + (unsigned)(((lane / C::CPR) * REC + 2 * wch) * 8));
   const unsigned facf_dst = lane_opaque(ring_u + (unsigned)(C::NRF * REC * 8 + 16 * lane));
   const unsigned facb_dst = lane_opaque(ring_u + (unsigned)(8 * REC * 8 + 16 * lane));
-  const double* ffb = co.ff + ((long long)cls * g.V + v) * nb * C::FFS + 2 * lane;
+  const double* ffb = ffbase + ((long long)cls * g.V + v) * nb * C::FFS + 2 * lane;
 
   // checked issue (first/last blocks and the prologue): rows outside [0, K) zero-fill
   auto issue_f_chk = [&](int k, int slot) {
@@ -195,10 +198,10 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   }
 
   {
-    const int pro = P < nb ? P : nb;
+    const int pro = P < ke - kb ? P : ke - kb;
 #pragma unroll 1
     for (int p = 0; p < pro; ++p) {
-      issue_f_chk(p, p);
+      issue_f_chk(kb + p, p);
       commit();
     }
 #pragma unroll 1
@@ -207,14 +210,14 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   // running sources of block k + P
   const double* fcur[C::JF];
 #pragma unroll
-  for (int j = 0; j < C::JF; ++j) fcur[j] = fsz[j] ? fsrc[j] + (long long)P * rs2 : rhs;
-  const double* fpc = ffb + (long long)P * C::FFS;
+  for (int j = 0; j < C::JF; ++j) fcur[j] = fsz[j] ? fsrc[j] + (long long)(kb + P) * rs2 : rhs;
+  const double* fpc = ffb + (long long)(kb + P) * C::FFS;
 
   int slot = 0, islot = P % R;
 #pragma unroll 1
-  for (int k = 0; k < nb; ++k) {
+  for (int k = kb; k < ke; ++k) {
     const int kk = k + P;
-    if (kk < nb) {
+    if (kk < ke) {
       if (kk == nb - 1) {
         issue_f_chk(kk, islot);
       } else {
@@ -322,7 +325,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     bsrc[j] = (r < 4 ? (const double*)out : (dotting ? rdot : rhs)) + col_a +
               (long long)(dc && okb ? 1 : 0) * cs + (long long)dr * rs + wofs;
   }
-  const double* fbb = co.fb + ((long long)cls * g.V + v) * nb * C::FB + 2 * lane;
+  const double* fbb = fbbase + ((long long)cls * g.V + v) * nb * C::FB + 2 * lane;
   auto issue_b_chk = [&](int k, int slot_) {
     const unsigned sb = lane_opaque((unsigned)(slot_ * C::SLOT * 8));
 #pragma unroll
@@ -337,10 +340,10 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       ldgsts(facb_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
   };
   {
-    const int pro = P < nb ? P : nb;
+    const int pro = P < ke - kb ? P : ke - kb;
 #pragma unroll 1
     for (int p = 0; p < pro; ++p) {
-      issue_b_chk(nb - 1 - p, p);
+      issue_b_chk(ke - 1 - p, p);
       commit();
     }
 #pragma unroll 1
@@ -349,8 +352,8 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   const double* bcur[C::JB];
 #pragma unroll
   for (int j = 0; j < C::JB; ++j)
-    bcur[j] = bsz[j] ? bsrc[j] + (long long)(nb - 1 - P) * rs2 : rhs;
-  const double* fbc = fbb + (long long)(nb - 1 - P) * C::FB;
+    bcur[j] = bsz[j] ? bsrc[j] + (long long)(ke - 1 - P) * rs2 : rhs;
+  const double* fbc = fbb + (long long)(ke - 1 - P) * C::FB;
 
   double2 xd[MT][NT];
 #pragma unroll
@@ -360,9 +363,9 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   slot = 0;
   islot = P % R;
 #pragma unroll 1
-  for (int k = nb - 1; k >= 0; --k) {
+  for (int k = ke - 1; k >= kb; --k) {
     const int kk = k - P;
-    if (kk >= 0) {
+    if (kk >= kb) {
       const unsigned sb = lane_opaque((unsigned)(islot * C::SLOT * 8));
 #pragma unroll
       for (int j = 0; j < C::JB; ++j)
@@ -419,6 +422,10 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
 #pragma unroll
       for (int h = 0; h < NT; ++h) {
         xd[m][h] = xn[m][h];
+        if (ucap != nullptr && m == 0 && h == 0) {
+          if (k == kb) ucap[0] = xn[0][0];
+          if (k == ke - 1) ucap[1] = xn[0][0];
+        }
         if (ook[m][h] && !(lastk && 2 * k + orow[h] >= K)) {
           *reinterpret_cast<double2*>(out + oofs[m][h] + (long long)k * rs2) = xn[m][h];
           if (dotting) {
@@ -453,11 +460,185 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
     const int v = item / nseg;
     const int4 sg = seg[item - v * nseg];
     chain_item<NS, INNER, P, MT>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x, sg.y, sg.z,
-                                 pol_s, pol_k, dot);
+                                 pol_s, pol_k, dot, 0, g.nb, co.ff, co.fb);
   }
   if (dotting) {
     double mu;
     if (warp_grid_sum(dot, partials, &st->counter[2], mu) && threadIdx.x == 0) {
+      if (dotmode == kDotInit) {
+        st->mu = mu;                       // pcg.py:92
+      } else {
+        st->beta = mu / st->mu;            // pcg.py:127-131
+        st->mu = mu;
+      }
+    }
+  }
+}
+
+// ---- domain-decomposed sweep (n = 2): one CTA of 8 warps per 8-chain group ----------------
+// Phase 1: warp w solves interior segment w with the restarted factors (the per-warp chain
+// code above, block range [kb, ke)), parks u in `out`, keeps u at the segment ends.
+// Phase 2: separator right-hand sides (warp w) and the separator chain (warp 0).
+// Phase 3: x = u - V x_left - W x_right over each interior; the q.r dot of the last sweep.
+__device__ __forceinline__ double2 ldg2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+
+template <bool INNER, int P, int W>
+__global__ void __launch_bounds__(32 * W) k_chain_dd(Geo g, ChainOps co, DDOps dd,
+                                                  const double* __restrict__ rhs,
+                                                  const double* __restrict__ th, double* out,
+                                                  const double* __restrict__ rdot, int n_items,
+                                                  double* partials, PcgState* st, int dotmode) {
+  using C = Ch<2, INNER, 1>;
+  constexpr int NS = 2, QQ = 64, KT = 3;
+  extern __shared__ __align__(16) double smem_dd[];
+  __shared__ double2 ub[W][2][32];     // u at the first / last block of each interior
+  __shared__ double2 gsm[W][32];       // separator right-hand sides, then x at separators
+  if (halted(st)) return;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
+  double* ring = smem_dd + (size_t)wid * (P + 1) * C::SLOT;
+  const uint64_t pol_s = pol_first(), pol_k = pol_last();
+  const bool dotting = dotmode != kDotNone;
+  const long long rs = (long long)g.T1 * NS;
+  const long long cs = (long long)g.K * rs;
+  const long long rs2 = 2 * rs;
+  const int nb = g.nb, K = g.K, ns = dd.ns, m = dd.m;
+  const int kb = wid * m;
+  const int ke = wid == ns - 1 ? nb : wid * m + m - 1;
+  double dot = 0.0;
+#pragma unroll 1
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int v = item / co.nseg;
+    const int4 sg = co.seg[item - v * co.nseg];
+    const int t0 = sg.x, nvalid = sg.y, cls = sg.z;
+    const int a = 2 * v;
+    const bool okb = a + 1 < g.N;
+    const long long col_a = (long long)a * cs + (long long)t0 * NS;
+    // lane fragment: features 2qd, 2qd+1 (node qd) of chain rw
+    const int nd = qd;
+    const long long oofs = col_a + (long long)(nd & 1) * cs + (long long)(nd >> 1) * rs + rw * NS;
+    const bool ook = rw < nvalid && ((nd & 1) ? okb : true);
+    const int orow = nd >> 1;
+    const int bofs = rw * 8 + 2 * qd;
+    const long long tbase = ((long long)cls * g.V + v) * nb;   // (class, pair) block base
+
+    // ---- phase 1: interiors ----
+    double2 uc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    if (wid < ns)
+      chain_item<2, INNER, P, 1>(g, co, rhs, th, out, rdot, false, ring, v, t0, nvalid, cls,
+                                 pol_s, pol_k, dot, kb, ke, dd.ffd, dd.fbd, uc);
+    ub[wid][0][lane] = uc[0];
+    ub[wid][1][lane] = uc[1];
+    __syncthreads();
+
+    // ---- phase 2a: separator right-hand sides g_w = b_g - E_g u_w[last] - E_n' u_{w+1}[first]
+    if (wid < ns - 1) {
+      const int gk = ke;   // separator block
+      const double* T = dd.sept + (((long long)cls * g.V + v) * 8 + wid) * 9 * QQ;
+      double2 acc = make_double2(0.0, 0.0);
+      {
+        const bool ok = ook && 2 * gk + orow < K;
+        acc = ok ? ldg2(rhs + oofs + (long long)gk * rs2) : acc;       // tau_g (D layout)
+      }
+      double2 e0 = make_double2(0.0, 0.0), e1 = e0;
+      const double2 bE = ldg2(T + bofs), bN = ldg2(T + QQ + bofs);
+      dmma(e0, uc[1].x, bE.x);
+      dmma(e1, uc[1].y, bE.y);
+      const double2 un = ub[wid + 1][0][lane];
+      dmma(e0, un.x, bN.x);
+      dmma(e1, un.y, bN.y);
+      if (INNER) {
+#pragma unroll
+        for (int p = 0; p < KT; ++p) {
+          const int r = 4 * p + qd;                  // theta record of this k-pair / lane
+          const int dc = th_dc(r), dr = th_dr(r);
+          const int row = 2 * gk + dr;
+          const bool ok = rw < nvalid && a + dc >= 0 && a + dc < g.N && row >= 0 && row < K;
+          const double2 tq = ok ? ldg2(th + col_a + (long long)dc * cs + (long long)row * rs + rw * NS)
+                                : make_double2(0.0, 0.0);
+          const double2 mb = ldg2(T + 2 * QQ + p * 64 + bofs);
+          dmma(e0, tq.x, mb.x);
+          dmma(e1, tq.y, mb.y);
+        }
+      }
+      gsm[wid][lane] = add2(acc, add2(e0, e1));
+    }
+    __syncthreads();
+
+    // ---- phase 2b: separator chain (ns - 1 blocks), warp 0 ----
+    if (wid == 0 && ns > 1) {
+      const double* T0 = dd.sept + ((long long)cls * g.V + v) * 8 * 9 * QQ;
+      double2 z = make_double2(0.0, 0.0);
+      for (int s2 = 0; s2 < ns - 1; ++s2) {
+        const double* T = T0 + (long long)s2 * 9 * QQ;
+        const double2 gv = gsm[s2][lane];
+        double2 a0 = make_double2(0.0, 0.0), a1 = a0, g0 = a0, g1 = a0;
+        const double2 bL = ldg2(T + 5 * QQ + bofs), bG = ldg2(T + 6 * QQ + bofs);
+        dmma(a0, gv.x, bL.x);
+        dmma(a1, gv.y, bL.y);
+        dmma(g0, z.x, bG.x);
+        dmma(g1, z.y, bG.y);
+        z = add2(add2(a0, a1), add2(g0, g1));
+        gsm[s2][lane] = z;
+      }
+      double2 xg = make_double2(0.0, 0.0);
+      for (int s2 = ns - 2; s2 >= 0; --s2) {
+        const double* T = T0 + (long long)s2 * 9 * QQ;
+        const double2 zv = gsm[s2][lane];
+        double2 a0 = make_double2(0.0, 0.0), a1 = a0, g0 = a0, g1 = a0;
+        const double2 bL = ldg2(T + 7 * QQ + bofs), bH = ldg2(T + 8 * QQ + bofs);
+        dmma(a0, zv.x, bL.x);
+        dmma(a1, zv.y, bL.y);
+        dmma(g0, xg.x, bH.x);
+        dmma(g1, xg.y, bH.y);
+        xg = add2(add2(a0, a1), add2(g0, g1));
+        gsm[s2][lane] = xg;
+        const int gk = s2 * m + m - 1;
+        if (ook && 2 * gk + orow < K) {
+          *reinterpret_cast<double2*>(out + oofs + (long long)gk * rs2) = xg;
+          if (dotting) {
+            const double2 rv = ldg2(rdot + oofs + (long long)gk * rs2);
+            dot = fma(xg.x, rv.x, dot);
+            dot = fma(xg.y, rv.y, dot);
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- phase 3: interior corrections x = u - V x_left - W x_right ----
+    if (wid < ns) {
+      const double2 xl = wid > 0 ? gsm[wid - 1][lane] : make_double2(0.0, 0.0);
+      const double2 xr = wid < ns - 1 ? gsm[wid][lane] : make_double2(0.0, 0.0);
+      const double* SPb = dd.spt + tbase * 128 + bofs;
+#pragma unroll 2
+      for (int k = kb; k < ke; ++k) {
+        const bool ok = ook && 2 * k + orow < K;
+        double2 x = ok ? __ldcg(reinterpret_cast<const double2*>(out + oofs + (long long)k * rs2))
+                       : make_double2(0.0, 0.0);
+        const double2 bV = ldg2(SPb + (long long)k * 128), bW = ldg2(SPb + (long long)k * 128 + 64);
+        double2 c0 = make_double2(0.0, 0.0), c1 = c0;
+        dmma(c0, xl.x, bV.x);
+        dmma(c1, xl.y, bV.y);
+        dmma(c0, xr.x, bW.x);
+        dmma(c1, xr.y, bW.y);
+        x = add2(x, add2(c0, c1));
+        if (ok) {
+          *reinterpret_cast<double2*>(out + oofs + (long long)k * rs2) = x;
+          if (dotting) {
+            const double2 rv = ldg2(rdot + oofs + (long long)k * rs2);
+            dot = fma(x.x, rv.x, dot);
+            dot = fma(x.y, rv.y, dot);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (dotting) {
+    double mu;
+    if (grid_reduce<false>(dot, partials, &st->counter[2], mu) && threadIdx.x == 0) {
       if (dotmode == kDotInit) {
         st->mu = mu;                       // pcg.py:92
       } else {
@@ -610,6 +791,39 @@ cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const dou
     return inner ? chain_mt<4, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
                  : chain_mt<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   return cudaErrorInvalidValue;
+}
+
+template <bool INNER, int P, int W>
+static cudaError_t chain_dd_launch(const Geo& g, const ChainOps& co, const DDOps& dd,
+                                   const double* rhs, const double* th, double* out,
+                                   const double* rdot, int sm_count, double* partials,
+                                   PcgState* st, int dotmode, cudaStream_t s) {
+  constexpr size_t smem = (size_t)W * (P + 1) * Ch<2, INNER, 1>::SLOT * sizeof(double);
+  const int n_items = g.V * co.nseg;
+  static int cache[64] = {0};
+  int per_sm = 1;
+  cudaError_t e = kernel_occupancy(k_chain_dd<INNER, P, W>, 32 * W, smem, cache, per_sm);
+  if (e != cudaSuccess) return e;
+  const int blocks = std::max(1, std::min(n_items, per_sm * sm_count));
+  k_chain_dd<INNER, P, W><<<blocks, 32 * W, smem, s>>>(g, co, dd, rhs, th, out, rdot, n_items,
+                                                       partials, st, dotmode);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chain_dd(const Geo& g, const ChainOps& co, const DDOps& dd, bool inner,
+                            const double* rhs, const double* th, double* out, const double* rdot,
+                            int sm_count, double* partials, PcgState* st, int dotmode,
+                            cudaStream_t s) {
+  const int p = env_or("GQ_DD_P", 2);
+  if (dd.ns > 4) {
+    if (inner) return chain_dd_launch<true, 2, 8>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    return chain_dd_launch<false, 2, 8>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  }
+  if (inner)
+    return p == 3 ? chain_dd_launch<true, 3, 4>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                  : chain_dd_launch<true, 2, 4>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  return p == 3 ? chain_dd_launch<false, 3, 4>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                : chain_dd_launch<false, 2, 4>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
 }
 
 long long chain_max_blocks(const Geo& g, int nseg, int sm_count) {

@@ -111,6 +111,27 @@ cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const dou
                          double* partials, PcgState* st, int dotmode, cudaStream_t s);
 long long chain_max_blocks(const Geo& g, int nseg, int sm_count);
 
+// ---- domain-decomposed pair-chain solve, n = 2 (gq_dd.cu setup, gq_chain.cu kernel) ----
+struct DDShape {
+  int m = 0, ns = 0;   // blocks per segment (last one a separator), segments per chain
+};
+struct DDOps {
+  const double* ffd;   // [npc][V][nb] interior tiles L^-1 | -G | -M (restarted per interior)
+  const double* fbd;   // [npc][V][nb] L^-T | -H
+  const double* spt;   // [npc][V][nb] spike tiles -V | -W
+  const double* sept;  // [npc][V][8] separator tiles -E_g | -E_n' | -Om(3) | Ls^-1 | -Gs | Ls^-T | -Hs
+  int m, ns;
+};
+bool dd_supported(const Geo& g);
+DDShape dd_shape(const Geo& g);
+size_t dd_doubles(const Geo& g, int npc);
+cudaError_t launch_build_dd(const Geo& g, int npc, const double* psi, const double* omega,
+                            double* arena, cudaStream_t s);
+cudaError_t launch_chain_dd(const Geo& g, const ChainOps& co, const DDOps& dd, bool inner,
+                            const double* rhs, const double* th, double* out, const double* rdot,
+                            int sm_count, double* partials, PcgState* st, int dotmode,
+                            cudaStream_t s);
+
 // ---- lean n = 2 grid stencils (gq_grid.cu) ----
 struct GridShape {
   int nchunk = 0, nstrip = 0, rows = 0, blocks = 0;

@@ -19,6 +19,8 @@ VARIANTS = {
     "chain_mt2": {"GQ_CHAIN_MT": "2"},           # two M-tiles (16 chains) per warp
     "chain_p2": {"GQ_CHAIN_P": "2", "GQ_GRID_P": "3"},
     "no_fork": {"GQ_NO_FORK": "1"},              # x update in line instead of on a branch
+    "dd4": {"GQ_DD": "1"},                       # domain-decomposed chain solve, 4 segments
+    "dd8": {"GQ_DD": "1", "GQ_DD_W": "8"},       # ... 8 segments
 }
 
 
