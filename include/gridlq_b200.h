@@ -95,6 +95,18 @@ int gq_pcg(gq_ctx* ctx, const double* rhs, const double* x0, double tol, int64_t
            int32_t use_precond, double* x_out, double* hist_out, int64_t hist_capacity,
            int64_t* steps, int32_t* converged);
 
+/* Primal recovery and first-order optimality residuals (recovery.py:50-80).
+ *   gq_recover:      x = -Qinv (A~' lam), u = -Rinv (B~' lam), objective 0.5 (x'Qx + u'Ru)
+ *                    [recovery.py:50-65; kkt_assembly.py:84-160]
+ *   gq_kkt_residual: res3 = {||Qx + A~'lam||_inf, ||Ru + B~'lam||_inf,
+ *                            ||A~x + B~u + omega~||_inf}      [recovery.py:68-80]
+ * lam, x and omega~ have gq_dim entries in the reference order (t, j, i, k); u has
+ * gq_input_dim entries in the order (t, j, i, c) of GridLayout.stage_u_slice. */
+int64_t gq_input_dim(const gq_ctx* ctx);
+int gq_recover(gq_ctx* ctx, const double* lam, double* x_out, double* u_out, double* objective);
+int gq_kkt_residual(gq_ctx* ctx, const double* lam, const double* x, const double* u,
+                    const double* offset, double* res3);
+
 /* Measurement helpers (bench.py): run `steps` PCG steps as individual launches with CUDA
  * events around every kernel; per-kernel total milliseconds go to ms_out[0..count) in the
  * order gq_kernel_name(ctx, i) reports.  Returns the number of kernels per step. */

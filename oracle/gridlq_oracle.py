@@ -464,3 +464,94 @@ def step_cost_model(dim, S, L):
 
 __all__ = ["Oracle", "pcg", "spd_inverse", "cholesky", "lower_inverse", "NotSPD",
            "OFF13", "OFF5", "step_cost_model", "math"]
+
+
+# ---- primal recovery and KKT residuals (recovery.py:50-80, kkt_assembly.py:84-160) ------------
+# TEST INFRASTRUCTURE ONLY, like everything in oracle/.
+
+_DIRS = ((0, -1), (0, 1), (-1, 0), (1, 0))   # C direction order (west, east, north, south)
+
+
+def _shift(X, di, dj):
+    """Z[j, i] = X[j + dj, i + di] (zero outside the grid); X is [N, K, ...]."""
+    Z = np.zeros_like(X)
+    N, K = X.shape[:2]
+    js = slice(max(0, -dj), min(N, N - dj))
+    jd = slice(max(0, dj), min(N, N + dj))
+    is_ = slice(max(0, -di), min(K, K - di))
+    id_ = slice(max(0, di), min(K, K + di))
+    Z[js, is_] = X[jd, id_]
+    return Z
+
+
+def _unshift(Y, di, dj):
+    """adjoint of _shift: W[j + dj, i + di] += Y[j, i]."""
+    return _shift(Y, -di, -dj)
+
+
+def ahat_apply(ga, dc, X):
+    """(A_hat x)(a) = A_a x_a + sum_d C_{a,d} x_{a+d}   (kkt_assembly.py:59-64, 217-246)."""
+    Y = np.einsum("jiab,jib->jia", ga.A[dc], X)
+    for d, (di, dj) in enumerate(_DIRS):
+        Y = Y + np.einsum("jiab,jib->jia", ga.C[dc, d], _shift(X, di, dj))
+    return Y
+
+
+def ahat_apply_t(ga, dc, Y):
+    """A_hat' y (kkt_assembly.py:66-71)."""
+    Z = np.einsum("jiba,jib->jia", ga.A[dc], Y)
+    for d, (di, dj) in enumerate(_DIRS):
+        Z = Z + _unshift(np.einsum("jiba,jib->jia", ga.C[dc, d], Y), di, dj)
+    return Z
+
+
+def _stages(ga, v, width):
+    return np.asarray(v, dtype=float).reshape(-1, ga.N, ga.K, width)
+
+
+def constraint_t(ga, lam):
+    """A~' lam: -lam_t + A_hat_t' lam_{t+1} (kkt_assembly.py:97-105)."""
+    L = _stages(ga, lam, ga.n)
+    out = -L.copy()
+    for t in range(ga.T):
+        out[t] += ahat_apply_t(ga, ga.dyn_class[t], L[t + 1])
+    return out
+
+
+def recover(ga, lam):
+    """x = -Qinv (A~' lam), u = -Rinv (B~' lam), objective (recovery.py:50-65)."""
+    a = constraint_t(ga, lam)
+    L = _stages(ga, lam, ga.n)
+    qinv = np.linalg.inv(ga.Q)
+    rinv = np.linalg.inv(ga.R)
+    x = np.stack([-np.einsum("jiab,jib->jia", qinv[ga.cost_class[t]], a[t])
+                  for t in range(ga.T + 1)])
+    u = np.stack([-np.einsum("jiab,jib->jia", rinv[ga.dyn_class[t]],
+                             np.einsum("jiba,jib->jia", ga.B[ga.dyn_class[t]], L[t + 1]))
+                  for t in range(ga.T)])
+    obj = 0.0
+    for t in range(ga.T + 1):
+        obj += float(np.sum(x[t] * np.einsum("jiab,jib->jia", ga.Q[ga.cost_class[t]], x[t])))
+    for t in range(ga.T):
+        obj += float(np.sum(u[t] * np.einsum("jiab,jib->jia", ga.R[ga.dyn_class[t]], u[t])))
+    return x.reshape(-1), u.reshape(-1), 0.5 * obj
+
+
+def kkt(ga, lam, x, u):
+    """(||Qx + A~'lam||, ||Ru + B~'lam||, ||A~x + B~u + omega~||) (recovery.py:68-80)."""
+    a = constraint_t(ga, lam)
+    L = _stages(ga, lam, ga.n)
+    X = _stages(ga, x, ga.n)
+    U = _stages(ga, u, ga.m)
+    off = _stages(ga, ga.offset, ga.n)
+    rx = np.stack([np.einsum("jiab,jib->jia", ga.Q[ga.cost_class[t]], X[t]) + a[t]
+                   for t in range(ga.T + 1)])
+    ru = np.stack([np.einsum("jiab,jib->jia", ga.R[ga.dyn_class[t]], U[t])
+                   + np.einsum("jiba,jib->jia", ga.B[ga.dyn_class[t]], L[t + 1])
+                   for t in range(ga.T)])
+    rd = -X + off
+    for t in range(ga.T):
+        dc = ga.dyn_class[t]
+        rd[t + 1] += ahat_apply(ga, dc, X[t]) + np.einsum("jiab,jib->jia", ga.B[dc], U[t])
+    inf = lambda v: float(np.max(np.abs(v))) if v.size else 0.0
+    return inf(rx), inf(ru), inf(rd)

@@ -89,6 +89,14 @@ def run_case(name, problem, L=2, S=2, tol=None, rel_tol=None, max_steps=None, pr
         snap_x=np.array([snaps[s][0] for s in sorted(snaps)]),
         snap_r=np.array([snaps[s][1] for s in sorted(snaps)]),
     )
+    # primal recovery + KKT residuals (recovery.py:50-80) at the solve's final multipliers
+    # and at the random vector (non-trivial dynamics residual)
+    for tag, lam in (("rec", x), ("recv", v)):
+        sol = gridlq.recover_solution(stacked, lam)
+        rec[f"{tag}_x"] = sol.x_flat
+        rec[f"{tag}_u"] = sol.u_flat
+        rec[f"{tag}_obj"] = sol.objective_value
+        rec[f"{tag}_kkt"] = np.array(gridlq.kkt_residual(stacked, sol))
     np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **rec)
     print(f"{name}: dim={schur.dim} steps={rep.steps} conv={rep.converged} "
           f"({time.time() - t0:.1f}s)", flush=True)

@@ -9,6 +9,7 @@ from .errors import (BreakdownError, DimensionGuardError, DimensionMismatchError
                      MaxIterationsExceeded, NotPositiveDefiniteError)
 from .problem import (BoundaryData, ConstSeq, GridArrays, GridLayout, GridLQProblem,
                       SubsystemData, arrays_from_problem, arrays_to_problem, validate_arrays)
+from .recovery import TrajectorySolution, kkt_residual, recover_solution
 from .solver import (COUNT_KEYS, GpuNestedJacobiPreconditioner, GpuSchurOperator, SolveReport,
                      apply_delta, build_schur, cg_solve, pcg_solve)
 
@@ -21,7 +22,8 @@ __all__ = [
     "GridArrays", "GridLQError", "GridLQProblem", "GridLayout", "MaxIterationsExceeded",
     "NestedJacobiPreconditioner", "NotPositiveDefiniteError", "SchurOperator", "SolveReport",
     "SubsystemData", "apply_delta", "arrays_from_problem", "arrays_to_problem", "build_schur",
-    "cg_solve", "pcg_solve", "validate_arrays",
+    "cg_solve", "pcg_solve", "validate_arrays", "TrajectorySolution", "recover_solution",
+    "kkt_residual",
 ]
 
 __version__ = "0.1.0"

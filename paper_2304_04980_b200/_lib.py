@@ -24,7 +24,8 @@ EXPORTS = (
     "gq_synchronize", "gq_set_sweeps", "gq_apply_delta", "gq_apply_outer_coupling",
     "gq_apply_inner_coupling", "gq_pair_solve", "gq_apply_precond", "gq_pcg_start",
     "gq_pcg_run", "gq_pcg_read", "gq_pcg_history", "gq_pcg_scalars", "gq_pcg",
-    "gq_profile_steps", "gq_kernel_name", "gq_launches_per_step",
+    "gq_profile_steps", "gq_kernel_name", "gq_launches_per_step", "gq_input_dim",
+    "gq_recover", "gq_kkt_residual",
 )
 
 
@@ -81,6 +82,9 @@ def load():
         "gq_profile_steps": (ctypes.c_int, [vp, i32, ctypes.POINTER(ctypes.c_float), i32]),
         "gq_kernel_name": (ctypes.c_char_p, [vp, i32]),
         "gq_launches_per_step": (ctypes.c_int, [vp]),
+        "gq_input_dim": (i64, [vp]),
+        "gq_recover": (ctypes.c_int, [vp, dp, dp, dp, ctypes.POINTER(ctypes.c_double)]),
+        "gq_kkt_residual": (ctypes.c_int, [vp, dp, dp, dp, dp, dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -46,6 +46,7 @@ struct gq_ctx {
   double *qinv = nullptr, *rinv = nullptr, *brb = nullptr;
   double *psi = nullptr, *xi = nullptr, *xit = nullptr, *fac = nullptr;
   int *psi_cls = nullptr, *xi_cls = nullptr, *psi_keys = nullptr, *xi_keys = nullptr;
+  int *dcls = nullptr, *ccls = nullptr;   // per-stage dynamics / cost class (recovery)
   double *x = nullptr, *r = nullptr, *d = nullptr, *y = nullptr, *q = nullptr;
   double *th[2] = {nullptr, nullptr}, *dl[2] = {nullptr, nullptr};
   double *tmp0 = nullptr, *tmp1 = nullptr;
@@ -103,7 +104,7 @@ static void release(gq_ctx* c) {
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
                   c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
                   c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->partials, c->st, c->hist, c->err};
+                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -288,6 +289,11 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   CKB(cudaMemcpy(c->psi_keys, pkeys.data(), pkeys.size() * 4, cudaMemcpyHostToDevice));
   if (!xkeys.empty())
     CKB(cudaMemcpy(c->xi_keys, xkeys.data(), xkeys.size() * 4, cudaMemcpyHostToDevice));
+  CKB(dalloc(&c->dcls, std::max(g.T, 1)));
+  CKB(dalloc(&c->ccls, g.T1));
+  if (g.T > 0)
+    CKB(cudaMemcpy(c->dcls, D.dyn_class, (size_t)g.T * 4, cudaMemcpyHostToDevice));
+  CKB(cudaMemcpy(c->ccls, D.cost_class, (size_t)g.T1 * 4, cudaMemcpyHostToDevice));
   CKB(dalloc(&c->err, 1));
   CKB(cudaMemset(c->err, 0, sizeof(SetupErr)));
 
@@ -853,6 +859,109 @@ extern "C" int gq_profile_steps(gq_ctx* c, int32_t steps, float* ms_out, int32_t
   if (rc) return rc;
   for (int i = 0; i < nk && i < count; ++i) ms_out[i] = (float)acc[i];
   return nk;
+}
+
+// ---- primal recovery and KKT residuals (recovery.py:50-80) -------------------------------
+namespace {
+// device view of a user vector (host or device pointer); owns a temporary when needed
+struct DevVec {
+  double* p = nullptr;
+  double* tmp = nullptr;
+  ~DevVec() {
+    if (tmp) cudaFree(tmp);
+  }
+};
+int dev_in(gq_ctx* c, const double* src, size_t n, DevVec& v) {
+  if (is_device_ptr(src)) {
+    v.p = const_cast<double*>(src);
+    return GQ_OK;
+  }
+  CK(cudaMalloc(&v.tmp, std::max<size_t>(n, 1) * 8));
+  if (n) CK(cudaMemcpyAsync(v.tmp, src, n * 8, cudaMemcpyHostToDevice, c->stream));
+  v.p = v.tmp;
+  return GQ_OK;
+}
+int dev_out(gq_ctx* c, double* dst, size_t n, DevVec& v) {
+  if (is_device_ptr(dst)) {
+    v.p = dst;
+    return GQ_OK;
+  }
+  CK(cudaMalloc(&v.tmp, std::max<size_t>(n, 1) * 8));
+  v.p = v.tmp;
+  return GQ_OK;
+}
+int dev_back(gq_ctx* c, double* dst, size_t n, const DevVec& v) {
+  if (v.tmp && n) CK(cudaMemcpyAsync(dst, v.tmp, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  return GQ_OK;
+}
+}  // namespace
+
+extern "C" int64_t gq_input_dim(const gq_ctx* c) {
+  return c ? (int64_t)c->g.T * c->g.nk * c->m : -1;
+}
+
+extern "C" int gq_recover(gq_ctx* c, const double* lam, double* x_out, double* u_out,
+                          double* objective) {
+  if (!c || !lam || !x_out || !u_out) return fail(GQ_INVALID_ARG, "null argument");
+  const size_t nx = (size_t)c->g.dim, nu = (size_t)c->g.T * c->g.nk * c->m;
+  DevVec L, X, U;
+  int rc;
+  if ((rc = dev_in(c, lam, nx, L)) || (rc = dev_out(c, x_out, nx, X)) || (rc = dev_out(c, u_out, nu, U)))
+    return rc;
+  const int nbk = recover_blocks(c->g);
+  double* part = nullptr;
+  CK(cudaMalloc(&part, (size_t)nbk * 8));
+  cudaError_t e = launch_recover(c->g, c->m, c->A, c->C, c->qinv, c->B, c->R, c->rinv, c->Q,
+                                 c->dcls, c->ccls, 0, L.p, nullptr, nullptr, nullptr, X.p, U.p,
+                                 part, c->stream);
+  std::vector<double> hp(nbk);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(hp.data(), part, (size_t)nbk * 8, cudaMemcpyDeviceToHost, c->stream);
+  if ((rc = dev_back(c, x_out, nx, X)) || (rc = dev_back(c, u_out, nu, U))) {
+    cudaFree(part);
+    return rc;
+  }
+  cudaError_t e2 = cudaStreamSynchronize(c->stream);
+  cudaFree(part);
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    return fail(GQ_CUDA_ERROR, std::string("gq_recover: ") +
+                                   cudaGetErrorString(e != cudaSuccess ? e : e2));
+  double obj = 0.0;
+  for (double v : hp) obj += v;   // fixed block order: reproducible
+  if (objective) *objective = 0.5 * obj;
+  return GQ_OK;
+}
+
+extern "C" int gq_kkt_residual(gq_ctx* c, const double* lam, const double* x, const double* u,
+                               const double* offset, double* res3) {
+  if (!c || !lam || !x || !u || !offset || !res3) return fail(GQ_INVALID_ARG, "null argument");
+  const size_t nx = (size_t)c->g.dim, nu = (size_t)c->g.T * c->g.nk * c->m;
+  DevVec L, X, U, O;
+  int rc;
+  if ((rc = dev_in(c, lam, nx, L)) || (rc = dev_in(c, x, nx, X)) || (rc = dev_in(c, u, nu, U)) ||
+      (rc = dev_in(c, offset, nx, O)))
+    return rc;
+  const int nbk = recover_blocks(c->g);
+  double* part = nullptr;
+  CK(cudaMalloc(&part, (size_t)nbk * 3 * 8));
+  cudaError_t e = launch_recover(c->g, c->m, c->A, c->C, c->qinv, c->B, c->R, c->rinv, c->Q,
+                                 c->dcls, c->ccls, 1, L.p, X.p, U.p, O.p, nullptr, nullptr, part,
+                                 c->stream);
+  std::vector<double> hp((size_t)nbk * 3);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(hp.data(), part, (size_t)nbk * 3 * 8, cudaMemcpyDeviceToHost, c->stream);
+  cudaError_t e2 = cudaStreamSynchronize(c->stream);
+  cudaFree(part);
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    return fail(GQ_CUDA_ERROR, std::string("gq_kkt_residual: ") +
+                                   cudaGetErrorString(e != cudaSuccess ? e : e2));
+  res3[0] = res3[1] = res3[2] = 0.0;
+  for (int b = 0; b < nbk; ++b)
+    for (int k = 0; k < 3; ++k) {
+      const double v = hp[3 * b + k];
+      if (v != v || v > res3[k]) res3[k] = v;   // NaN propagates (np.max semantics)
+    }
+  return GQ_OK;
 }
 
 extern "C" const char* gq_kernel_name(gq_ctx* c, int32_t i) {

@@ -52,6 +52,16 @@ cudaError_t launch_psi(const Geo& g, int npc, const int* psi_keys, const double*
 cudaError_t launch_factor(const Geo& g, int npc, const double* psi, double* fac,
                           double* scratch, SetupErr* err, cudaStream_t s);
 
+// primal recovery (which = 0: x, u, objective partials) and KKT residual partials
+// (which = 1: per block {max|r_x|, max|r_u|, max|r_dyn|}); vectors in the reference order
+int recover_blocks(const Geo& g);
+cudaError_t launch_recover(const Geo& g, int m, const double* A, const double* C,
+                           const double* qinv, const double* B, const double* R,
+                           const double* rinv, const double* Q, const int* dcls,
+                           const int* ccls, int which, const double* lam, const double* x,
+                           const double* u, const double* off, double* xo, double* uo,
+                           double* part, cudaStream_t s);
+
 // ---- stencil (gq_stencil.cu) ----
 struct StencilShape {
   int nchunk, nstrip, rows, blocks, threads;

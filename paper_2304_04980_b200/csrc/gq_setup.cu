@@ -470,6 +470,221 @@ static cudaError_t launch_setup(const Geo& g, int which, int ncls, const int* ke
   }
 }
 
+// ---- primal recovery and KKT residuals (recovery.py:50-80) --------------------------------
+// One thread per (stage t, node a); vectors in the reference order (t, j, i, k).
+//   (A~' lam)_t(a) = -lam_t(a) + [t < T] sum_u Ahat_t(a+off_u, opp(u))' lam_{t+1}(a+off_u)
+//   x_t(a) = -Qinv_t(a) (A~' lam)_t(a)             u_t(a) = -Rinv_t(a) B_t(a)' lam_{t+1}(a)
+//   objective = 0.5 (x'Qx + u'Ru)                  (kkt_assembly.py:84-160)
+//   r_x = Q x + A~' lam,  r_u = R u + B~' lam,  r_dyn = A~ x + B~ u + omega~
+struct RecData {
+  const double* B;      // [nd][N][K][n][m]
+  const double* R;      // [nd][N][K][m][m]
+  const double* rinv;   // [nd][N][K][m][m]
+  const double* Q;      // [nq][N][K][n][n]
+  const int* dcls;      // [T]
+  const int* ccls;      // [T+1]
+  int m;
+};
+
+template <int NS>
+__device__ void at_lambda(const Geo& g, const RawData& d, const RecData& r, const double* lam,
+                          int t, int j, int i, double* a) {
+  const long long nhat = g.nk * NS;
+  const long long node = (long long)j * g.K + i;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) a[k] = -lam[t * nhat + node * NS + k];
+  if (t < g.T) {
+    const int dc = r.dcls[t];
+    for (int u = 0; u < 5; ++u) {
+      const int jj = j + odj(u), ii = i + odi(u);
+      if (jj < 0 || jj >= g.N || ii < 0 || ii >= g.K) continue;
+      const Blk<NS> ab = ahat<NS>(g, d, dc, jj, ii, slot_opp(u));
+      const double* y = lam + (t + 1) * nhat + ((long long)jj * g.K + ii) * NS;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < NS; ++rr) s = fma(ab.a[rr * NS + c], y[rr], s);
+        a[c] += s;
+      }
+    }
+  }
+}
+
+template <int NS>
+__global__ void k_recover(Geo g, RawData d, RecData r, const double* __restrict__ lam,
+                          double* __restrict__ xo, double* __restrict__ uo,
+                          double* __restrict__ part) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double obj = 0.0;
+  if (idx < (long long)g.T1 * g.nk) {
+    const int t = (int)(idx / g.nk);
+    const long long node = idx % g.nk;
+    const int j = (int)(node / g.K), i = (int)(node % g.K);
+    const long long nhat = g.nk * NS;
+    double a[NS], x[NS];
+    at_lambda<NS>(g, d, r, lam, t, j, i, a);
+    const Blk<NS> qi = qinv_at<NS>(g, d, r.ccls[t], j, i);
+    const double* Qb = r.Q + ((long long)r.ccls[t] * g.nk + node) * NS * NS;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = fma(qi.a[k * NS + c], a[c], s);
+      x[k] = -s;
+      xo[t * nhat + node * NS + k] = x[k];
+    }
+    double xq = 0.0;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = fma(Qb[k * NS + c], x[c], s);
+      xq = fma(x[k], s, xq);
+    }
+    obj = xq;
+    if (t < g.T) {
+      const int m = r.m, dc = r.dcls[t];
+      const double* Bb = r.B + ((long long)dc * g.nk + node) * NS * m;
+      const double* Ri = r.rinv + ((long long)dc * g.nk + node) * m * m;
+      const double* Rb = r.R + ((long long)dc * g.nk + node) * m * m;
+      const double* y = lam + (t + 1) * nhat + node * NS;
+      double bt[8], u[8];
+      for (int c = 0; c < m; ++c) {
+        double s = 0.0;
+        for (int k = 0; k < NS; ++k) s = fma(Bb[k * m + c], y[k], s);
+        bt[c] = s;
+      }
+      for (int c = 0; c < m; ++c) {
+        double s = 0.0;
+        for (int e = 0; e < m; ++e) s = fma(Ri[c * m + e], bt[e], s);
+        u[c] = -s;
+        uo[(long long)t * g.nk * m + node * m + c] = u[c];
+      }
+      double ur = 0.0;
+      for (int c = 0; c < m; ++c) {
+        double s = 0.0;
+        for (int e = 0; e < m; ++e) s = fma(Rb[c * m + e], u[e], s);
+        ur = fma(u[c], s, ur);
+      }
+      obj += ur;
+    }
+  }
+  obj = block_reduce<false>(obj);
+  if (threadIdx.x == 0) part[blockIdx.x] = obj;
+}
+
+template <int NS>
+__global__ void k_kkt(Geo g, RawData d, RecData r, const double* __restrict__ lam,
+                      const double* __restrict__ x, const double* __restrict__ u,
+                      const double* __restrict__ off, double* __restrict__ part) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double mx = 0.0, mu = 0.0, md = 0.0;
+  if (idx < (long long)g.T1 * g.nk) {
+    const int t = (int)(idx / g.nk);
+    const long long node = idx % g.nk;
+    const int j = (int)(node / g.K), i = (int)(node % g.K);
+    const long long nhat = g.nk * NS;
+    const int m = r.m;
+    double a[NS];
+    at_lambda<NS>(g, d, r, lam, t, j, i, a);
+    const double* Qb = r.Q + ((long long)r.ccls[t] * g.nk + node) * NS * NS;
+    const double* xa = x + t * nhat + node * NS;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) s = fma(Qb[k * NS + c], xa[c], s);
+      mx = nmax(mx, fabs(s + a[k]));
+    }
+    if (t < g.T) {
+      const int dc = r.dcls[t];
+      const double* Bb = r.B + ((long long)dc * g.nk + node) * NS * m;
+      const double* Rb = r.R + ((long long)dc * g.nk + node) * m * m;
+      const double* y = lam + (t + 1) * nhat + node * NS;
+      const double* ua = u + (long long)t * g.nk * m + node * m;
+      for (int c = 0; c < m; ++c) {
+        double s = 0.0, b = 0.0;
+        for (int e = 0; e < m; ++e) s = fma(Rb[c * m + e], ua[e], s);
+        for (int k = 0; k < NS; ++k) b = fma(Bb[k * m + c], y[k], b);
+        mu = nmax(mu, fabs(s + b));
+      }
+    }
+    // dynamics rows: stage 0 is -x_0 + omega_0; stage t is Ahat_{t-1} x_{t-1} - x_t + B u + omega
+    double rd[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) rd[k] = -xa[k] + off[t * nhat + node * NS + k];
+    if (t > 0) {
+      const int dc = r.dcls[t - 1];
+      for (int uu = 0; uu < 5; ++uu) {
+        const int jj = j + odj(uu), ii = i + odi(uu);
+        if (jj < 0 || jj >= g.N || ii < 0 || ii >= g.K) continue;
+        const Blk<NS> ab = ahat<NS>(g, d, dc, j, i, uu);
+        const double* xp = x + (t - 1) * nhat + ((long long)jj * g.K + ii) * NS;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < NS; ++c) s = fma(ab.a[k * NS + c], xp[c], s);
+          rd[k] += s;
+        }
+      }
+      const double* Bb = r.B + ((long long)dc * g.nk + node) * NS * m;
+      const double* ua = u + (long long)(t - 1) * g.nk * m + node * m;
+      for (int k = 0; k < NS; ++k) {
+        double s = 0.0;
+        for (int c = 0; c < m; ++c) s = fma(Bb[k * m + c], ua[c], s);
+        rd[k] += s;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) md = nmax(md, fabs(rd[k]));
+  }
+  mx = block_reduce<true>(mx);
+  mu = block_reduce<true>(mu);
+  md = block_reduce<true>(md);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x] = mx;
+    part[3 * blockIdx.x + 1] = mu;
+    part[3 * blockIdx.x + 2] = md;
+  }
+}
+
+template <int NS>
+static cudaError_t recover_n(const Geo& g, const RawData& d, const RecData& r, int which,
+                             const double* lam, const double* x, const double* u,
+                             const double* off, double* xo, double* uo, double* part,
+                             cudaStream_t s) {
+  const long long n = (long long)g.T1 * g.nk;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  if (which == 0)
+    k_recover<NS><<<blocks, 256, 0, s>>>(g, d, r, lam, xo, uo, part);
+  else
+    k_kkt<NS><<<blocks, 256, 0, s>>>(g, d, r, lam, x, u, off, part);
+  return cudaGetLastError();
+}
+
+int recover_blocks(const Geo& g) { return (int)(((long long)g.T1 * g.nk + 255) / 256); }
+
+cudaError_t launch_recover(const Geo& g, int m, const double* A, const double* C,
+                           const double* qinv, const double* B, const double* R,
+                           const double* rinv, const double* Q, const int* dcls,
+                           const int* ccls, int which, const double* lam, const double* x,
+                           const double* u, const double* off, double* xo, double* uo,
+                           double* part, cudaStream_t s) {
+  RawData d{A, C, qinv, nullptr};
+  RecData r{B, R, rinv, Q, dcls, ccls, m};
+  if (m > 8) return cudaErrorInvalidValue;
+  switch (g.n) {
+    case 1: return recover_n<1>(g, d, r, which, lam, x, u, off, xo, uo, part, s);
+    case 2: return recover_n<2>(g, d, r, which, lam, x, u, off, xo, uo, part, s);
+    case 3: return recover_n<3>(g, d, r, which, lam, x, u, off, xo, uo, part, s);
+    case 4: return recover_n<4>(g, d, r, which, lam, x, u, off, xo, uo, part, s);
+    case 8: return recover_n<8>(g, d, r, which, lam, x, u, off, xo, uo, part, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_xi(const Geo& g, int nxc, const int* xi_keys, const double* A,
                       const double* C, const double* qinv, double* xi, double* xit,
                       cudaStream_t s) {

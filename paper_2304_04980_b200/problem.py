@@ -115,10 +115,12 @@ class GridLayout:
     Column pairs ``[(0,1),(2,3),...]`` with a singleton last pair for odd N (``:135-137``).
     """
 
-    def __init__(self, K, N, T, n):
-        self.K, self.N, self.T, self.n = int(K), int(N), int(T), int(n)
+    def __init__(self, K, N, T, n, m=0):
+        self.K, self.N, self.T, self.n, self.m = int(K), int(N), int(T), int(n), int(m)
         self.nhat = self.K * self.N * self.n
+        self.mhat = self.K * self.N * self.m
         self.n_total = self.nhat * (self.T + 1)
+        self.m_total = self.mhat * self.T
         self.pairs = [tuple(range(j, min(j + 2, self.N))) for j in range(0, self.N, 2)]
 
     @property
@@ -134,6 +136,17 @@ class GridLayout:
 
     def stage_x_slice(self, t):
         return slice(t * self.nhat, (t + 1) * self.nhat)
+
+    def u_offset(self, i, j, t):
+        """Input vector order (``grid_problem.py:146-161``): ``t*mhat + (j*K+i)*m``."""
+        return t * self.mhat + (j * self.K + i) * self.m
+
+    def u_slice(self, i, j, t):
+        o = self.u_offset(i, j, t)
+        return slice(o, o + self.m)
+
+    def stage_u_slice(self, t):
+        return slice(t * self.mhat, (t + 1) * self.mhat)
 
 
 @dataclass
@@ -176,7 +189,7 @@ class GridArrays:
 
     @property
     def layout(self):
-        return GridLayout(self.K, self.N, self.T, self.n)
+        return GridLayout(self.K, self.N, self.T, self.n, self.m)
 
     @property
     def time_invariant(self):
