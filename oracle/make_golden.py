@@ -140,8 +140,11 @@ def main():
                  rel_tol=1e-10)
     if want("boundary"):
         run_case("boundary", cases.boundary_problem(), tol=1e-9, snap=(1, 2))
+        # problem files written by the reference itself (JSON ingestion parity)
+        gridlq.save_problem(cases.boundary_problem(), os.path.join(OUT, "boundary_problem.json"))
     if want("time_varying"):
         run_case("time_varying", cases.time_varying(), rel_tol=1e-10, snap=(1, 3))
+        gridlq.save_problem(cases.time_varying(), os.path.join(OUT, "time_varying_problem.json"))
     if want("sparse"):
         run_case("sparse", cases.sparse_couplings(), rel_tol=1e-10, snap=(1,))
     if want("uncoupled"):

@@ -8,7 +8,8 @@ preconditioner duck types, executed by hand-written sm_100a CUDA in libgridlq_b2
 from .errors import (BreakdownError, DimensionGuardError, DimensionMismatchError, GridLQError,
                      MaxIterationsExceeded, NotPositiveDefiniteError)
 from .problem import (BoundaryData, ConstSeq, GridArrays, GridLayout, GridLQProblem,
-                      SubsystemData, arrays_from_problem, arrays_to_problem, validate_arrays)
+                      SubsystemData, arrays_from_problem, arrays_to_problem, load_problem,
+                      problem_from_dict, problem_to_dict, save_problem, validate_arrays)
 from .recovery import TrajectorySolution, kkt_residual, recover_solution
 from .solver import (COUNT_KEYS, GpuNestedJacobiPreconditioner, GpuSchurOperator, SolveReport,
                      apply_delta, build_schur, cg_solve, pcg_solve)
@@ -23,7 +24,7 @@ __all__ = [
     "NestedJacobiPreconditioner", "NotPositiveDefiniteError", "SchurOperator", "SolveReport",
     "SubsystemData", "apply_delta", "arrays_from_problem", "arrays_to_problem", "build_schur",
     "cg_solve", "pcg_solve", "validate_arrays", "TrajectorySolution", "recover_solution",
-    "kkt_residual",
+    "kkt_residual", "load_problem", "save_problem", "problem_from_dict", "problem_to_dict",
 ]
 
 __version__ = "0.1.0"

@@ -562,3 +562,84 @@ def check_spd_blocks(mats, what):
     ok = _cholesky_ok(mats)
     if not np.all(ok):
         raise NotPositiveDefiniteError(f"{what}: not positive definite")
+
+
+# ---- problem files (JSON, ``grid_problem.py:431-529``) --------------------------------------
+# Same self-describing document as the reference ("format": "grid-lq-problem", version 1);
+# floats go through repr, so load(save(p)) reproduces every matrix bit for bit.
+
+def _mats_to_lists(seq):
+    if seq is None:
+        return None
+    return [np.asarray(m).tolist() for m in seq]
+
+
+def _lists_to_mats(seq):
+    if seq is None:
+        return None
+    return [np.array(m, dtype=float) for m in seq]
+
+
+def problem_to_dict(problem) -> dict:
+    """``grid_problem.py:444-476``"""
+    subs = []
+    for i in range(problem.K):
+        row = []
+        for j in range(problem.N):
+            s = problem.sub(i, j)
+            row.append({"n": s.n, "m": s.m, "A": _mats_to_lists(s.A), "B": _mats_to_lists(s.B),
+                        "Q": _mats_to_lists(s.Q), "R": _mats_to_lists(s.R),
+                        **{d: _mats_to_lists(s.coupling(d)) for d in DIRECTIONS}})
+        subs.append(row)
+    bnd = problem.boundary
+    return {
+        "format": "grid-lq-problem",
+        "version": 1,
+        "K": problem.K,
+        "N": problem.N,
+        "T": problem.T,
+        "subsystems": subs,
+        "boundary": {
+            "init": [[np.asarray(g).tolist() for g in row] for row in bnd.init],
+            **{d: None if getattr(bnd, d) is None
+               else [[np.asarray(v).tolist() for v in seq] for seq in getattr(bnd, d)]
+               for d in DIRECTIONS},
+        },
+    }
+
+
+def problem_from_dict(data: dict) -> GridLQProblem:
+    """``grid_problem.py:479-510``; ValueError for a document of another format."""
+    if data.get("format") != "grid-lq-problem":
+        raise ValueError("not a grid-lq-problem document")
+    subs = []
+    for row in data["subsystems"]:
+        subs.append([SubsystemData(n=int(rec["n"]), m=int(rec["m"]), A=_lists_to_mats(rec["A"]),
+                                   B=_lists_to_mats(rec["B"]), Q=_lists_to_mats(rec["Q"]),
+                                   R=_lists_to_mats(rec["R"]),
+                                   **{d: _lists_to_mats(rec.get(d)) for d in DIRECTIONS})
+                     for rec in row])
+    bnd = data["boundary"]
+    boundary = BoundaryData(
+        init=[[np.array(g, dtype=float) for g in row] for row in bnd["init"]],
+        **{d: None if bnd.get(d) is None
+           else [[np.array(v, dtype=float) for v in seq] for seq in bnd[d]]
+           for d in DIRECTIONS})
+    return GridLQProblem(int(data["K"]), int(data["N"]), int(data["T"]), subs, boundary)
+
+
+def save_problem(problem, path):
+    """``grid_problem.py:513-523``"""
+    import json
+
+    with open(path, "w") as fh:
+        json.dump(problem_to_dict(problem), fh)
+        fh.write("\n")
+
+
+def load_problem(path) -> GridLQProblem:
+    """``grid_problem.py:526-529``"""
+    import json
+
+    with open(path) as fh:
+        return problem_from_dict(json.load(fh))
