@@ -110,7 +110,7 @@ struct Ch {
 
 using namespace as;
 
-template <int NS, bool INNER, int P, int MT>
+template <int NS, bool INNER, int P, int MT, bool TF = false>
 __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            const double* __restrict__ rhs,
                                            const double* __restrict__ th, double* out,
@@ -119,7 +119,10 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            uint64_t pol_s, uint64_t pol_k, double& dot,
                                            int kb, int ke, const double* __restrict__ ffbase,
                                            const double* __restrict__ fbbase,
-                                           double2* ucap = nullptr) {
+                                           double2* ucap = nullptr, uint64_t* bars = nullptr,
+                                           uint32_t* phase = nullptr) {
+  // TF: the factor block of each chain block arrives by one bulk (TMA) copy issued by lane 0
+  // and completes on the slot's mbarrier; records stay on per-lane LDGSTS
   using C = Ch<NS, INNER, MT>;
   constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::RSTR, R = P + 1;
   const int lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
@@ -158,6 +161,20 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   const unsigned facf_dst = lane_opaque(ring_u + (unsigned)(C::NRF * REC * 8 + 16 * lane));
   const unsigned facb_dst = lane_opaque(ring_u + (unsigned)(8 * REC * 8 + 16 * lane));
   const double* ffb = ffbase + ((long long)cls * g.V + v) * nb * C::FFS + 2 * lane;
+  const double* ffb0 = ffbase + ((long long)cls * g.V + v) * nb * C::FFS;
+  auto bulk_f = [&](int k, int slot_) {
+    if (lane == 0) {
+      mbar_expect_tx(bars + slot_, C::FF * 8);
+      bulk_g2s(ring + slot_ * C::SLOT + C::NRF * REC, ffb0 + (long long)k * C::FFS, C::FF * 8,
+               bars + slot_);
+    }
+  };
+  auto fwait = [&](int slot_) {
+    if constexpr (TF) {
+      mbar_wait(bars + slot_, (*phase >> slot_) & 1u);
+      *phase ^= 1u << slot_;
+    }
+  };
 
   // checked issue (first/last blocks and the prologue): rows outside [0, K) zero-fill
   auto issue_f_chk = [&](int k, int slot) {
@@ -169,10 +186,14 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       ldgsts(rec_dst + sb + j * C::RPI * REC * 8, ok ? fsrc[j] + k * rs2 : rhs, ok ? 16 : 0,
              pol_s);
     }
-    const double* fp = ffb + (long long)k * C::FFS;
+    if constexpr (TF) {
+      bulk_f(k, slot);
+    } else {
+      const double* fp = ffb + (long long)k * C::FFS;
 #pragma unroll
-    for (int i = 0; i < C::CFF; ++i)
-      ldgsts(facf_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
+      for (int i = 0; i < C::CFF; ++i)
+        ldgsts(facf_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
+    }
   };
 
   double2 wd[MT][NT];
@@ -225,9 +246,13 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
 #pragma unroll
         for (int j = 0; j < C::JF; ++j)
           ldgsts(rec_dst + sb + j * C::RPI * REC * 8, fcur[j], fsz[j], pol_s);
+        if constexpr (TF) {
+          bulk_f(kk, islot);
+        } else {
 #pragma unroll
-        for (int i = 0; i < C::CFF; ++i)
-          ldgsts(facf_dst + sb + 512 * i, fpc + 64 * i, 16, pol_k);
+          for (int i = 0; i < C::CFF; ++i)
+            ldgsts(facf_dst + sb + 512 * i, fpc + 64 * i, 16, pol_k);
+        }
       }
     }
     commit();
@@ -236,6 +261,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       if (fsz[j]) fcur[j] += rs2;
     fpc += C::FFS;
     wait_groups<P>();
+    fwait(slot);
     __syncwarp();
 
     const double* sl = ring + slot * C::SLOT;
@@ -326,6 +352,14 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
               (long long)(dc && okb ? 1 : 0) * cs + (long long)dr * rs + wofs;
   }
   const double* fbb = fbbase + ((long long)cls * g.V + v) * nb * C::FB + 2 * lane;
+  const double* fbb0 = fbbase + ((long long)cls * g.V + v) * nb * C::FB;
+  auto bulk_b = [&](int k, int slot_) {
+    if (lane == 0) {
+      mbar_expect_tx(bars + slot_, C::FB * 8);
+      bulk_g2s(ring + slot_ * C::SLOT + 8 * REC, fbb0 + (long long)k * C::FB, C::FB * 8,
+               bars + slot_);
+    }
+  };
   auto issue_b_chk = [&](int k, int slot_) {
     const unsigned sb = lane_opaque((unsigned)(slot_ * C::SLOT * 8));
 #pragma unroll
@@ -334,10 +368,14 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       ldgsts(rec_dst + sb + j * C::RPI * REC * 8, ok ? bsrc[j] + k * rs2 : rhs, ok ? 16 : 0,
              pol_s);
     }
-    const double* fp = fbb + (long long)k * C::FB;
+    if constexpr (TF) {
+      bulk_b(k, slot_);
+    } else {
+      const double* fp = fbb + (long long)k * C::FB;
 #pragma unroll
-    for (int i = 0; i < C::CFB; ++i)
-      ldgsts(facb_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
+      for (int i = 0; i < C::CFB; ++i)
+        ldgsts(facb_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
+    }
   };
   {
     const int pro = P < ke - kb ? P : ke - kb;
@@ -370,9 +408,13 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
 #pragma unroll
       for (int j = 0; j < C::JB; ++j)
         ldgsts(rec_dst + sb + j * C::RPI * REC * 8, bcur[j], bsz[j], pol_s);
+      if constexpr (TF) {
+        bulk_b(kk, islot);
+      } else {
 #pragma unroll
-      for (int i = 0; i < C::CFB; ++i)
-        ldgsts(facb_dst + sb + 512 * i, fbc + 64 * i, 16, pol_k);
+        for (int i = 0; i < C::CFB; ++i)
+          ldgsts(facb_dst + sb + 512 * i, fbc + 64 * i, 16, pol_k);
+      }
     }
     commit();
 #pragma unroll
@@ -380,6 +422,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       if (bsz[j]) bcur[j] -= rs2;
     fbc -= C::FB;
     wait_groups<P>();
+    fwait(slot);
     __syncwarp();
 
     const double* sl = ring + slot * C::SLOT;
@@ -443,7 +486,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   __syncwarp();
 }
 
-template <int NS, bool INNER, int P, int MT>
+template <int NS, bool INNER, int P, int MT, bool TF>
 __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* __restrict__ rhs,
                                               const double* __restrict__ th, double* out,
                                               const double* __restrict__ rdot, int n_items,
@@ -455,12 +498,21 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
   const int nseg = MT == 1 ? co.nseg : co.nseg16;
   const int4* seg = MT == 1 ? co.seg : co.seg16;
   double dot = 0.0;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (P + 1) * Ch<NS, INNER, MT>::SLOT);
+  uint32_t phase = 0;
+  if constexpr (TF) {
+    if (threadIdx.x == 0)
+      for (int i = 0; i <= P; ++i) mbar_init(bars + i, 1);
+    fence_proxy_async();
+    __syncwarp();
+  }
 #pragma unroll 1
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int v = item / nseg;
     const int4 sg = seg[item - v * nseg];
-    chain_item<NS, INNER, P, MT>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x, sg.y, sg.z,
-                                 pol_s, pol_k, dot, 0, g.nb, co.ff, co.fb);
+    chain_item<NS, INNER, P, MT, TF>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x, sg.y,
+                                     sg.z, pol_s, pol_k, dot, 0, g.nb, co.ff, co.fb, nullptr,
+                                     bars, &phase);
   }
   if (dotting) {
     double mu;
@@ -737,22 +789,23 @@ cudaError_t launch_build_chain(const Geo& g, int npc, const double* fac, const d
   return cudaGetLastError();
 }
 
-template <int NS, bool INNER, int P, int MT>
+template <int NS, bool INNER, int P, int MT, bool TF = false>
 static cudaError_t chain_launch(const Geo& g, const ChainOps& co, const double* rhs,
                                 const double* th, double* out, const double* rdot, int sm_count,
                                 double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  constexpr size_t smem = (size_t)(P + 1) * Ch<NS, INNER, MT>::SLOT * sizeof(double);
+  constexpr size_t smem =
+      (size_t)(P + 1) * Ch<NS, INNER, MT>::SLOT * sizeof(double) + (TF ? (P + 1) * 8 : 0);
   const int n_items = g.V * (MT == 1 ? co.nseg : co.nseg16);
   static int cache[64] = {0};
   int per_sm = 1;
-  cudaError_t e = kernel_occupancy(k_chain<NS, INNER, P, MT>, 32, smem, cache, per_sm);
+  cudaError_t e = kernel_occupancy(k_chain<NS, INNER, P, MT, TF>, 32, smem, cache, per_sm);
   if (e != cudaSuccess) return e;
   int cap = per_sm;
   const int want = env_or(INNER ? "GQ_CHAIN_WARPS_INNER" : "GQ_CHAIN_WARPS_OUTER",
                           env_or("GQ_CHAIN_WARPS", 0));
   if (want > 0) cap = std::min(cap, want);
   const int blocks = std::max(1, std::min(n_items, cap * sm_count));
-  k_chain<NS, INNER, P, MT><<<blocks, 32, smem, s>>>(g, co, rhs, th, out, rdot, n_items,
+  k_chain<NS, INNER, P, MT, TF><<<blocks, 32, smem, s>>>(g, co, rhs, th, out, rdot, n_items,
                                                       partials, st, dotmode);
   return cudaGetLastError();
 }
@@ -761,8 +814,21 @@ template <int NS, bool INNER, int MT>
 static cudaError_t chain_p(const Geo& g, const ChainOps& co, const double* rhs, const double* th,
                            double* out, const double* rdot, int sm_count, double* partials,
                            PcgState* st, int dotmode, cudaStream_t s) {
-  switch (env_or("GQ_CHAIN_P", 3)) {
+  // ring depth (blocks in flight per warp), measured at n = 2 (tools/ab.sh, round 1):
+  // outer P 3 -> 7 took the outer sweep 0.216 -> 0.182 ms, inner P 3 -> 4 took 0.304 ->
+  // 0.287 ms; deeper inner rings lose (P 5: 0.331). n = 4 slots are 2.5x larger: keep P = 3.
+  const int pdef = env_or("GQ_CHAIN_P", NS == 2 ? (INNER ? 4 : 7) : 3);
+  const int pd = env_or(INNER ? "GQ_CHAIN_P_INNER" : "GQ_CHAIN_P_OUTER", pdef);
+  if constexpr (MT == 1) {
+    if (env_or("GQ_CHAIN_TMA", 0) == 1) {
+      if (pd == 5)
+        return chain_launch<NS, INNER, 5, MT, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+      return chain_launch<NS, INNER, 3, MT, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    }
+  }
+  switch (pd) {
     case 2: return chain_launch<NS, INNER, 2, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    case 4: return chain_launch<NS, INNER, 4, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
     case 5: return chain_launch<NS, INNER, 5, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
     case 7: return chain_launch<NS, INNER, 7, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
     default: break;

@@ -18,6 +18,9 @@ VARIANTS = {
     "no_grid": {"GQ_NO_GRID": "1"},              # v2 stencils instead of the n=2 grid kernel
     "chain_mt2": {"GQ_CHAIN_MT": "2"},           # two M-tiles (16 chains) per warp
     "chain_p2": {"GQ_CHAIN_P": "2", "GQ_GRID_P": "3"},
+    "chain_p3": {"GQ_CHAIN_P": "3"},             # the pre-tuning ring depth
+    "chain_p5": {"GQ_CHAIN_P": "5"},
+    "chain_tma": {"GQ_CHAIN_TMA": "1"},          # factor tiles by bulk copy + mbarrier
     "no_fork": {"GQ_NO_FORK": "1"},              # x update in line instead of on a branch
     "dd4": {"GQ_DD": "1"},                       # domain-decomposed chain solve, 4 segments
     "dd8": {"GQ_DD": "1", "GQ_DD_W": "8"},       # ... 8 segments
