@@ -57,6 +57,8 @@ def kernel_passes(name, S=2, L=2):
         return 3                       # read x, d; write x (parallel graph branch)
     if name == "dirupdate":
         return 3                       # read q, d; write d
+    if name == "dirupdate_x":
+        return 5                       # read q, d, x; write d, x (x update fused)
     if name == "dot":
         return 2
     if name.startswith("outer_rhs"):
@@ -67,7 +69,8 @@ def kernel_passes(name, S=2, L=2):
         s_ = int(name[len("sweep_s"):].split("_")[0])
         l_ = int(name.split("_l")[1].split("_")[0])
         last = s_ == S - 1 and l_ == L - 1
-        return 2 + (1 if l_ > 0 else 0) + (1 if last else 0) + (1 if name.endswith("_xi") else 0)
+        return (2 + (1 if l_ > 0 else 0) + (1 if last else 0) + (1 if name.endswith("_xi") else 0)
+                + (2 if name.endswith("_r") else 0))   # _r: + read y, write r (r update fused)
     return 0
 
 

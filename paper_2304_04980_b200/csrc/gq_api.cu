@@ -58,6 +58,11 @@ struct gq_ctx {
   ChainOps co{};
   bool chain = false;          // lean DMMA chain sweeps (n in {2, 4})
   bool dd = false;             // domain-decomposed chain sweeps (n = 2)
+  bool fuse_x = false;         // x update fused into the direction update (opt-in)
+  bool fuse_r = false;         // r update fused into the first outer sweep (chain kernel)
+  bool cta = false;            // CTA-cooperative TMA-fed chain sweeps (n = 2, opt-in)
+  double* cgt = nullptr;       // their inner-sweep forward tiles
+  CtaOps cto{};
   double* ddarena = nullptr;
   DDOps ddo{};
   bool grid = false;           // lean n = 2 grid stencils
@@ -104,7 +109,7 @@ static void release(gq_ctx* c) {
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
                   c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
                   c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
+                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->cgt, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -192,6 +197,12 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   c->L = inner_sweeps;
   c->S = outer_sweeps;
   c->n_dyn = D.n_dyn;
+  {
+    // measured at the headline (tools/steptime.py): the x update on its own graph branch
+    // overlaps the sweeps and beats the fused direction update by ~1.3%; fusion is opt-in
+    const char* e = getenv("GQ_FUSE_X");
+    c->fuse_x = e && *e == '1';
+  }
   c->n_cost = D.n_cost;
   Geo& g = c->g;
   g.K = D.K;
@@ -366,6 +377,17 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
       c->chain = true;
+      if (cta_supported(g, pcls.data())) {
+        bool ok = false;
+        CKB(cta_check_stage0(g, pcls[0], c->cff, c->cfb, ok, c->stream));
+        if (ok) {
+          CKB(dalloc(&c->cgt, chain_ff_doubles(g, c->npc)));
+          CKB(launch_build_cta(g, c->npc, c->cff, c->cgt, c->stream));
+          CKB(cudaStreamSynchronize(c->stream));
+          c->cto = CtaOps{c->cff, c->cfb, c->cgt, pcls[0], pcls[1]};
+          c->cta = true;
+        }
+      }
       if (dd_supported(g)) {
         const DDShape sh = dd_shape(g);
         CKB(dalloc(&c->ddarena, dd_doubles(g, c->npc)));
@@ -378,6 +400,10 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
     }
   }
 
+  {
+    const char* e = getenv("GQ_NO_FUSE_R");
+    c->fuse_r = c->chain && !c->dd && !c->cta && !(e && *e == '1');
+  }
   // work vectors (stage-inner layout) and the reference-layout staging buffers
   const size_t dim = (size_t)g.dim;
   double** vecs[] = {&c->x, &c->r, &c->d, &c->y, &c->q, &c->th[0], &c->th[1],
@@ -396,6 +422,8 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                              fast_max_blocks(g, c->sh_delta, c->sm_count),
                              fast_max_blocks(g, c->sh_outer, c->sm_count),
                              c->chain ? chain_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
+                             c->cta ? cta_max_blocks(g) : 0LL,
+                             c->chain ? chain_fr_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->grid ? (long long)c->gsh.blocks : 0LL});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));
   CKB(dalloc(&c->st, 1));
@@ -491,7 +519,8 @@ static int export_vec(gq_ctx* c, const double* src, double* dst) {
 // S outer x L inner sweeps from zero: out = P r  (nested_jacobi.py:105-122)
 static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* st, int dotmode,
                            std::vector<std::string>* names,
-                           const std::function<int()>& mark = nullptr) {
+                           const std::function<int()>& mark = nullptr,
+                           const double* fuse_y = nullptr) {
   for (int s = 0; s < c->S; ++s) {
     if (c->fast && s > 0) {
       // rhs_s = r + Xi~ delta_{s-1}, materialised once per outer sweep (nested_jacobi.py:119-121)
@@ -513,7 +542,15 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
       const double* tp = l > 0 ? c->th[(l - 1) % 2] : nullptr;
       const double* dp = s > 0 ? c->dl[(s - 1) % 2] : nullptr;
       const int dm = (last && s == c->S - 1) ? dotmode : kDotNone;
-      if (c->dd) {
+      if (fuse_y != nullptr && s == 0 && l == 0) {
+        // first sweep of a PCG step: r -= alpha y, max|r| and the convergence test run on
+        // the staged right-hand side (the separate r-update kernel is skipped)
+        CK(launch_chain_fr(c->g, c->co, const_cast<double*>(rin), fuse_y, ob, c->sm_count,
+                           c->partials, st, c->stream));
+      } else if (c->cta && !c->dd) {
+        CK(launch_chain_cta(c->g, c->cto, l > 0, s > 0 ? c->rs : rin, tp, ob, rin, c->sm_count,
+                            c->partials, st, dm, c->stream));
+      } else if (c->dd) {
         CK(launch_chain_dd(c->g, c->co, c->ddo, l > 0, s > 0 ? c->rs : rin, tp, ob, rin,
                            c->sm_count, c->partials, st, dm, c->stream));
       } else if (c->chain) {
@@ -528,7 +565,8 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
       }
       if (names)
         names->push_back("sweep_s" + std::to_string(s) + "_l" + std::to_string(l) +
-                         (!c->fast && s > 0 ? "_xi" : ""));
+                         (!c->fast && s > 0 ? "_xi" : "") +
+                         (fuse_y != nullptr && s == 0 && l == 0 ? "_r" : ""));
       if (mark) {
         const int rc = mark();
         if (rc) return rc;
@@ -615,15 +653,19 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
                       kDotStep, c->stream));
   if (names) names->push_back("delta");
   if ((rc = mark())) return rc;
-  // x += alpha d only feeds the result: it runs on a parallel branch of the step graph,
-  // overlapping the r update and the sweeps, and joins before d is overwritten.  Profiled
-  // (evs != null) steps run it in line so it gets its own timing.
+  // x += alpha d only feeds the result.  By default it is a separate kernel on a parallel
+  // branch of the step graph (joined before d is overwritten), or in line when GQ_NO_FORK=1
+  // or when the step is profiled.  GQ_FUSE_X=1 fuses it into the direction update at the
+  // end of the step (one pass over q, d, x).
   static const bool no_fork = [] {
     const char* e = getenv("GQ_NO_FORK");
     return e && *e == '1';
   }();
-  const bool fork = evs == nullptr && !no_fork;
-  if (fork) {
+  const bool fuse_x = c->fuse_x;
+  const bool fork = !fuse_x && evs == nullptr && !no_fork;
+  if (fuse_x) {
+    // nothing here: k_dirupdate_x below
+  } else if (fork) {
     CK(cudaEventRecord(c->ev_fork, c->stream));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     CK(launch_update_x(c->g, c->x, c->d, c->vblocks, c->st, c->side));
@@ -633,13 +675,17 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
     if (names) names->push_back("update_x");
     if ((rc = mark())) return rc;
   }
-  CK(launch_update_r(c->g, c->r, c->y, c->vblocks, c->partials, c->st, c->stream));
-  if (names) names->push_back("update");
-  if ((rc = mark())) return rc;
+  const bool fuse_r = use_precond && c->fuse_r;
+  if (!fuse_r) {
+    CK(launch_update_r(c->g, c->r, c->y, c->vblocks, c->partials, c->st, c->stream));
+    if (names) names->push_back("update");
+    if ((rc = mark())) return rc;
+  }
   const double* qv = c->q;
   if (use_precond) {
     rc = enqueue_precond(c, c->r, c->q, c->st, kDotStep, names,
-                         evs ? std::function<int()>(mark) : std::function<int()>());
+                         evs ? std::function<int()>(mark) : std::function<int()>(),
+                         fuse_r ? c->y : nullptr);
     if (rc) return rc;
   } else {
     CK(launch_dot(c->g, c->r, c->r, c->vblocks, c->partials, c->st, kDotStep, c->stream));
@@ -648,15 +694,21 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
     qv = c->r;
   }
   if (fork) CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-  CK(launch_dirupdate(c->g, c->d, qv, c->vblocks, c->st, c->stream));
-  if (names) names->push_back("dirupdate");
+  if (fuse_x) {
+    CK(launch_dirupdate_x(c->g, c->d, qv, c->x, c->vblocks, c->st, c->stream));
+    if (names) names->push_back("dirupdate_x");
+  } else {
+    CK(launch_dirupdate(c->g, c->d, qv, c->vblocks, c->st, c->stream));
+    if (names) names->push_back("dirupdate");
+  }
   return mark();
 }
 
 extern "C" int gq_launches_per_step(gq_ctx* c) {
   if (!c) return -1;
-  if (!c->use_precond) return 5;
-  return 4 + c->S * c->L + (c->fast ? c->S - 1 : 0);
+  const int vec = c->fuse_x ? 3 : 4;   // delta, r update, direction update (+ x update)
+  if (!c->use_precond) return vec + 1;
+  return vec - (c->fuse_r ? 1 : 0) + c->S * c->L + (c->fast ? c->S - 1 : 0);
 }
 
 extern "C" int gq_pcg_start(gq_ctx* c, const double* rhs, const double* x0, int32_t use_precond) {

@@ -82,9 +82,30 @@ __device__ bool warp_grid_sum(double v, double* partials, unsigned int* counter,
   return true;
 }
 
+__device__ bool warp_grid_max(double v, double* partials, unsigned int* counter, double& out) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = nmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  int last = 0;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = v;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return false;
+  __threadfence();
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) acc = nmax(acc, __ldcg(partials + b));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc = nmax(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  out = acc;
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
 }  // namespace
 
-template <int NS, bool INNER, int MT = 1>
+template <int NS, bool INNER, int MT = 1, bool FR = false>
 struct Ch {
   static constexpr int Q = 4 * NS, QQ = Q * Q, NT = Q / 8;
   static constexpr int TC = 12 * NS;                  // theta feature count
@@ -96,7 +117,9 @@ struct Ch {
   static constexpr int REC = ST * NS;                 // record: ST stages x NS
   static constexpr int CPR = REC / 2;                 // 16-byte chunks per record
   static constexpr int RPI = 32 / CPR;                // records per warp instruction
-  static constexpr int NRF = INNER ? 16 : 4;          // forward records: tau(4) + theta(12)
+  // forward records: tau(4) + theta(12) (inner) or tau(4) + y(4) (outer sweep fused with the
+  // PCG residual update r -= alpha y)
+  static constexpr int NRF = INNER ? 16 : (FR ? 8 : 4);
   static constexpr int JF = NRF / RPI, JB = 8 / RPI;  // record instructions fwd / bwd (w + r)
   static constexpr int CFF = FF / 64, CFB = FB / 64;  // factor instructions (32 x 16 B each)
   // record stride in shared memory: padded by 16*NS bytes so the A-fragment reads of a
@@ -110,7 +133,7 @@ struct Ch {
 
 using namespace as;
 
-template <int NS, bool INNER, int P, int MT, bool TF = false>
+template <int NS, bool INNER, int P, int MT, bool TF = false, bool FR = false>
 __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            const double* __restrict__ rhs,
                                            const double* __restrict__ th, double* out,
@@ -120,10 +143,13 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            int kb, int ke, const double* __restrict__ ffbase,
                                            const double* __restrict__ fbbase,
                                            double2* ucap = nullptr, uint64_t* bars = nullptr,
-                                           uint32_t* phase = nullptr) {
+                                           uint32_t* phase = nullptr,
+                                           const double* __restrict__ yv = nullptr,
+                                           double* rupd = nullptr, double alpha = 0.0,
+                                           double* rmax = nullptr) {
   // TF: the factor block of each chain block arrives by one bulk (TMA) copy issued by lane 0
   // and completes on the slot's mbarrier; records stay on per-lane LDGSTS
-  using C = Ch<NS, INNER, MT>;
+  using C = Ch<NS, INNER, MT, FR>;
   constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::RSTR, R = P + 1;
   const int lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
   const long long rs = (long long)g.T1 * NS;
@@ -147,13 +173,14 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
 #pragma unroll
   for (int j = 0; j < C::JF; ++j) {
     const int r = j * C::RPI + lane / C::CPR;
-    const int dc = r < 4 ? (r & 1) : th_dc(r - 4);
-    const int dr = r < 4 ? (r >> 1) : th_dr(r - 4);
+    const bool own = r < 4 || FR;                    // tau or y: the pair's own four nodes
+    const int dc = own ? (r & 1) : th_dc(r - 4);
+    const int dr = own ? ((r & 3) >> 1) : th_dr(r - 4);
     const bool colok = a + dc >= 0 && a + dc < g.N;
     fsz[j] = (colok && stage_ok) ? 16 : 0;
     frow[j] = dr;
     // off-grid columns are redirected to the pair's own column (never read: size 0)
-    fsrc[j] = (r < 4 ? rhs : th) + col_a + (long long)(colok ? dc : 0) * cs +
+    fsrc[j] = (r < 4 ? rhs : (FR ? yv : th)) + col_a + (long long)(colok ? dc : 0) * cs +
               (long long)dr * rs + wofs;
   }
   // per-lane shared destinations, kept in vector registers (no [R + UR] LDGSTS forms)
@@ -272,6 +299,23 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     for (int m = 0; m < MT; ++m)
 #pragma unroll
       for (int p = 0; p < NT; ++p) tv[m][p] = lds2(sl + aofs(0, m, 8 * p + 2 * qd));
+    if constexpr (FR) {
+      // r -= alpha y (pcg.py:111) on the staged records; the updated residual is this sweep's
+      // right-hand side, is written back, and feeds max|r| (pcg.py:113)
+      const bool lastk_ = k == nb - 1;
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int p = 0; p < NT; ++p) {
+          const double2 yy = lds2(sl + aofs(4, m, 8 * p + 2 * qd));
+          tv[m][p].x = __dsub_rn(tv[m][p].x, __dmul_rn(alpha, yy.x));
+          tv[m][p].y = __dsub_rn(tv[m][p].y, __dmul_rn(alpha, yy.y));
+          if (ook[m][p] && !(lastk_ && 2 * k + orow[p] >= K)) {
+            *reinterpret_cast<double2*>(rupd + oofs[m][p] + (long long)k * rs2) = tv[m][p];
+            *rmax = nmax(*rmax, nmax(fabs(tv[m][p].x), fabs(tv[m][p].y)));
+          }
+        }
+    }
     double2 wn[MT][NT];
 #pragma unroll
     for (int h = 0; h < NT; ++h) {
@@ -486,19 +530,23 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   __syncwarp();
 }
 
-template <int NS, bool INNER, int P, int MT, bool TF>
+template <int NS, bool INNER, int P, int MT, bool TF, bool FR = false>
 __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* __restrict__ rhs,
                                               const double* __restrict__ th, double* out,
                                               const double* __restrict__ rdot, int n_items,
-                                              double* partials, PcgState* st, int dotmode) {
+                                              double* partials, PcgState* st, int dotmode,
+                                              const double* __restrict__ yv = nullptr,
+                                              double* rupd = nullptr) {
   extern __shared__ __align__(16) double ring[];
   if (halted(st)) return;
+  const double alpha = FR ? st->alpha : 0.0;
+  double rmax = 0.0;
   const uint64_t pol_s = pol_first(), pol_k = pol_last();
   const bool dotting = dotmode != kDotNone;
   const int nseg = MT == 1 ? co.nseg : co.nseg16;
   const int4* seg = MT == 1 ? co.seg : co.seg16;
   double dot = 0.0;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (P + 1) * Ch<NS, INNER, MT>::SLOT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (P + 1) * Ch<NS, INNER, MT, FR>::SLOT);
   uint32_t phase = 0;
   if constexpr (TF) {
     if (threadIdx.x == 0)
@@ -510,9 +558,22 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int v = item / nseg;
     const int4 sg = seg[item - v * nseg];
-    chain_item<NS, INNER, P, MT, TF>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x, sg.y,
-                                     sg.z, pol_s, pol_k, dot, 0, g.nb, co.ff, co.fb, nullptr,
-                                     bars, &phase);
+    chain_item<NS, INNER, P, MT, TF, FR>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x,
+                                         sg.y, sg.z, pol_s, pol_k, dot, 0, g.nb, co.ff, co.fb,
+                                         nullptr, bars, &phase, yv, rupd, alpha, &rmax);
+  }
+  if constexpr (FR) {
+    // max |r| over the grid, then the reference's history / convergence step (pcg.py:113-121)
+    double res;
+    if (warp_grid_max(rmax, partials, &st->counter[1], res) && threadIdx.x == 0) {
+      st->res = res;
+      st->hist[st->step] = res;
+      st->step += 1;
+      if (res < st->tol) {
+        st->converged = 1;
+        st->done = 1;
+      }
+    }
   }
   if (dotting) {
     double mu;
@@ -857,6 +918,39 @@ cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const dou
     return inner ? chain_mt<4, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
                  : chain_mt<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   return cudaErrorInvalidValue;
+}
+
+// outer sweep fused with the PCG residual update: r -= alpha y is applied to the staged
+// right-hand-side records, written back to r, and its max-norm reduced (pcg.py:111-121)
+template <int NS, int P>
+static cudaError_t chain_fr_launch(const Geo& g, const ChainOps& co, double* r, const double* y,
+                                   double* out, int sm_count, double* partials, PcgState* st,
+                                   cudaStream_t s) {
+  constexpr size_t smem = (size_t)(P + 1) * Ch<NS, false, 1, true>::SLOT * sizeof(double);
+  const int n_items = g.V * co.nseg;
+  static int cache[64] = {0};
+  int per_sm = 1;
+  cudaError_t e = kernel_occupancy(k_chain<NS, false, P, 1, false, true>, 32, smem, cache, per_sm);
+  if (e != cudaSuccess) return e;
+  const int blocks = std::max(1, std::min(n_items, per_sm * sm_count));
+  k_chain<NS, false, P, 1, false, true><<<blocks, 32, smem, s>>>(
+      g, co, r, nullptr, out, nullptr, n_items, partials, st, kDotNone, y, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const double* y,
+                            double* out, int sm_count, double* partials, PcgState* st,
+                            cudaStream_t s) {
+  if (g.n == 2)
+    return env_or("GQ_CHAIN_P_OUTER", 7) == 4
+               ? chain_fr_launch<2, 4>(g, co, r, y, out, sm_count, partials, st, s)
+               : chain_fr_launch<2, 7>(g, co, r, y, out, sm_count, partials, st, s);
+  if (g.n == 4) return chain_fr_launch<4, 3>(g, co, r, y, out, sm_count, partials, st, s);
+  return cudaErrorInvalidValue;
+}
+
+long long chain_fr_max_blocks(const Geo& g, int nseg, int sm_count) {
+  return std::min<long long>((long long)g.V * nseg, 64LL * sm_count);
 }
 
 template <bool INNER, int P, int W>

@@ -120,6 +120,11 @@ cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const dou
                          const double* th, double* out, const double* rdot, int sm_count,
                          double* partials, PcgState* st, int dotmode, cudaStream_t s);
 long long chain_max_blocks(const Geo& g, int nseg, int sm_count);
+// outer sweep with the PCG residual update fused in (r -= alpha y, max|r|, history)
+cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const double* y,
+                            double* out, int sm_count, double* partials, PcgState* st,
+                            cudaStream_t s);
+long long chain_fr_max_blocks(const Geo& g, int nseg, int sm_count);
 
 // ---- domain-decomposed pair-chain solve, n = 2 (gq_dd.cu setup, gq_chain.cu kernel) ----
 struct DDShape {
@@ -141,6 +146,25 @@ cudaError_t launch_chain_dd(const Geo& g, const ChainOps& co, const DDOps& dd, b
                             const double* rhs, const double* th, double* out, const double* rdot,
                             int sm_count, double* partials, PcgState* st, int dotmode,
                             cudaStream_t s);
+
+// ---- CTA-cooperative TMA-fed pair-chain sweeps, n = 2 (gq_cta.cu) ----
+struct CtaOps {
+  const double* ff;    // chain forward tiles (ChainOps::ff), stride 320
+  const double* fb;    // chain backward tiles (ChainOps::fb), stride 128
+  const double* gt;    // inner-sweep forward tiles in k-pair group order, stride 320
+  int c0, c1;          // Psi classes of stage 0 / stages >= 1
+};
+// time-invariant pattern (stage 0 its own class, one class for t >= 1), n = 2, N even
+bool cta_supported(const Geo& g, const int* pcls);
+cudaError_t launch_build_cta(const Geo& g, int npc, const double* ff, double* gt,
+                             cudaStream_t s);
+// ok = the stage-0 class tiles carry no coupling (G, M, H all zero)
+cudaError_t cta_check_stage0(const Geo& g, int c0, const double* ff, const double* fb,
+                             bool& ok, cudaStream_t s);
+cudaError_t launch_chain_cta(const Geo& g, const CtaOps& co, bool inner, const double* rhs,
+                             const double* th, double* out, const double* rdot, int sm_count,
+                             double* partials, PcgState* st, int dotmode, cudaStream_t s);
+long long cta_max_blocks(const Geo& g);
 
 // ---- lean n = 2 grid stencils (gq_grid.cu) ----
 struct GridShape {
@@ -165,6 +189,8 @@ cudaError_t launch_update_x(const Geo& g, double* x, const double* d, int blocks
                             cudaStream_t s);
 cudaError_t launch_dirupdate(const Geo& g, double* d, const double* q, int blocks,
                              PcgState* st, cudaStream_t s);
+cudaError_t launch_dirupdate_x(const Geo& g, double* d, const double* q, double* x, int blocks,
+                               PcgState* st, cudaStream_t s);
 cudaError_t launch_dot(const Geo& g, const double* a, const double* b, int blocks,
                        double* partials, PcgState* st, int dotmode, cudaStream_t s);
 cudaError_t launch_sub(const Geo& g, double* out, const double* a, const double* b, int blocks,

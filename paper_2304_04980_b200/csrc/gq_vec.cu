@@ -187,6 +187,53 @@ __global__ void __launch_bounds__(256) k_dirupdate(long long dim, double* __rest
   if ((dim & 1) && tid == 0) d[dim - 1] = __dadd_rn(q[dim - 1], __dmul_rn(beta, d[dim - 1]));
 }
 
+// d = q + beta d (pcg.py:129) fused with the iterate update x += alpha d_old (pcg.py:109) of
+// the same step: one pass reads q, d, x and writes d, x.  Runs unless the step was skipped
+// (budget) or broke down; after convergence (done) only x is updated, as the reference
+// updates x in the step that converges and stops before the direction update.
+__global__ void __launch_bounds__(256) k_dirupdate_x(long long dim, double* __restrict__ d,
+                                                     const double* __restrict__ q,
+                                                     double* __restrict__ x, PcgState* st) {
+  if (st->skip || st->breakdown) return;
+  const double alpha = st->alpha, beta = st->beta;
+  const bool dir = !st->done;
+  const long long n2 = dim >> 1;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long b = tid; b < n2; b += nth * kVU) {
+    double2 dv[kVU], qv[kVU], xv[kVU];
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        dv[u] = *reinterpret_cast<const double2*>(d + e);
+        xv[u] = ld_stream(x + e);
+        if (dir) qv[u] = ld_stream(q + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kVU; ++u) {
+      const long long e = 2 * (b + u * nth);
+      if (b + u * nth < n2) {
+        xv[u].x = __dadd_rn(xv[u].x, __dmul_rn(alpha, dv[u].x));
+        xv[u].y = __dadd_rn(xv[u].y, __dmul_rn(alpha, dv[u].y));
+        __stcs(reinterpret_cast<double2*>(x + e), xv[u]);
+        if (dir) {
+          dv[u].x = __dadd_rn(qv[u].x, __dmul_rn(beta, dv[u].x));
+          dv[u].y = __dadd_rn(qv[u].y, __dmul_rn(beta, dv[u].y));
+          *reinterpret_cast<double2*>(d + e) = dv[u];
+        }
+      }
+    }
+  }
+  if ((dim & 1) && tid == 0) {
+    const long long e = dim - 1;
+    const double dold = d[e];
+    x[e] = __dadd_rn(x[e], __dmul_rn(alpha, dold));
+    if (dir) d[e] = __dadd_rn(q[e], __dmul_rn(beta, dold));
+  }
+}
+
 __global__ void __launch_bounds__(256) k_dot(long long dim, const double* __restrict__ a,
                                              const double* __restrict__ b, double* partials,
                                              PcgState* st, int dotmode) {
@@ -252,6 +299,12 @@ cudaError_t launch_update_x(const Geo& g, double* x, const double* d, int blocks
 cudaError_t launch_dirupdate(const Geo& g, double* d, const double* q, int blocks, PcgState* st,
                              cudaStream_t s) {
   k_dirupdate<<<blocks, 256, 0, s>>>(g.dim, d, q, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dirupdate_x(const Geo& g, double* d, const double* q, double* x, int blocks,
+                               PcgState* st, cudaStream_t s) {
+  k_dirupdate_x<<<blocks, 256, 0, s>>>(g.dim, d, q, x, st);
   return cudaGetLastError();
 }
 

@@ -21,6 +21,13 @@ VARIANTS = {
     "chain_p3": {"GQ_CHAIN_P": "3"},             # the pre-tuning ring depth
     "chain_p5": {"GQ_CHAIN_P": "5"},
     "chain_tma": {"GQ_CHAIN_TMA": "1"},          # factor tiles by bulk copy + mbarrier
+    "cta": {"GQ_CTA": "1"},                      # CTA-cooperative TMA-fed chain sweeps
+    "cta_r2": {"GQ_CTA": "1", "GQ_CTA_R_INNER": "2", "GQ_CTA_R_OUTER": "3"},
+    "cta_r4": {"GQ_CTA": "1", "GQ_CTA_R_INNER": "4", "GQ_CTA_R_OUTER": "7"},
+    "cta_persist": {"GQ_CTA": "1", "GQ_CTA_PERSIST": "1"},
+    "fuse_x": {"GQ_FUSE_X": "1"},                # x update fused into the direction update
+    "no_fuse_r": {"GQ_NO_FUSE_R": "1"},          # separate r update kernel
+    "no_fuse": {"GQ_NO_FUSE_R": "1", "GQ_NO_FORK": "1"},
     "no_fork": {"GQ_NO_FORK": "1"},              # x update in line instead of on a branch
     "dd4": {"GQ_DD": "1"},                       # domain-decomposed chain solve, 4 segments
     "dd8": {"GQ_DD": "1", "GQ_DD_W": "8"},       # ... 8 segments
