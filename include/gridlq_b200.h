@@ -13,6 +13,8 @@
  *   gq_apply_inner_coupling  PairSplitting.apply_inner_coupling   [kkt_assembly.py:645-662]
  *   gq_pair_solve        NestedJacobiPreconditioner._pair_solves  [nested_jacobi.py:65-77]
  *   gq_apply_precond     NestedJacobiPreconditioner.apply         [nested_jacobi.py:105-122]
+ *   gq_nbjm_solve        NestedJacobiPreconditioner.solve / nbjm_solve
+ *                                                                 [nested_jacobi.py:124-159]
  *   gq_pcg_start / gq_pcg_run / gq_pcg_read / gq_pcg_history / gq_pcg
  *                        pcg_solve / cg_solve                     [pcg.py:50-156]
  *
@@ -81,6 +83,14 @@ int gq_apply_outer_coupling(gq_ctx* ctx, const double* x, double* y);
 int gq_apply_inner_coupling(gq_ctx* ctx, const double* x, double* y);
 int gq_pair_solve(gq_ctx* ctx, const double* rhs, double* out);
 int gq_apply_precond(gq_ctx* ctx, const double* r, double* q);
+
+/* Standalone nested block Jacobi solve with the context's inner budget (any L >= 1):
+ * outer sweeps, inner sweeps warm-started from the outer iterate, until
+ * max|new - prev| < tol [nested_jacobi.py:124-151].  Returns GQ_OK with the solution and
+ * the outer sweep count, or GQ_MAX_ITER with the last iterate in x_out and
+ * *outers = max_outer.  Resets any PCG solve in progress on the context. */
+int gq_nbjm_solve(gq_ctx* ctx, const double* rhs, double tol, int64_t max_outer,
+                  double* x_out, int64_t* outers);
 
 /* Stateful PCG: start (r = rhs - Delta x0, d = P r, mu = d.r), then run until convergence
  * (||r||_inf < tol, absolute), breakdown or max_steps total steps. */

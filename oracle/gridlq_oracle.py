@@ -395,12 +395,36 @@ class Oracle:
             out[ts] = self.from_local(work, len(ts))
         return out.reshape(-1)
 
-    def inner_sweep(self, rhs):
-        """nested_jacobi.py:79-103 from the zero start."""
-        theta = self.pair_solve(rhs)
-        for _ in range(self.L - 1):
+    def inner_sweep(self, rhs, start=None):
+        """nested_jacobi.py:79-103: L sweeps from the zero start, or L sweeps warm-started
+        from `start` (the standalone iteration)."""
+        if start is None:
+            theta = self.pair_solve(rhs)
+            remaining = self.L - 1
+        else:
+            theta = start
+            remaining = self.L
+        for _ in range(remaining):
             theta = self.pair_solve(rhs + self.apply_inner(theta))
         return theta
+
+    def nbjm_solve(self, rhs, tol=1e-9, max_outer=50000):
+        """NestedJacobiPreconditioner.solve (nested_jacobi.py:124-151).  Returns
+        (solution, outer sweeps, converged); on budget exhaustion the solution is the last
+        iterate (the reference raises MaxIterationsExceeded carrying it)."""
+        rhs = np.asarray(rhs, dtype=float)
+        delta = None
+        for s in range(max_outer):
+            if delta is None:
+                new = self.inner_sweep(rhs)
+                prev = np.zeros_like(new)
+            else:
+                new = self.inner_sweep(rhs + self.apply_outer(delta), start=delta)
+                prev = delta
+            if float(np.max(np.abs(new - prev))) < tol:
+                return new, s + 1, True
+            delta = new
+        return delta, max_outer, False
 
     def apply_precond(self, r):
         """NestedJacobiPreconditioner.apply (nested_jacobi.py:105-122)."""

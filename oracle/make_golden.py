@@ -102,6 +102,29 @@ def run_case(name, problem, L=2, S=2, tol=None, rel_tol=None, max_steps=None, pr
           f"({time.time() - t0:.1f}s)", flush=True)
 
 
+def run_nbjm(name, problem, L=2, tol=1e-9, max_outer=50000):
+    """Standalone nested Jacobi solve (nested_jacobi.py:124-151) -> tests/golden/nbjm_<name>.npz."""
+    t0 = time.time()
+    ga = arrays_from_problem(problem)
+    stacked = gridlq.build_stacked(problem)
+    schur = gridlq.build_schur(stacked)
+    pc = gridlq.NestedJacobiPreconditioner(schur, L, 1)
+    rhs = stacked.offset
+    try:
+        x, outers = gridlq.nbjm_solve(pc, rhs, tol=tol, max_outer=max_outer)
+        converged = 1
+    except gridlq.MaxIterationsExceeded as exc:
+        x, outers, converged = exc.iterate, exc.iterations, 0
+    rec = dict(
+        K=ga.K, N=ga.N, T=ga.T, n=ga.n, m=ga.m, A=ga.A, B=ga.B, R=ga.R, C=ga.C,
+        cmask=ga.cmask, Q=ga.Q, dyn_class=ga.dyn_class, cost_class=ga.cost_class,
+        offset=ga.offset, ref_offset=rhs, L=L, tol=tol, max_outer=max_outer, x=x,
+        outers=outers, converged=converged)
+    np.savez_compressed(os.path.join(OUT, f"nbjm_{name}.npz"), **rec)
+    print(f"nbjm_{name}: dim={schur.dim} L={L} outers={outers} conv={converged} "
+          f"({time.time() - t0:.1f}s)", flush=True)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
@@ -109,6 +132,16 @@ def main():
     def want(n):
         return not only or n in only
 
+    if want("nbjm"):
+        msd = gridlq.generate_msd_case
+        run_nbjm("msd_l2", msd(3, 3, 3, seed=1), L=2, tol=1e-9)
+        run_nbjm("msd_l4", msd(3, 3, 3, seed=1), L=4, tol=1e-9)
+        run_nbjm("msd_budget", msd(3, 3, 3, seed=1), L=2, tol=1e-9, max_outer=3)
+        run_nbjm("msd5_l2", msd(5, 5, 5, seed=0), L=2, tol=1e-9)
+        run_nbjm("msd_odd_l2", msd(5, 3, 4, seed=2), L=2, tol=1e-9)
+        run_nbjm("irr_l1", gridlq.generate_irrigation_case(2, 2, 2), L=1, tol=1e-10)
+        run_nbjm("irr_l3", gridlq.generate_irrigation_case(3, 4, 3, seed=2), L=3, tol=1e-9)
+        return
     if want("config1"):
         run_case("config1", arrays_to_problem(G.config1(0)), tol=1e-30, max_steps=50,
                  snap=(1, 25, 50))

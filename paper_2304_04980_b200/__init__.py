@@ -12,7 +12,7 @@ from .problem import (BoundaryData, ConstSeq, GridArrays, GridLayout, GridLQProb
                       problem_from_dict, problem_to_dict, save_problem, validate_arrays)
 from .recovery import TrajectorySolution, kkt_residual, recover_solution
 from .solver import (COUNT_KEYS, GpuNestedJacobiPreconditioner, GpuSchurOperator, SolveReport,
-                     apply_delta, build_schur, cg_solve, pcg_solve)
+                     apply_delta, build_schur, cg_solve, nbjm_solve, pcg_solve)
 
 NestedJacobiPreconditioner = GpuNestedJacobiPreconditioner
 SchurOperator = GpuSchurOperator
@@ -23,7 +23,7 @@ __all__ = [
     "GridArrays", "GridLQError", "GridLQProblem", "GridLayout", "MaxIterationsExceeded",
     "NestedJacobiPreconditioner", "NotPositiveDefiniteError", "SchurOperator", "SolveReport",
     "SubsystemData", "apply_delta", "arrays_from_problem", "arrays_to_problem", "build_schur",
-    "cg_solve", "pcg_solve", "validate_arrays", "TrajectorySolution", "recover_solution",
+    "cg_solve", "nbjm_solve", "pcg_solve", "validate_arrays", "TrajectorySolution", "recover_solution",
     "kkt_residual", "load_problem", "save_problem", "problem_from_dict", "problem_to_dict",
 ]
 

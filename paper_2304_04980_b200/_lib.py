@@ -25,7 +25,7 @@ EXPORTS = (
     "gq_apply_inner_coupling", "gq_pair_solve", "gq_apply_precond", "gq_pcg_start",
     "gq_pcg_run", "gq_pcg_read", "gq_pcg_history", "gq_pcg_scalars", "gq_pcg",
     "gq_profile_steps", "gq_kernel_name", "gq_launches_per_step", "gq_input_dim",
-    "gq_recover", "gq_kkt_residual",
+    "gq_recover", "gq_kkt_residual", "gq_nbjm_solve",
 )
 
 
@@ -85,6 +85,8 @@ def load():
         "gq_input_dim": (i64, [vp]),
         "gq_recover": (ctypes.c_int, [vp, dp, dp, dp, ctypes.POINTER(ctypes.c_double)]),
         "gq_kkt_residual": (ctypes.c_int, [vp, dp, dp, dp, dp, dp]),
+        "gq_nbjm_solve": (ctypes.c_int, [vp, dp, ctypes.c_double, i64, dp,
+                                         ctypes.POINTER(ctypes.c_int64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -576,6 +576,90 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
   return GQ_OK;
 }
 
+// One pair-chain sweep out = Phi~^-1 (rhs + Omega~ th) (th null: out = Phi~^-1 rhs) on whichever
+// sweep kernel the context selected; v1 contexts (no materialised outer rhs) take the
+// outer-coupling source `xi` and add Xi~ xi to rhs on the fly (nested_jacobi.py:79-103).
+static int launch_one_sweep(gq_ctx* c, const double* rhs, const double* th, const double* xi,
+                            double* out) {
+  const bool inner = th != nullptr;
+  if (c->cta && !c->dd) {
+    CK(launch_chain_cta(c->g, c->cto, inner, rhs, th, out, nullptr, c->sm_count, c->partials,
+                        nullptr, kDotNone, c->stream));
+  } else if (c->dd) {
+    CK(launch_chain_dd(c->g, c->co, c->ddo, inner, rhs, th, out, nullptr, c->sm_count,
+                       c->partials, nullptr, kDotNone, c->stream));
+  } else if (c->chain) {
+    CK(launch_chain(c->g, c->co, inner, rhs, th, out, nullptr, c->sm_count, c->partials,
+                    nullptr, kDotNone, c->stream));
+  } else if (c->fast) {
+    CK(launch_sweep3(c->g, c->fo, inner, rhs, th, out, nullptr, c->sm_count, c->partials,
+                     nullptr, kDotNone, c->stream));
+  } else {
+    CK(launch_sweep(c->g, c->op, inner, xi != nullptr, rhs, th, xi, out,
+                    xi != nullptr ? c->sw_outer : c->sw, c->partials, nullptr, kDotNone,
+                    c->stream));
+  }
+  return GQ_OK;
+}
+
+// Standalone nested block Jacobi iteration (nested_jacobi.py:124-151, nbjm_solve :155-159).
+// Outer sweep s = 0 runs L inner sweeps from zero on the right-hand side; every later outer
+// sweep runs L inner sweeps on rhs + Xi~ delta warm-started from delta (so its fixed point
+// solves Delta x = rhs), until max |new - prev| < tol.  Any inner budget >= 1 (odd allowed).
+// The test is read back once per outer sweep.  GQ_MAX_ITER leaves the last iterate in x_out.
+extern "C" int gq_nbjm_solve(gq_ctx* c, const double* rhs, double tol, int64_t max_outer,
+                             double* x_out, int64_t* outers) {
+  if (!c || !rhs || !x_out || !outers) return fail(GQ_INVALID_ARG, "null argument");
+  if (max_outer < 1) return fail(GQ_INVALID_ARG, "need at least one outer sweep");
+  c->started = false;   // the PCG work vectors are reused below
+  int rc = import_vec(c, rhs, c->r);
+  if (rc) return rc;
+  double* delta = c->d;
+  double* fresh = c->q;
+  double* res = reinterpret_cast<double*>(c->st);   // scratch: mu slot of the PCG state
+  unsigned int* counter = &c->st->counter[3];
+  double h = 0.0;
+  for (int64_t s = 0; s < max_outer; ++s) {
+    const double* rhs_s = c->r;
+    const double* xi = nullptr;
+    if (s > 0) {
+      if (c->grid) {
+        CK(launch_grid(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->gsh, c->partials,
+                       nullptr, kDotNone, c->stream));
+        rhs_s = c->rs;
+      } else if (c->fast) {
+        CK(launch_stencil3(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->sh_outer,
+                           c->partials, nullptr, kDotNone, c->stream));
+        rhs_s = c->rs;
+      } else {
+        xi = delta;   // v1 sweeps add Xi~ delta on the fly
+      }
+    }
+    // theta_0 = delta (warm start) for s > 0; from zero at s = 0
+    const double* th = s > 0 ? delta : nullptr;
+    for (int l = 0; l < c->L; ++l) {
+      double* ob = (l == c->L - 1) ? fresh : c->th[l % 2];
+      rc = launch_one_sweep(c, rhs_s, th, xi, ob);
+      if (rc) return rc;
+      th = ob;
+    }
+    CK(launch_maxdiff(c->g, fresh, s > 0 ? delta : nullptr, c->vblocks, c->partials, counter,
+                      res, c->stream));
+    CK(cudaMemcpyAsync(&h, res, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::swap(delta, fresh);   // delta = new
+    if (h < tol) {              // nested_jacobi.py:145-146 (NaN compares false: keeps going)
+      *outers = s + 1;
+      return export_vec(c, delta, x_out);
+    }
+  }
+  *outers = max_outer;
+  rc = export_vec(c, delta, x_out);
+  if (rc) return rc;
+  return fail(GQ_MAX_ITER, "nested Jacobi did not converge within " + std::to_string(max_outer) +
+                               " outer sweeps");
+}
+
 extern "C" int gq_apply_delta(gq_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, x, c->tmp0);

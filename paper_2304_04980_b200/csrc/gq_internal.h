@@ -191,6 +191,10 @@ cudaError_t launch_dirupdate(const Geo& g, double* d, const double* q, int block
                              PcgState* st, cudaStream_t s);
 cudaError_t launch_dirupdate_x(const Geo& g, double* d, const double* q, double* x, int blocks,
                                PcgState* st, cudaStream_t s);
+cudaError_t launch_maxdiff(const Geo& g, const double* a, const double* b, int blocks,
+                          double* partials, unsigned int* counter, double* out, cudaStream_t s);
+cudaError_t launch_add(const Geo& g, double* out, const double* a, const double* b, int blocks,
+                       cudaStream_t s);
 cudaError_t launch_dot(const Geo& g, const double* a, const double* b, int blocks,
                        double* partials, PcgState* st, int dotmode, cudaStream_t s);
 cudaError_t launch_sub(const Geo& g, double* out, const double* a, const double* b, int blocks,

@@ -234,6 +234,28 @@ __global__ void __launch_bounds__(256) k_dirupdate_x(long long dim, double* __re
   }
 }
 
+// max |a - b| (b may be null: max |a|), the successive-iterate test of the standalone nested
+// Jacobi iteration (nested_jacobi.py:145); result in *out, reduced in a fixed order
+__global__ void __launch_bounds__(256) k_maxdiff(long long dim, const double* __restrict__ a,
+                                                 const double* __restrict__ b, double* partials,
+                                                 unsigned int* counter, double* out) {
+  double m = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride)
+    m = nmax(m, fabs(b ? a[e] - b[e] : a[e]));
+  double res;
+  if (grid_reduce<true>(m, partials, counter, res) && threadIdx.x == 0) *out = res;
+}
+
+// out = a + b
+__global__ void __launch_bounds__(256) k_add(long long dim, double* __restrict__ out,
+                                             const double* __restrict__ a,
+                                             const double* __restrict__ b) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < dim; e += stride)
+    out[e] = a[e] + b[e];
+}
+
 __global__ void __launch_bounds__(256) k_dot(long long dim, const double* __restrict__ a,
                                              const double* __restrict__ b, double* partials,
                                              PcgState* st, int dotmode) {
@@ -305,6 +327,18 @@ cudaError_t launch_dirupdate(const Geo& g, double* d, const double* q, int block
 cudaError_t launch_dirupdate_x(const Geo& g, double* d, const double* q, double* x, int blocks,
                                PcgState* st, cudaStream_t s) {
   k_dirupdate_x<<<blocks, 256, 0, s>>>(g.dim, d, q, x, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxdiff(const Geo& g, const double* a, const double* b, int blocks,
+                          double* partials, unsigned int* counter, double* out, cudaStream_t s) {
+  k_maxdiff<<<blocks, 256, 0, s>>>(g.dim, a, b, partials, counter, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add(const Geo& g, double* out, const double* a, const double* b, int blocks,
+                       cudaStream_t s) {
+  k_add<<<blocks, 256, 0, s>>>(g.dim, out, a, b);
   return cudaGetLastError();
 }
 

@@ -132,9 +132,9 @@ def config1(seed=0):
     return random_case(4, 4, 20, 2, 1, seed, rho=0.9, coupling_std=0.05)
 
 
-def config2(seed=0):
+def config2(seed=0, K=16, N=16, T=50):
     """Mass-spring-damper 16x16, T=50."""
-    return msd_case(16, 16, 50, seed)
+    return msd_case(K, N, T, seed)
 
 
 def config3(seed=0, K=64, N=64, T=100):

@@ -252,6 +252,31 @@ class GpuNestedJacobiPreconditioner:
             return np.stack([self.apply(r[:, c]) for c in range(r.shape[1])], axis=1)
         return self.schur._ctx.unary("gq_apply_precond", r, "r")
 
+    def solve(self, rhs, tol=1e-9, max_outer=50000, pool=None):
+        """Standalone nested Jacobi iteration (``nested_jacobi.py:124-151``) on the device.
+
+        Outer sweeps run until the successive-iterate infinity norm drops below ``tol``;
+        inner sweeps are warm-started from the current outer iterate, so any inner budget
+        >= 1 is allowed.  Returns ``(solution, outer sweep count)``; raises
+        MaxIterationsExceeded carrying the last iterate when the budget runs out.  ``pool``
+        is accepted and ignored.
+        """
+        ctx = self.schur._ctx
+        max_outer = int(max_outer)
+        msg = f"nested Jacobi did not converge within {max_outer} outer sweeps"
+        v = _Vec(rhs, self.dim, "rhs")
+        if max_outer < 1:            # the reference loop never runs
+            raise MaxIterationsExceeded(msg, iterate=None, iterations=max_outer)
+        self._select()
+        out = v.like()
+        outers = ctypes.c_int64()
+        rc = ctx.lib.gq_nbjm_solve(ctx.h, v.ptr, float(tol), max_outer, _ptr(out),
+                                   ctypes.byref(outers))
+        if rc == _lib.GQ_MAX_ITER:
+            raise MaxIterationsExceeded(msg, iterate=out, iterations=max_outer)
+        _lib.check(rc, "nbjm_solve")
+        return out, int(outers.value)
+
     def pair_solves(self, rhs):
         """Phi~^-1 rhs over every (pair, stage) chain (nested_jacobi.py:65-77)."""
         return self.schur._ctx.unary("gq_pair_solve", rhs, "rhs")
@@ -259,6 +284,13 @@ class GpuNestedJacobiPreconditioner:
     def apply_inner_coupling(self, x):
         """Omega~ x (kkt_assembly.py:645-662)."""
         return self.schur._ctx.unary("gq_apply_inner_coupling", x)
+
+
+def nbjm_solve(precond: GpuNestedJacobiPreconditioner, rhs, tol=1e-9, max_outer=50000,
+               pool=None):
+    """Standalone nested-Jacobi solve with an existing preconditioner's factors and budgets
+    (``nested_jacobi.py:155-159``)."""
+    return precond.solve(rhs, tol=tol, max_outer=max_outer, pool=pool)
 
 
 def _op_counts(dim, matvec, precond_flops, steps, converged, warm):

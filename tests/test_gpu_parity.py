@@ -186,3 +186,48 @@ def test_headline_properties():
     assert rep.steps == 100 and h[-1] < 1e-6 * h[0]
     true_r = rhs - op.apply(x)
     assert float(true_r.abs().max()) < 1e-8 * float(rhs.abs().max()) + 10 * h[-1]
+
+
+def test_nbjm_parity(nbjm_golden):
+    """Device standalone nested Jacobi solve vs the reference's nbjm_solve."""
+    from paper_2304_04980_b200 import (GpuNestedJacobiPreconditioner, GpuSchurOperator,
+                                       MaxIterationsExceeded, nbjm_solve)
+
+    name, ga, rec = nbjm_golden
+    op = GpuSchurOperator(ga, rec["L"], 1)
+    pc = GpuNestedJacobiPreconditioner(op, rec["L"], 1)
+    if rec["converged"]:
+        x, outers = nbjm_solve(pc, ga.offset, tol=rec["tol"], max_outer=rec["max_outer"])
+    else:
+        with pytest.raises(MaxIterationsExceeded) as info:
+            pc.solve(ga.offset, tol=rec["tol"], max_outer=rec["max_outer"])
+        x, outers = info.value.iterate, info.value.iterations
+        assert x is not None
+    assert outers == rec["outers"]
+    assert rel_err(x, rec["x"]) < 1e-9
+    # the fixed point solves Delta x = rhs
+    if rec["converged"]:
+        res = np.max(np.abs(op.apply(x) - ga.offset)) / np.max(np.abs(ga.offset))
+        assert res < 1e-6
+
+
+def test_nbjm_budget_and_device_vectors():
+    """max_outer < 1 raises with no iterate (the reference loop never runs); torch device
+    vectors in and out."""
+    import torch
+    from paper_2304_04980_b200 import (GpuNestedJacobiPreconditioner, GpuSchurOperator,
+                                       MaxIterationsExceeded, generators)
+
+    ga = generators.config1(0)
+    op = GpuSchurOperator(ga, 2, 2)
+    pc = GpuNestedJacobiPreconditioner(op, 2, 2)
+    with pytest.raises(MaxIterationsExceeded) as info:
+        pc.solve(ga.offset, max_outer=0)
+    assert info.value.iterate is None
+    rhs = torch.tensor(ga.offset, device="cuda", dtype=torch.float64)
+    with pytest.raises(MaxIterationsExceeded) as info:
+        pc.solve(rhs, tol=1e-30, max_outer=4)
+    assert isinstance(info.value.iterate, torch.Tensor) and info.value.iterations == 4
+    with pytest.raises(MaxIterationsExceeded) as info2:
+        pc.solve(ga.offset, tol=1e-30, max_outer=4)
+    assert rel_err(info.value.iterate.cpu().numpy(), info2.value.iterate) < 1e-15

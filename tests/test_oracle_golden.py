@@ -87,3 +87,15 @@ def test_c_oracle_matches_golden(golden):
                                                  max_steps=rec["max_steps"],
                                                  precond=bool(rec["precond"]))
         check_run(name, rec, x, hist, steps, conv, {})
+
+
+def test_nbjm_parity(nbjm_golden):
+    """Standalone nested Jacobi (nested_jacobi.py:124-151): same outer-sweep count and the
+    same solution / last iterate as the reference."""
+    name, ga, rec = nbjm_golden
+    assert np.array_equal(ga.offset, rec["ref_offset"])
+    orc = Oracle(ga, rec["L"], 1)
+    x, outers, conv = orc.nbjm_solve(ga.offset, tol=rec["tol"], max_outer=rec["max_outer"])
+    assert int(conv) == rec["converged"]
+    assert outers == rec["outers"]
+    assert rel_err(x, rec["x"]) < 1e-9
