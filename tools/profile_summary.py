@@ -5,7 +5,9 @@ profiles/ncu_traffic.json (dram bytes per launch, keyed by the bench's kernel na
 """
 import csv, io, json, os, subprocess, sys
 
-STEP_NAMES = ["delta", "update_x", "update", "sweep_s0_l0", "sweep_s0_l1", "outer_rhs_s1",
+# one PCGM step as captured by tools/stepprof.py (launch order); the first outer sweep
+# carries the fused r update (sweep_s0_l0_r)
+STEP_NAMES = ["delta", "update_x", "sweep_s0_l0_r", "sweep_s0_l1", "outer_rhs_s1",
               "sweep_s1_l0", "sweep_s1_l1", "dirupdate"]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
