@@ -66,6 +66,8 @@ struct gq_ctx {
   double* ddarena = nullptr;
   DDOps ddo{};
   bool grid = false;           // lean n = 2 grid stencils
+  bool dfac = false;           // factored Delta apply (time-invariant n = 2)
+  double* dfac_ops = nullptr;  // its per-node operator records
   GridShape gsh{};
   bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
   double* partials = nullptr;
@@ -109,7 +111,7 @@ static void release(gq_ctx* c) {
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
                   c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
                   c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->cgt, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
+                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->cgt, c->dfac_ops, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -412,6 +414,12 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   c->sh_delta = stencil_shape(g, kDelta, c->sm_count);
   c->grid = c->fast && grid_supported(g.n);
   if (c->grid) c->gsh = grid_shape(g, c->sm_count);
+  if (dfac_supported(g, D.n_dyn, D.n_cost)) {
+    CKB(dalloc(&c->dfac_ops, (size_t)g.nk * 48));
+    CKB(launch_build_dfac(g, c->A, c->C, c->qinv, c->brb, c->dfac_ops, c->stream));
+    CKB(cudaStreamSynchronize(c->stream));
+    c->dfac = true;
+  }
   c->sh_outer = stencil_shape(g, kOuter, c->sm_count);
   c->sh_inner = stencil_shape(g, kInner, c->sm_count);
   c->sw = sweep_shape(g, false);
@@ -423,6 +431,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                              fast_max_blocks(g, c->sh_outer, c->sm_count),
                              c->chain ? chain_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->cta ? cta_max_blocks(g) : 0LL,
+                             c->dfac ? dfac_max_blocks(c->sm_count) : 0LL,
                              c->chain ? chain_fr_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->grid ? (long long)c->gsh.blocks : 0LL});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));
@@ -664,7 +673,10 @@ extern "C" int gq_apply_delta(gq_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, x, c->tmp0);
   if (rc) return rc;
-  if (c->grid)
+  if (c->dfac)
+    CK(launch_dfac(c->g, c->dfac_ops, c->tmp0, c->y, c->partials, nullptr, kDotNone,
+                   c->sm_count, c->stream));
+  else if (c->grid)
     CK(launch_grid(c->g, c->fo, kDelta, c->tmp0, nullptr, c->y, c->gsh, c->partials, nullptr,
                    kDotNone, c->stream));
   else if (c->fast)
@@ -726,7 +738,10 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
   };
   int rc = mark();
   if (rc) return rc;
-  if (c->grid)
+  if (c->dfac)
+    CK(launch_dfac(c->g, c->dfac_ops, c->d, c->y, c->partials, c->st, kDotStep, c->sm_count,
+                   c->stream));
+  else if (c->grid)
     CK(launch_grid(c->g, c->fo, kDelta, c->d, nullptr, c->y, c->gsh, c->partials, c->st,
                    kDotStep, c->stream));
   else if (c->fast)

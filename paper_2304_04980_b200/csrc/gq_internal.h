@@ -166,6 +166,15 @@ cudaError_t launch_chain_cta(const Geo& g, const CtaOps& co, bool inner, const d
                              double* partials, PcgState* st, int dotmode, cudaStream_t s);
 long long cta_max_blocks(const Geo& g);
 
+// ---- factored Delta apply, time-invariant n = 2 (gq_dfac.cu) ----
+bool dfac_supported(const Geo& g, int n_dyn, int n_cost);
+cudaError_t launch_build_dfac(const Geo& g, const double* A, const double* C, const double* qinv,
+                              const double* brb, double* rec, cudaStream_t s);
+// y = Delta x (+ y.x curvature, alpha, breakdown when dotmode != kDotNone)
+cudaError_t launch_dfac(const Geo& g, const double* ops, const double* x, double* y,
+                        double* partials, PcgState* st, int dotmode, int sm_count, cudaStream_t s);
+long long dfac_max_blocks(int sm_count);
+
 // ---- lean n = 2 grid stencils (gq_grid.cu) ----
 struct GridShape {
   int nchunk = 0, nstrip = 0, rows = 0, blocks = 0;

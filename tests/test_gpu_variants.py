@@ -28,6 +28,8 @@ VARIANTS = {
     "fuse_x": {"GQ_FUSE_X": "1"},                # x update fused into the direction update
     "no_fuse_r": {"GQ_NO_FUSE_R": "1"},          # separate r update kernel
     "no_fuse": {"GQ_NO_FUSE_R": "1", "GQ_NO_FORK": "1"},
+    "dfac": {"GQ_DFAC": "1"},                    # factored Delta apply (CTA, w shared in smem)
+    "dfac16": {"GQ_DFAC": "1", "GQ_DFAC_NW": "16"},
     "no_fork": {"GQ_NO_FORK": "1"},              # x update in line instead of on a branch
     "dd4": {"GQ_DD": "1"},                       # domain-decomposed chain solve, 4 segments
     "dd8": {"GQ_DD": "1", "GQ_DD_W": "8"},       # ... 8 segments
