@@ -48,14 +48,18 @@ namespace {
 
 using namespace as;
 
-constexpr int CW = 5;                  // consumer warps per CTA
-constexpr int CT = 32 * CW;            // threads per CTA
-constexpr int CST = 8 * CW;            // stages per CTA item
-constexpr int PITCH = 2 * (CST + 2);   // doubles per staged record (2-stage pad)
-constexpr int RECB = 8 * PITCH;        // 672 bytes
+// CW consumer warps per CTA (5 by default; 1 gives a per-warp TMA pipeline)
+template <int CW>
+struct Cg {
+  static constexpr int CT = 32 * CW;            // threads per CTA
+  static constexpr int CST = 8 * CW;            // stages per CTA item
+  static constexpr int PITCH = 2 * (CST + 2);   // doubles per staged record (2-stage pad)
+  static constexpr int RECB = 8 * PITCH;        // bytes per record (672 at CW = 5)
+};
 
-template <bool INNER>
+template <bool INNER, int CW>
 struct Cc {
+  static constexpr int PITCH = Cg<CW>::PITCH, RECB = Cg<CW>::RECB;
   // forward: tau box (4 records) | a-1 box (4) | a+2 box (4) | a-2 box (2) | pad (2) |
   //          a+3 box (2) | factor tiles
   static constexpr int NRF = INNER ? 18 : 4;
@@ -141,10 +145,11 @@ struct CtaArgs {
 
 }  // namespace
 
-template <bool INNER, int R>
-__global__ void __launch_bounds__(CT) k_chain_cta(const __grid_constant__ CtaMaps tm,
-                                                  const CtaArgs a) {
-  using C = Cc<INNER>;
+template <bool INNER, int R, int CW>
+__global__ void __launch_bounds__(32 * CW) k_chain_cta(const __grid_constant__ CtaMaps tm,
+                                                       const CtaArgs a) {
+  using C = Cc<INNER, CW>;
+  constexpr int CT = Cg<CW>::CT, CST = Cg<CW>::CST, PITCH = Cg<CW>::PITCH, RECB = Cg<CW>::RECB;
   extern __shared__ unsigned char smraw[];
   if (halted(a.st)) return;
   // 128-byte aligned ring; offsetting smraw keeps the pointer in the shared window, so the
@@ -465,12 +470,12 @@ int env_i(const char* name, int dflt) {
 }
 
 // vector v[j][i][t][k] as a 3-D tensor (2*T1 doubles, K rows, N columns)
-bool make_map(CUtensorMap* m, const Geo& g, const double* base, int rows, int cols) {
+bool make_map(CUtensorMap* m, const Geo& g, const double* base, int rows, int cols, int pitch) {
   EncodeTiled enc = encoder();
   if (!enc || base == nullptr) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)g.T1 * 2, (cuuint64_t)g.K, (cuuint64_t)g.N};
   const cuuint64_t strides[2] = {(cuuint64_t)g.T1 * 16, (cuuint64_t)g.T1 * 16 * g.K};
-  const cuuint32_t box[3] = {(cuuint32_t)PITCH, (cuuint32_t)rows, (cuuint32_t)cols};
+  const cuuint32_t box[3] = {(cuuint32_t)pitch, (cuuint32_t)rows, (cuuint32_t)cols};
   const cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -478,20 +483,21 @@ bool make_map(CUtensorMap* m, const Geo& g, const double* base, int rows, int co
          CUDA_SUCCESS;
 }
 
-template <bool INNER, int R>
+template <bool INNER, int R, int CW>
 cudaError_t cta_launch(const CtaMaps& tm, const CtaArgs& a, int sm_count, cudaStream_t s) {
+  constexpr int CT = Cg<CW>::CT;
   // GQ_CTA_CPS caps the resident CTAs per SM (extra dynamic shared memory per CTA)
   const int cps = env_i("GQ_CTA_CPS", 0);
-  size_t smem = (size_t)R * Cc<INNER>::SLOT * 8 + (2 * R + 1) * 8 + 128;
+  size_t smem = (size_t)R * Cc<INNER, CW>::SLOT * 8 + (2 * R + 1) * 8 + 128;
   if (cps > 0) smem = std::max(smem, (size_t)(225 * 1024 / cps));
   static int cache[8][64] = {{0}};
   int per_sm = 1;
-  cudaError_t e = kernel_occupancy(k_chain_cta<INNER, R>, CT, smem, cache[std::min(cps, 7)], per_sm);
+  cudaError_t e = kernel_occupancy(k_chain_cta<INNER, R, CW>, CT, smem, cache[std::min(cps, 7)], per_sm);
   if (e != cudaSuccess) return e;
   // persistent only when asked (GQ_CTA_PERSIST=1); by default one CTA per item
   int blocks = a.n_items;
   if (env_i("GQ_CTA_PERSIST", 0)) blocks = std::max(1, std::min(a.n_items, per_sm * sm_count));
-  k_chain_cta<INNER, R><<<blocks, CT, smem, s>>>(tm, a);
+  k_chain_cta<INNER, R, CW><<<blocks, CT, smem, s>>>(tm, a);
   return cudaGetLastError();
 }
 
@@ -532,19 +538,21 @@ cudaError_t cta_check_stage0(const Geo& g, int c0, const double* ff, const doubl
   return e;
 }
 
-cudaError_t launch_chain_cta(const Geo& g, const CtaOps& co, bool inner, const double* rhs,
-                             const double* th, double* out, const double* rdot, int sm_count,
-                             double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+template <int CW>
+static cudaError_t chain_cta_w(const Geo& g, const CtaOps& co, bool inner, const double* rhs,
+                               const double* th, double* out, const double* rdot, int sm_count,
+                               double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  constexpr int CST = Cg<CW>::CST, PITCH = Cg<CW>::PITCH;
   CtaMaps tm;
   memset(&tm, 0, sizeof(tm));
   const bool dotting = dotmode != kDotNone;
-  if (!make_map(&tm.rhs, g, rhs, 2, 2) || !make_map(&tm.w, g, out, 2, 2))
+  if (!make_map(&tm.rhs, g, rhs, 2, 2, PITCH) || !make_map(&tm.w, g, out, 2, 2, PITCH))
     return cudaErrorInvalidValue;
-  if (inner && (!make_map(&tm.th4, g, th, 4, 1) || !make_map(&tm.th2, g, th, 2, 1)))
+  if (inner && (!make_map(&tm.th4, g, th, 4, 1, PITCH) || !make_map(&tm.th2, g, th, 2, 1, PITCH)))
     return cudaErrorInvalidValue;
   if (!inner) tm.th4 = tm.th2 = tm.rhs;
   if (dotting) {
-    if (!make_map(&tm.r, g, rdot, 2, 2)) return cudaErrorInvalidValue;
+    if (!make_map(&tm.r, g, rdot, 2, 2, PITCH)) return cudaErrorInvalidValue;
   } else {
     tm.r = tm.rhs;
   }
@@ -566,21 +574,30 @@ cudaError_t launch_chain_cta(const Geo& g, const CtaOps& co, bool inner, const d
   a.dotmode = dotmode;
   const int r = env_i(inner ? "GQ_CTA_R_INNER" : "GQ_CTA_R_OUTER", inner ? 3 : 5);
   if (inner) {
-    if (r == 6) return cta_launch<true, 6>(tm, a, sm_count, s);
-    if (r == 8) return cta_launch<true, 8>(tm, a, sm_count, s);
-    if (r == 4) return cta_launch<true, 4>(tm, a, sm_count, s);
-    if (r == 2) return cta_launch<true, 2>(tm, a, sm_count, s);
-    return cta_launch<true, 3>(tm, a, sm_count, s);
+    if (r == 6) return cta_launch<true, 6, CW>(tm, a, sm_count, s);
+    if (r == 4) return cta_launch<true, 4, CW>(tm, a, sm_count, s);
+    if (r == 2) return cta_launch<true, 2, CW>(tm, a, sm_count, s);
+    return cta_launch<true, 3, CW>(tm, a, sm_count, s);
   }
-  if (r == 3) return cta_launch<false, 3>(tm, a, sm_count, s);
-  if (r == 4) return cta_launch<false, 4>(tm, a, sm_count, s);
-  if (r == 7) return cta_launch<false, 7>(tm, a, sm_count, s);
-  if (r == 11) return cta_launch<false, 11>(tm, a, sm_count, s);
-  return cta_launch<false, 5>(tm, a, sm_count, s);
+  if (r == 3) return cta_launch<false, 3, CW>(tm, a, sm_count, s);
+  if (r == 7) return cta_launch<false, 7, CW>(tm, a, sm_count, s);
+  return cta_launch<false, 5, CW>(tm, a, sm_count, s);
+}
+
+static int cta_w() { return env_i("GQ_CTA_W", 5); }
+
+cudaError_t launch_chain_cta(const Geo& g, const CtaOps& co, bool inner, const double* rhs,
+                             const double* th, double* out, const double* rdot, int sm_count,
+                             double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  switch (cta_w()) {
+    case 1: return chain_cta_w<1>(g, co, inner, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    case 2: return chain_cta_w<2>(g, co, inner, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    default: return chain_cta_w<5>(g, co, inner, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  }
 }
 
 long long cta_max_blocks(const Geo& g) {
-  return (long long)g.V * ((g.T1 - 1 + CST - 1) / CST);
+  return (long long)g.V * ((g.T1 - 1 + 8 - 1) / 8);   // the finest item split (CW = 1)
 }
 
 }  // namespace gq
