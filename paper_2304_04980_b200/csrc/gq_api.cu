@@ -67,6 +67,7 @@ struct gq_ctx {
   DDOps ddo{};
   bool grid = false;           // lean n = 2 grid stencils
   bool dfac = false;           // factored Delta apply (time-invariant n = 2)
+  bool st8 = false;            // n = 8 DMMA block stencils
   double* dfac_ops = nullptr;  // its per-node operator records
   GridShape gsh{};
   bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
@@ -402,6 +403,28 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
     }
   }
 
+  if (!c->fast && g.n == 8 && chain_supported(g.n)) {
+    // n = 8: DMMA pair-chain sweeps without the fast-path stencils (generic v1 stencils for
+    // Delta and Xi~); the chain tiles need the cross-pair Psi blocks
+    std::vector<int4> s8;
+    for (int t = 0; t < g.T1;) {
+      int e = t + 1;
+      while (e < g.T1 && e - t < 8 && pcls[e] == pcls[t]) ++e;
+      s8.push_back(make_int4(t, e - t, pcls[t], 0));
+      t = e;
+    }
+    CKB(dalloc(&c->omega, (size_t)c->npc * nk * 5 * nn));
+    CKB(launch_build_omega(g, c->npc, c->psi, c->omega, c->stream));
+    CKB(dalloc(&c->cff, chain_ff_doubles(g, c->npc)));
+    CKB(dalloc(&c->cfb, chain_fb_doubles(g, c->npc)));
+    CKB(dalloc(&c->seg, s8.size()));
+    CKB(cudaMemcpy(c->seg, s8.data(), s8.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CKB(launch_build_chain(g, c->npc, c->fac, c->omega, c->cff, c->cfb, c->stream));
+    CKB(cudaStreamSynchronize(c->stream));
+    c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg, (int)s8.size()};
+    c->chain = true;
+    c->st8 = st8_supported(g, c->nxc);
+  }
   {
     const char* e = getenv("GQ_NO_FUSE_R");
     c->fuse_r = c->chain && !c->dd && !c->cta && !(e && *e == '1');
@@ -432,6 +455,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                              c->chain ? chain_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->cta ? cta_max_blocks(g) : 0LL,
                              c->dfac ? dfac_max_blocks(c->sm_count) : 0LL,
+                             c->st8 ? st8_max_blocks(c->sm_count) : 0LL,
                              c->chain ? chain_fr_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->grid ? (long long)c->gsh.blocks : 0LL});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));
@@ -531,14 +555,22 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
                            const std::function<int()>& mark = nullptr,
                            const double* fuse_y = nullptr) {
   for (int s = 0; s < c->S; ++s) {
-    if (c->fast && s > 0) {
+    if ((c->fast || c->chain) && s > 0) {
       // rhs_s = r + Xi~ delta_{s-1}, materialised once per outer sweep (nested_jacobi.py:119-121)
-      if (c->grid)
+      if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->gsh,
                        c->partials, st, kDotNone, c->stream));
-      else
+      } else if (c->fast) {
         CK(launch_stencil3(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->sh_outer,
                            c->partials, st, kDotNone, c->stream));
+      } else if (c->st8) {
+        CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kOuterRhs, c->dl[(s - 1) % 2], rin,
+                      c->rs, c->sm_count, c->partials, st, kDotNone, c->stream));
+      } else {   // chain sweeps without the fast stencils: generic Xi~ apply + add
+        CK(launch_stencil(c->g, c->op, kOuter, c->dl[(s - 1) % 2], c->rs, c->sh_outer,
+                          c->partials, st, kDotNone, c->stream));
+        CK(launch_add(c->g, c->rs, rin, c->rs, c->vblocks, c->stream));
+      }
       if (names) names->push_back("outer_rhs_s" + std::to_string(s));
       if (mark) {
         const int rc = mark();
@@ -574,7 +606,7 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
       }
       if (names)
         names->push_back("sweep_s" + std::to_string(s) + "_l" + std::to_string(l) +
-                         (!c->fast && s > 0 ? "_xi" : "") +
+                         (!c->fast && !c->chain && s > 0 ? "_xi" : "") +
                          (fuse_y != nullptr && s == 0 && l == 0 ? "_r" : ""));
       if (mark) {
         const int rc = mark();
@@ -640,6 +672,15 @@ extern "C" int gq_nbjm_solve(gq_ctx* c, const double* rhs, double tol, int64_t m
         CK(launch_stencil3(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->sh_outer,
                            c->partials, nullptr, kDotNone, c->stream));
         rhs_s = c->rs;
+      } else if (c->st8) {
+        CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kOuterRhs, delta, c->r, c->rs,
+                      c->sm_count, c->partials, nullptr, kDotNone, c->stream));
+        rhs_s = c->rs;
+      } else if (c->chain) {
+        CK(launch_stencil(c->g, c->op, kOuter, delta, c->rs, c->sh_outer, c->partials, nullptr,
+                          kDotNone, c->stream));
+        CK(launch_add(c->g, c->rs, c->r, c->rs, c->vblocks, c->stream));
+        rhs_s = c->rs;
       } else {
         xi = delta;   // v1 sweeps add Xi~ delta on the fly
       }
@@ -673,7 +714,10 @@ extern "C" int gq_apply_delta(gq_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, x, c->tmp0);
   if (rc) return rc;
-  if (c->dfac)
+  if (c->st8)
+    CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kDelta, c->tmp0, nullptr, c->y,
+                  c->sm_count, c->partials, nullptr, kDotNone, c->stream));
+  else if (c->dfac)
     CK(launch_dfac(c->g, c->dfac_ops, c->tmp0, c->y, c->partials, nullptr, kDotNone,
                    c->sm_count, c->stream));
   else if (c->grid)
@@ -738,7 +782,10 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
   };
   int rc = mark();
   if (rc) return rc;
-  if (c->dfac)
+  if (c->st8)
+    CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kDelta, c->d, nullptr, c->y, c->sm_count,
+                  c->partials, c->st, kDotStep, c->stream));
+  else if (c->dfac)
     CK(launch_dfac(c->g, c->dfac_ops, c->d, c->y, c->partials, c->st, kDotStep, c->sm_count,
                    c->stream));
   else if (c->grid)
@@ -807,7 +854,7 @@ extern "C" int gq_launches_per_step(gq_ctx* c) {
   if (!c) return -1;
   const int vec = c->fuse_x ? 3 : 4;   // delta, r update, direction update (+ x update)
   if (!c->use_precond) return vec + 1;
-  return vec - (c->fuse_r ? 1 : 0) + c->S * c->L + (c->fast ? c->S - 1 : 0);
+  return vec - (c->fuse_r ? 1 : 0) + c->S * c->L + (c->fast || c->chain ? c->S - 1 : 0);
 }
 
 extern "C" int gq_pcg_start(gq_ctx* c, const double* rhs, const double* x0, int32_t use_precond) {

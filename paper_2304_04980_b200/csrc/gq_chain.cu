@@ -122,11 +122,17 @@ struct Ch {
   static constexpr int NRF = INNER ? 16 : (FR ? 8 : 4);
   static constexpr int JF = NRF / RPI, JB = 8 / RPI;  // record instructions fwd / bwd (w + r)
   static constexpr int CFF = FF / 64, CFB = FB / 64;  // factor instructions (32 x 16 B each)
+  // n = 8: the factor tiles of a block (40 KB inner) are not staged; B fragments are read
+  // straight from global memory (L1-cached, shared by the warps of an SM that work on the
+  // same pair, see k_chain's item mapping)
+  static constexpr bool BG = NS == 8;
+  static constexpr int FFST = BG ? 0 : FF, FBST = BG ? 0 : FB;   // staged factor doubles
   // record stride in shared memory: padded by 16*NS bytes so the A-fragment reads of a
   // quarter warp (4 records x 2 chains) hit 8 distinct 16-byte bank groups
   static constexpr int RSTR = REC + 2 * NS;
-  static constexpr int SLOT = (NRF * RSTR + FF) > (8 * RSTR + FB) ? (NRF * RSTR + FF) : (8 * RSTR + FB);
-  static_assert(NS == 2 || NS == 4, "chain sweep needs n in {2, 4}");
+  static constexpr int SLOT = (NRF * RSTR + FFST) > (8 * RSTR + FBST) ? (NRF * RSTR + FFST)
+                                                                     : (8 * RSTR + FBST);
+  static_assert(NS == 2 || NS == 4 || NS == 8, "chain sweep needs n in {2, 4, 8}");
   static_assert(CPR <= 32 && 32 % CPR == 0, "a record must split evenly over the warp");
   static_assert(FF % 64 == 0 && FB % 64 == 0, "factor blocks must be whole warp copies");
 };
@@ -151,6 +157,13 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   // and completes on the slot's mbarrier; records stay on per-lane LDGSTS
   using C = Ch<NS, INNER, MT, FR>;
   constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::RSTR, R = P + 1;
+  // B fragment: staged tile in shared memory, or (n = 8) the tile in global memory
+  auto ldb = [](const double* p) -> double2 {
+    if constexpr (C::BG)
+      return __ldg(reinterpret_cast<const double2*>(p));
+    else
+      return lds2(p);
+  };
   const int lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
   const long long rs = (long long)g.T1 * NS;
   const long long cs = (long long)g.K * rs;
@@ -216,10 +229,12 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     if constexpr (TF) {
       bulk_f(k, slot);
     } else {
-      const double* fp = ffb + (long long)k * C::FFS;
+      if constexpr (!C::BG) {
+        const double* fp = ffb + (long long)k * C::FFS;
 #pragma unroll
-      for (int i = 0; i < C::CFF; ++i)
-        ldgsts(facf_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
+        for (int i = 0; i < C::CFF; ++i)
+          ldgsts(facf_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
+      }
     }
   };
 
@@ -275,7 +290,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
           ldgsts(rec_dst + sb + j * C::RPI * REC * 8, fcur[j], fsz[j], pol_s);
         if constexpr (TF) {
           bulk_f(kk, islot);
-        } else {
+        } else if constexpr (!C::BG) {
 #pragma unroll
           for (int i = 0; i < C::CFF; ++i)
             ldgsts(facf_dst + sb + 512 * i, fpc + 64 * i, 16, pol_k);
@@ -292,7 +307,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     __syncwarp();
 
     const double* sl = ring + slot * C::SLOT;
-    const double* sf = sl + C::NRF * REC;
+    const double* sf = C::BG ? ffb0 + (long long)k * C::FFS : sl + C::NRF * REC;
     // A operands: tau k-pairs and theta k-pairs of every M-tile
     double2 tv[MT][NT];
 #pragma unroll
@@ -325,7 +340,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
         a0[m] = a1[m] = g0[m] = g1[m] = m0[m] = m1[m] = m2[m] = m3[m] = make_double2(0.0, 0.0);
 #pragma unroll
       for (int p = 0; p < NT; ++p) {
-        const double2 b = lds2(sf + (h * NT + p) * 64 + rw * 8 + 2 * qd);
+        const double2 b = ldb(sf + (h * NT + p) * 64 + rw * 8 + 2 * qd);
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
           dmma(a0[m], tv[m][p].x, b.x);
@@ -335,7 +350,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       if (INNER) {
 #pragma unroll
         for (int p = 0; p < KT; ++p) {
-          const double2 b = lds2(sf + 2 * QQ + (h * KT + p) * 64 + rw * 8 + 2 * qd);
+          const double2 b = ldb(sf + 2 * QQ + (h * KT + p) * 64 + rw * 8 + 2 * qd);
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
             const double2 tq = lds2(sl + aofs(4, m, 8 * p + 2 * qd));
@@ -351,7 +366,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       }
 #pragma unroll
       for (int p = 0; p < NT; ++p) {
-        const double2 b = lds2(sf + QQ + (h * NT + p) * 64 + rw * 8 + 2 * qd);
+        const double2 b = ldb(sf + QQ + (h * NT + p) * 64 + rw * 8 + 2 * qd);
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
           dmma(g0[m], wd[m][p].x, b.x);
@@ -415,10 +430,12 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     if constexpr (TF) {
       bulk_b(k, slot_);
     } else {
-      const double* fp = fbb + (long long)k * C::FB;
+      if constexpr (!C::BG) {
+        const double* fp = fbb + (long long)k * C::FB;
 #pragma unroll
-      for (int i = 0; i < C::CFB; ++i)
-        ldgsts(facb_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
+        for (int i = 0; i < C::CFB; ++i)
+          ldgsts(facb_dst + sb + 512 * i, fp + 64 * i, 16, pol_k);
+      }
     }
   };
   {
@@ -454,7 +471,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
         ldgsts(rec_dst + sb + j * C::RPI * REC * 8, bcur[j], bsz[j], pol_s);
       if constexpr (TF) {
         bulk_b(kk, islot);
-      } else {
+      } else if constexpr (!C::BG) {
 #pragma unroll
         for (int i = 0; i < C::CFB; ++i)
           ldgsts(facb_dst + sb + 512 * i, fbc + 64 * i, 16, pol_k);
@@ -470,7 +487,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     __syncwarp();
 
     const double* sl = ring + slot * C::SLOT;
-    const double* sf = sl + 8 * REC;
+    const double* sf = C::BG ? fbb0 + (long long)k * C::FB : sl + 8 * REC;
     double2 wv[MT][NT];
 #pragma unroll
     for (int m = 0; m < MT; ++m)
@@ -484,7 +501,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       for (int m = 0; m < MT; ++m) a0[m] = a1[m] = g0[m] = g1[m] = make_double2(0.0, 0.0);
 #pragma unroll
       for (int p = 0; p < NT; ++p) {
-        const double2 b = lds2(sf + (h * NT + p) * 64 + rw * 8 + 2 * qd);
+        const double2 b = ldb(sf + (h * NT + p) * 64 + rw * 8 + 2 * qd);
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
           dmma(a0[m], wv[m][p].x, b.x);
@@ -493,7 +510,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
       }
 #pragma unroll
       for (int p = 0; p < NT; ++p) {
-        const double2 b = lds2(sf + QQ + (h * NT + p) * 64 + rw * 8 + 2 * qd);
+        const double2 b = ldb(sf + QQ + (h * NT + p) * 64 + rw * 8 + 2 * qd);
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
           dmma(g0[m], xd[m][p].x, b.x);
@@ -536,7 +553,7 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
                                               const double* __restrict__ rdot, int n_items,
                                               double* partials, PcgState* st, int dotmode,
                                               const double* __restrict__ yv = nullptr,
-                                              double* rupd = nullptr) {
+                                              double* rupd = nullptr, int smc = 0) {
   extern __shared__ __align__(16) double ring[];
   if (halted(st)) return;
   const double alpha = FR ? st->alpha : 0.0;
@@ -554,10 +571,21 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
     fence_proxy_async();
     __syncwarp();
   }
+  // n = 8 reads its factor tiles through L1: map the work so that the warps resident on one
+  // SM (blocks b = s, s + smc, s + 2 smc, ... when the grid is per_sm x smc) take consecutive
+  // stage chunks of the same pair.  A different block-to-SM placement only costs L1 hits.
+  const int G = gridDim.x;
+  const bool grouped = Ch<NS, INNER, MT, FR>::BG && smc > 0 && G % smc == 0;
+  const int per = grouped ? G / smc : 1;
+  // round r covers units [r G, r G + G): a permutation of the blocks in every round, so a
+  // partial last round skips exactly the units past n_items
+  const int off = grouped ? (blockIdx.x % smc) * per + blockIdx.x / smc : blockIdx.x;
 #pragma unroll 1
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int v = item / nseg;
-    const int4 sg = seg[item - v * nseg];
+  for (int base = 0; base < n_items; base += G) {
+    const int u = base + off;
+    if (u >= n_items) continue;
+    const int v = u / nseg;
+    const int4 sg = seg[u - v * nseg];
     chain_item<NS, INNER, P, MT, TF, FR>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x,
                                          sg.y, sg.z, pol_s, pol_k, dot, 0, g.nb, co.ff, co.fb,
                                          nullptr, bars, &phase, yv, rupd, alpha, &rmax);
@@ -817,6 +845,33 @@ __global__ void k_build_chain(Geo g, int npc, const double* __restrict__ fac,
   for (int c = 0; c < TC; ++c) F[2 * QQ + tile_at(p, c, TC)] = -mrow[c];
 }
 
+// omega[pc][node] = the five cross-pair Psi blocks in the order the chain tiles use them
+// (same as gq_fast.cu k_build_rows, for sizes without the fast-path operator rows)
+template <int NS>
+__global__ void k_build_omega(Geo g, int npc, const double* __restrict__ psi,
+                              double* __restrict__ omega) {
+  constexpr int B2 = NS * NS;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)npc * g.nk) return;
+  const int j = (int)((idx % g.nk) / g.K);
+  const double* P = psi + idx * 13 * B2;
+  const int ev[5] = {7, 9, 3, 11, 8};
+  const int od[5] = {7, 10, 4, 12, 8};
+  double* W = omega + idx * 5 * B2;
+  for (int u = 0; u < 5; ++u) {
+    const int o = (j & 1) ? od[u] : ev[u];
+    for (int e = 0; e < B2; ++e) W[u * B2 + e] = P[o * B2 + e];
+  }
+}
+
+cudaError_t launch_build_omega(const Geo& g, int npc, const double* psi, double* omega,
+                               cudaStream_t s) {
+  const long long n = (long long)npc * g.nk;
+  if (g.n != 8) return cudaErrorInvalidValue;
+  k_build_omega<8><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(g, npc, psi, omega);
+  return cudaGetLastError();
+}
+
 // ---- host side -----------------------------------------------------------------------------
 
 static int env_or(const char* name, int dflt) {
@@ -825,16 +880,16 @@ static int env_or(const char* name, int dflt) {
 }
 
 bool chain_supported(int n) {
-  return (n == 2 || n == 4) && env_or("GQ_NO_CHAIN", 0) == 0;
+  return (n == 2 || n == 4 || n == 8) && env_or("GQ_NO_CHAIN", 0) == 0;
 }
 
 size_t chain_ff_doubles(const Geo& g, int npc) {
-  return g.n == 2 ? (size_t)npc * g.V * g.nb * Ch<2, true>::FFS
-                  : (size_t)npc * g.V * g.nb * Ch<4, true>::FFS;
+  const size_t blocks = (size_t)npc * g.V * g.nb;
+  return blocks * (g.n == 2 ? Ch<2, true>::FFS : g.n == 4 ? Ch<4, true>::FFS : Ch<8, true>::FFS);
 }
 size_t chain_fb_doubles(const Geo& g, int npc) {
-  return g.n == 2 ? (size_t)npc * g.V * g.nb * Ch<2, true>::FB
-                  : (size_t)npc * g.V * g.nb * Ch<4, true>::FB;
+  const size_t blocks = (size_t)npc * g.V * g.nb;
+  return blocks * (g.n == 2 ? Ch<2, true>::FB : g.n == 4 ? Ch<4, true>::FB : Ch<8, true>::FB);
 }
 
 cudaError_t launch_build_chain(const Geo& g, int npc, const double* fac, const double* omega,
@@ -845,6 +900,8 @@ cudaError_t launch_build_chain(const Geo& g, int npc, const double* fac, const d
     k_build_chain<2><<<blocks, 128, 0, s>>>(g, npc, fac, omega, ff, fb);
   else if (g.n == 4)
     k_build_chain<4><<<blocks, 128, 0, s>>>(g, npc, fac, omega, ff, fb);
+  else if (g.n == 8)
+    k_build_chain<8><<<blocks, 128, 0, s>>>(g, npc, fac, omega, ff, fb);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();
@@ -866,8 +923,10 @@ static cudaError_t chain_launch(const Geo& g, const ChainOps& co, const double* 
                           env_or("GQ_CHAIN_WARPS", 0));
   if (want > 0) cap = std::min(cap, want);
   const int blocks = std::max(1, std::min(n_items, cap * sm_count));
+  const int smc = env_or("GQ_CHAIN8_GROUP", 1) ? sm_count : 0;   // n = 8 item grouping
   k_chain<NS, INNER, P, MT, TF><<<blocks, 32, smem, s>>>(g, co, rhs, th, out, rdot, n_items,
-                                                      partials, st, dotmode);
+                                                      partials, st, dotmode, nullptr, nullptr,
+                                                      smc);
   return cudaGetLastError();
 }
 
@@ -917,6 +976,15 @@ cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const dou
   if (g.n == 4)
     return inner ? chain_mt<4, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
                  : chain_mt<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  if (g.n == 8) {
+    // P = 2 (10 KB inner / 5 KB outer record slots; factor tiles are not staged)
+    const int p = env_or("GQ_CHAIN8_P", 2);
+    if (inner)
+      return p == 3 ? chain_launch<8, true, 3, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                    : chain_launch<8, true, 2, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    return p == 3 ? chain_launch<8, false, 3, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                  : chain_launch<8, false, 2, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  }
   return cudaErrorInvalidValue;
 }
 
@@ -934,7 +1002,7 @@ static cudaError_t chain_fr_launch(const Geo& g, const ChainOps& co, double* r, 
   if (e != cudaSuccess) return e;
   const int blocks = std::max(1, std::min(n_items, per_sm * sm_count));
   k_chain<NS, false, P, 1, false, true><<<blocks, 32, smem, s>>>(
-      g, co, r, nullptr, out, nullptr, n_items, partials, st, kDotNone, y, r);
+      g, co, r, nullptr, out, nullptr, n_items, partials, st, kDotNone, y, r, sm_count);
   return cudaGetLastError();
 }
 
@@ -946,6 +1014,7 @@ cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const d
                ? chain_fr_launch<2, 4>(g, co, r, y, out, sm_count, partials, st, s)
                : chain_fr_launch<2, 7>(g, co, r, y, out, sm_count, partials, st, s);
   if (g.n == 4) return chain_fr_launch<4, 3>(g, co, r, y, out, sm_count, partials, st, s);
+  if (g.n == 8) return chain_fr_launch<8, 3>(g, co, r, y, out, sm_count, partials, st, s);
   return cudaErrorInvalidValue;
 }
 

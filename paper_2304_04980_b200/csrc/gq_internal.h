@@ -120,6 +120,9 @@ cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const dou
                          const double* th, double* out, const double* rdot, int sm_count,
                          double* partials, PcgState* st, int dotmode, cudaStream_t s);
 long long chain_max_blocks(const Geo& g, int nseg, int sm_count);
+// cross-pair Psi blocks for the chain tiles when the fast-path operator rows are not built (n = 8)
+cudaError_t launch_build_omega(const Geo& g, int npc, const double* psi, double* omega,
+                               cudaStream_t s);
 // outer sweep with the PCG residual update fused in (r -= alpha y, max|r|, history)
 cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const double* y,
                             double* out, int sm_count, double* partials, PcgState* st,
@@ -174,6 +177,15 @@ cudaError_t launch_build_dfac(const Geo& g, const double* A, const double* C, co
 cudaError_t launch_dfac(const Geo& g, const double* ops, const double* x, double* y,
                         double* partials, PcgState* st, int dotmode, int sm_count, cudaStream_t s);
 long long dfac_max_blocks(int sm_count);
+
+// ---- n = 8 block stencils on DMMA (gq_st8.cu) ----
+bool st8_supported(const Geo& g, int nxc);
+// modes kDelta (y = Delta x, optional curvature) and kOuterRhs (y = rin + Xi~ x); seg = the
+// class-pure stage chunks of the chain sweeps
+cudaError_t launch_st8(const Geo& g, const Ops& op, const int4* seg, int nseg, int mode,
+                       const double* x, const double* rin, double* y, int sm_count,
+                       double* partials, PcgState* st, int dotmode, cudaStream_t s);
+long long st8_max_blocks(int sm_count);
 
 // ---- lean n = 2 grid stencils (gq_grid.cu) ----
 struct GridShape {

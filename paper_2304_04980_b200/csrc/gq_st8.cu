@@ -1,0 +1,185 @@
+// Block stencils for n = 8 on the fp64 tensor cores ("st8" kernels).
+//
+// Same operators as the generic stencils of gq_stencil.cu (kkt_assembly.py:379-425):
+//   Delta:      (Delta x)_t = Psi_t x_t + Xi_{t-1} x_{t-1} + Xi_t' x_{t+1}
+//   outer rhs:  y_t = r_t - (Xi_{t-1} x_{t-1} + Xi_t' x_{t+1})        (r + Xi~ x)
+// At n = 8 every block is 8 x 8, i.e. exactly one m8n8k4 fp64 DMMA pair with the 8 stages of
+// a class-pure stage chunk on M: D[stage][out] += x_nbr[stage][feat] * B[feat][out] with
+// B[f][o] = block[o][f].  With features interleaved across the two k-steps (lane quad qd
+// holds features 2qd and 2qd+1), the A fragment is ONE 16-byte load of the neighbour's
+// record (stage-inner layout), the B fragment ONE 16-byte load of the row-major block and
+// the D fragment the lane's 16 bytes of the output record -- no staging, no shuffles.
+// A warp owns one node and walks its stage chunks (the chain kernel's class-pure segments);
+// the node's operator blocks stay in L1 across chunks.  23 (Delta) or 10 (outer rhs) blocks
+// are spread over 8 independent accumulators to keep the DMMA dependency chains short.
+#include <algorithm>
+#include <cstdlib>
+
+#include "gq_async.cuh"
+#include "gq_internal.h"
+
+namespace gq {
+
+namespace {
+using namespace as;
+__device__ __forceinline__ double2 ld16(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+}  // namespace
+
+template <int MODE>
+__global__ void __launch_bounds__(32) k_st8(Geo g, Ops op, const int4* __restrict__ seg,
+                                            int nseg, const double* __restrict__ x,
+                                            const double* __restrict__ rin,
+                                            double* __restrict__ y, double* partials,
+                                            PcgState* st, int dotmode) {
+  constexpr int NS = 8, B2 = 64;
+  if (st != nullptr) {
+    if (dotmode == kDotStep) {
+      const bool stop = st->done || st->step >= st->max_steps;
+      if (blockIdx.x == 0 && threadIdx.x == 0) st->skip = stop ? 1 : 0;
+      if (stop) return;
+    } else if (halted(st)) {
+      return;
+    }
+  }
+  const int lane = threadIdx.x, rw = lane >> 2, qd = lane & 3;
+  const long long rs = (long long)g.T1 * NS, cs = (long long)g.K * rs;
+  double dot = 0.0;
+#pragma unroll 1
+  for (long long node = blockIdx.x; node < g.nk; node += gridDim.x) {
+    const int j = (int)(node / g.K), i = (int)(node % g.K);
+    // neighbour record bases (stage 0) and validity for the 13-point diamond
+    const double* nb[13];
+    bool ok[13];
+#pragma unroll
+    for (int o = 0; o < 13; ++o) {
+      const int jj = j + odj(o), ii = i + odi(o);
+      ok[o] = jj >= 0 && jj < g.N && ii >= 0 && ii < g.K;
+      nb[o] = x + (ok[o] ? (long long)jj * cs + (long long)ii * rs : 0) + 2 * qd;
+    }
+    const double* xi = op.xi + (long long)node * 5 * B2 + rw * 8 + 2 * qd;    // nxc == 1
+    const double* xit = op.xit + (long long)node * 5 * B2 + rw * 8 + 2 * qd;
+#pragma unroll 1
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+      const int4 sg = seg[sgi];
+      const int t0 = sg.x, nvalid = sg.y, pc = sg.z;
+      const int t = t0 + rw;
+      const bool tv = rw < nvalid;
+      double2 acc[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) acc[a] = make_double2(0.0, 0.0);
+      double2 xself = make_double2(0.0, 0.0);
+      if (MODE == kDelta) {
+        const double* P = op.psi + ((long long)pc * g.nk + node) * 13 * B2 + rw * 8 + 2 * qd;
+#pragma unroll
+        for (int o = 0; o < 13; ++o) {
+          const double2 a = (ok[o] && tv) ? ld16(nb[o] + (long long)t * NS) : make_double2(0.0, 0.0);
+          if (o == 0) xself = a;
+          const double2 b = ld16(P + o * B2);
+          dmma(acc[o & 7], a.x, b.x);
+          dmma(acc[o & 7], a.y, b.y);
+        }
+      } else {
+        xself = make_double2(0.0, 0.0);
+      }
+      // Xi_{t-1} x_{t-1} (t >= 1) and Xi_t' x_{t+1} (t + 1 <= T): 5-point neighbours
+      const bool tm = tv && t >= 1, tp = tv && t + 1 < g.T1;
+      double2 e[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        const double2 am = (ok[u] && tm) ? ld16(nb[u] + (long long)(t - 1) * NS) : make_double2(0.0, 0.0);
+        const double2 ap = (ok[u] && tp) ? ld16(nb[u] + (long long)(t + 1) * NS) : make_double2(0.0, 0.0);
+        const double2 bm = ld16(xi + u * B2), bp = ld16(xit + u * B2);
+        double2& am_acc = MODE == kDelta ? acc[(u + 5) & 7] : e[0];
+        double2& ap_acc = MODE == kDelta ? acc[(u + 2) & 7] : e[1];
+        dmma(am_acc, am.x, bm.x);
+        dmma(am_acc, am.y, bm.y);
+        dmma(ap_acc, ap.x, bp.x);
+        dmma(ap_acc, ap.y, bp.y);
+      }
+      double2 out;
+      if (MODE == kDelta) {
+        out = add2(add2(add2(acc[0], acc[1]), add2(acc[2], acc[3])),
+                   add2(add2(acc[4], acc[5]), add2(acc[6], acc[7])));
+      } else {   // y = r + (-(Xi_{t-1} x_{t-1}) - Xi_t' x_{t+1})   (gq_grid.cu convention)
+        const double2 rv = tv ? ld16(rin + (long long)j * cs + (long long)i * rs + (long long)t * NS + 2 * qd)
+                              : make_double2(0.0, 0.0);
+        out.x = rv.x + ((0.0 - e[0].x) - e[1].x);
+        out.y = rv.y + ((0.0 - e[0].y) - e[1].y);
+      }
+      if (tv) {
+        *reinterpret_cast<double2*>(y + (long long)j * cs + (long long)i * rs + (long long)t * NS + 2 * qd) = out;
+        if (MODE == kDelta && dotmode != kDotNone) {
+          dot = fma(out.x, xself.x, dot);
+          dot = fma(out.y, xself.y, dot);
+        }
+      }
+    }
+  }
+  if (MODE == kDelta && dotmode != kDotNone) {
+    double c;
+    // one-warp CTAs: warp sum + last-block pass over the per-CTA partials (fixed order)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    int last = 0;
+    if (lane == 0) {
+      partials[blockIdx.x] = dot;
+      __threadfence();
+      last = atomicAdd(&st->counter[0], 1u) == gridDim.x - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence();
+      double acc = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + b);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      c = acc;
+      if (lane == 0) {
+        st->counter[0] = 0u;
+        st->curv = c;                        // pcg.py:101-108
+        if (c <= 0.0) {
+          st->breakdown = 1;
+          st->done = 1;
+        } else {
+          st->alpha = st->mu / c;
+        }
+      }
+    }
+  }
+}
+
+static int s8env(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return (s && *s) ? atoi(s) : dflt;
+}
+
+bool st8_supported(const Geo& g, int nxc) {
+  return g.n == 8 && nxc == 1 && s8env("GQ_NO_ST8", 0) == 0;
+}
+
+template <int MODE>
+static cudaError_t st8_launch(const Geo& g, const Ops& op, const int4* seg, int nseg,
+                              const double* x, const double* rin, double* y, int sm_count,
+                              double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  static int cache[64] = {0};
+  int per_sm = 1;
+  cudaError_t e = kernel_occupancy(k_st8<MODE>, 32, 0, cache, per_sm);
+  if (e != cudaSuccess) return e;
+  const long long blocks = std::min<long long>(g.nk, (long long)per_sm * sm_count);
+  k_st8<MODE><<<(unsigned)blocks, 32, 0, s>>>(g, op, seg, nseg, x, rin, y, partials, st, dotmode);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_st8(const Geo& g, const Ops& op, const int4* seg, int nseg, int mode,
+                       const double* x, const double* rin, double* y, int sm_count,
+                       double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  if (mode == kDelta)
+    return st8_launch<kDelta>(g, op, seg, nseg, x, rin, y, sm_count, partials, st, dotmode, s);
+  return st8_launch<kOuterRhs>(g, op, seg, nseg, x, rin, y, sm_count, partials, st, kDotNone, s);
+}
+
+long long st8_max_blocks(int sm_count) { return 64LL * sm_count; }
+
+}  // namespace gq
