@@ -68,6 +68,8 @@ struct gq_ctx {
   bool grid = false;           // lean n = 2 grid stencils
   bool dfac = false;           // factored Delta apply (time-invariant n = 2)
   bool st8 = false;            // n = 8 DMMA block stencils
+  bool st2 = false;            // n = 2 DMMA block stencils over 2 x 2 groups (opt-in)
+  double* st2_tiles = nullptr;
   double* dfac_ops = nullptr;  // its per-node operator records
   GridShape gsh{};
   bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
@@ -112,7 +114,7 @@ static void release(gq_ctx* c) {
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
                   c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
                   c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->cgt, c->dfac_ops, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
+                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->cgt, c->dfac_ops, c->st2_tiles, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -437,6 +439,12 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   c->sh_delta = stencil_shape(g, kDelta, c->sm_count);
   c->grid = c->fast && grid_supported(g.n);
   if (c->grid) c->gsh = grid_shape(g, c->sm_count);
+  if (c->chain && st2_supported(g, c->nxc)) {
+    CKB(dalloc(&c->st2_tiles, st2_doubles(g, c->npc)));
+    CKB(launch_build_st2(g, c->npc, c->op, c->st2_tiles, c->stream));
+    CKB(cudaStreamSynchronize(c->stream));
+    c->st2 = true;
+  }
   if (dfac_supported(g, D.n_dyn, D.n_cost)) {
     CKB(dalloc(&c->dfac_ops, (size_t)g.nk * 48));
     CKB(launch_build_dfac(g, c->A, c->C, c->qinv, c->brb, c->dfac_ops, c->stream));
@@ -456,6 +464,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                              c->cta ? cta_max_blocks(g) : 0LL,
                              c->dfac ? dfac_max_blocks(c->sm_count) : 0LL,
                              c->st8 ? st8_max_blocks(c->sm_count) : 0LL,
+                             c->st2 ? st2_max_blocks(c->sm_count) : 0LL,
                              c->chain ? chain_fr_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->grid ? (long long)c->gsh.blocks : 0LL});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));
@@ -557,7 +566,10 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
   for (int s = 0; s < c->S; ++s) {
     if ((c->fast || c->chain) && s > 0) {
       // rhs_s = r + Xi~ delta_{s-1}, materialised once per outer sweep (nested_jacobi.py:119-121)
-      if (c->grid) {
+      if (c->st2) {
+        CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kOuterRhs, c->dl[(s - 1) % 2],
+                      rin, c->rs, c->sm_count, c->partials, st, kDotNone, c->stream));
+      } else if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->gsh,
                        c->partials, st, kDotNone, c->stream));
       } else if (c->fast) {
@@ -664,7 +676,11 @@ extern "C" int gq_nbjm_solve(gq_ctx* c, const double* rhs, double tol, int64_t m
     const double* rhs_s = c->r;
     const double* xi = nullptr;
     if (s > 0) {
-      if (c->grid) {
+      if (c->st2) {
+        CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kOuterRhs, delta, c->r, c->rs,
+                      c->sm_count, c->partials, nullptr, kDotNone, c->stream));
+        rhs_s = c->rs;
+      } else if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->gsh, c->partials,
                        nullptr, kDotNone, c->stream));
         rhs_s = c->rs;
@@ -714,7 +730,10 @@ extern "C" int gq_apply_delta(gq_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, x, c->tmp0);
   if (rc) return rc;
-  if (c->st8)
+  if (c->st2)
+    CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kDelta, c->tmp0, nullptr, c->y,
+                  c->sm_count, c->partials, nullptr, kDotNone, c->stream));
+  else if (c->st8)
     CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kDelta, c->tmp0, nullptr, c->y,
                   c->sm_count, c->partials, nullptr, kDotNone, c->stream));
   else if (c->dfac)
@@ -782,7 +801,10 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
   };
   int rc = mark();
   if (rc) return rc;
-  if (c->st8)
+  if (c->st2)
+    CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kDelta, c->d, nullptr, c->y,
+                  c->sm_count, c->partials, c->st, kDotStep, c->stream));
+  else if (c->st8)
     CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kDelta, c->d, nullptr, c->y, c->sm_count,
                   c->partials, c->st, kDotStep, c->stream));
   else if (c->dfac)

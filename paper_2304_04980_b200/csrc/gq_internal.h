@@ -178,6 +178,15 @@ cudaError_t launch_dfac(const Geo& g, const double* ops, const double* x, double
                         double* partials, PcgState* st, int dotmode, int sm_count, cudaStream_t s);
 long long dfac_max_blocks(int sm_count);
 
+// ---- n = 2 block stencils on DMMA over 2 x 2 node groups (gq_st2.cu) ----
+bool st2_supported(const Geo& g, int nxc);
+size_t st2_doubles(const Geo& g, int npc);
+cudaError_t launch_build_st2(const Geo& g, int npc, const Ops& op, double* tiles, cudaStream_t s);
+cudaError_t launch_st2(const Geo& g, const double* tiles, const int4* seg, int nseg, int mode,
+                       const double* x, const double* rin, double* y, int sm_count,
+                       double* partials, PcgState* st, int dotmode, cudaStream_t s);
+long long st2_max_blocks(int sm_count);
+
 // ---- n = 8 block stencils on DMMA (gq_st8.cu) ----
 bool st8_supported(const Geo& g, int nxc);
 // modes kDelta (y = Delta x, optional curvature) and kOuterRhs (y = rin + Xi~ x); seg = the

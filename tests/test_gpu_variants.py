@@ -30,6 +30,7 @@ VARIANTS = {
     "no_fuse_r": {"GQ_NO_FUSE_R": "1"},          # separate r update kernel
     "no_fuse": {"GQ_NO_FUSE_R": "1", "GQ_NO_FORK": "1"},
     "dfac": {"GQ_DFAC": "1"},                    # factored Delta apply (CTA, w shared in smem)
+    "st2": {"GQ_ST2": "1"},                      # n = 2 DMMA stencils over 2 x 2 node groups
     "dfac16": {"GQ_DFAC": "1", "GQ_DFAC_NW": "16"},
     "no_fork": {"GQ_NO_FORK": "1"},              # x update in line instead of on a branch
     "dd4": {"GQ_DD": "1"},                       # domain-decomposed chain solve, 4 segments
