@@ -331,6 +331,35 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
           }
         }
     }
+    // n = 8 inner sweeps: z = tau - Psi_cross theta first (20 raw 8x8 cross-pair blocks,
+    // 40 DMMAs), then w = L^-1 z - G w_prev -- instead of the precomputed L^-1 Omega~ tiles
+    // (96 DMMAs); B traffic per block 26 KB instead of 40 KB
+    constexpr bool ZF = C::BG && INNER;
+    if constexpr (ZF) {
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const int dr = p >> 1, dc = p & 1, row = 2 * k + dr, col = a + dc;
+        if (col < g.N && row < K) {
+          const double* om =
+              co.omega + (((long long)cls * g.nk + (long long)col * K + row) * 5) * 64 + rw * 8 + 2 * qd;
+          double2 s0 = make_double2(0.0, 0.0), s1 = s0;
+#pragma unroll
+          for (int u = 0; u < 5; ++u) {
+            const double2 tq = lds2(sl + aofs(4 + th_rec(dc, u) + dr, 0, 2 * qd));
+            const double2 b = __ldg(reinterpret_cast<const double2*>(om + u * 64));
+            if (u & 1) {
+              dmma(s1, tq.x, b.x);
+              dmma(s1, tq.y, b.y);
+            } else {
+              dmma(s0, tq.x, b.x);
+              dmma(s0, tq.y, b.y);
+            }
+          }
+          tv[0][p].x = tv[0][p].x - (s0.x + s1.x);
+          tv[0][p].y = tv[0][p].y - (s0.y + s1.y);
+        }
+      }
+    }
     double2 wn[MT][NT];
 #pragma unroll
     for (int h = 0; h < NT; ++h) {
@@ -347,7 +376,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
           dmma(a1[m], tv[m][p].y, b.y);
         }
       }
-      if (INNER) {
+      if (INNER && !ZF) {
 #pragma unroll
         for (int p = 0; p < KT; ++p) {
           const double2 b = ldb(sf + 2 * QQ + (h * KT + p) * 64 + rw * 8 + 2 * qd);
@@ -376,7 +405,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         double2 sm = add2(a0[m], a1[m]);
-        if (INNER) sm = add2(sm, add2(add2(m0[m], m1[m]), add2(m2[m], m3[m])));
+        if (INNER && !ZF) sm = add2(sm, add2(add2(m0[m], m1[m]), add2(m2[m], m3[m])));
         wn[m][h] = add2(sm, add2(g0[m], g1[m]));
       }
     }

@@ -110,6 +110,7 @@ struct ChainOps {
   int nseg;
   const int4* seg16;   // [nseg16] the same with chunks of <= 16 stages (two M-tiles per warp)
   int nseg16;
+  const double* omega = nullptr;   // [npc][N][K][5][n][n] cross-pair Psi blocks (n = 8 inner)
 };
 bool chain_supported(int n);
 size_t chain_ff_doubles(const Geo& g, int npc);
