@@ -105,7 +105,7 @@ __device__ bool warp_grid_max(double v, double* partials, unsigned int* counter,
 
 }  // namespace
 
-template <int NS, bool INNER, int MT = 1, bool FR = false>
+template <int NS, bool INNER, int MT = 1, bool FR = false, bool BGX = false>
 struct Ch {
   static constexpr int Q = 4 * NS, QQ = Q * Q, NT = Q / 8;
   static constexpr int TC = 12 * NS;                  // theta feature count
@@ -125,7 +125,7 @@ struct Ch {
   // n = 8: the factor tiles of a block (40 KB inner) are not staged; B fragments are read
   // straight from global memory (L1-cached, shared by the warps of an SM that work on the
   // same pair, see k_chain's item mapping)
-  static constexpr bool BG = NS == 8;
+  static constexpr bool BG = NS == 8 || BGX;
   static constexpr int FFST = BG ? 0 : FF, FBST = BG ? 0 : FB;   // staged factor doubles
   // record stride in shared memory: padded by 16*NS bytes so the A-fragment reads of a
   // quarter warp (4 records x 2 chains) hit 8 distinct 16-byte bank groups
@@ -139,7 +139,7 @@ struct Ch {
 
 using namespace as;
 
-template <int NS, bool INNER, int P, int MT, bool TF = false, bool FR = false>
+template <int NS, bool INNER, int P, int MT, bool TF = false, bool FR = false, bool BGX = false>
 __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            const double* __restrict__ rhs,
                                            const double* __restrict__ th, double* out,
@@ -155,7 +155,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
                                            double* rmax = nullptr) {
   // TF: the factor block of each chain block arrives by one bulk (TMA) copy issued by lane 0
   // and completes on the slot's mbarrier; records stay on per-lane LDGSTS
-  using C = Ch<NS, INNER, MT, FR>;
+  using C = Ch<NS, INNER, MT, FR, BGX>;
   constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, REC = C::RSTR, R = P + 1;
   // B fragment: staged tile in shared memory, or (n = 8) the tile in global memory
   auto ldb = [](const double* p) -> double2 {
@@ -334,7 +334,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
     // n = 8 inner sweeps: z = tau - Psi_cross theta first (20 raw 8x8 cross-pair blocks,
     // 40 DMMAs), then w = L^-1 z - G w_prev -- instead of the precomputed L^-1 Omega~ tiles
     // (96 DMMAs); B traffic per block 26 KB instead of 40 KB
-    constexpr bool ZF = C::BG && INNER;
+    constexpr bool ZF = NS == 8 && INNER;
     if constexpr (ZF) {
 #pragma unroll
       for (int p = 0; p < NT; ++p) {
@@ -576,7 +576,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
   __syncwarp();
 }
 
-template <int NS, bool INNER, int P, int MT, bool TF, bool FR = false>
+template <int NS, bool INNER, int P, int MT, bool TF, bool FR = false, bool BGX = false>
 __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* __restrict__ rhs,
                                               const double* __restrict__ th, double* out,
                                               const double* __restrict__ rdot, int n_items,
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
   const int nseg = MT == 1 ? co.nseg : co.nseg16;
   const int4* seg = MT == 1 ? co.seg : co.seg16;
   double dot = 0.0;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (P + 1) * Ch<NS, INNER, MT, FR>::SLOT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (P + 1) * Ch<NS, INNER, MT, FR, BGX>::SLOT);
   uint32_t phase = 0;
   if constexpr (TF) {
     if (threadIdx.x == 0)
@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
   // SM (blocks b = s, s + smc, s + 2 smc, ... when the grid is per_sm x smc) take consecutive
   // stage chunks of the same pair.  A different block-to-SM placement only costs L1 hits.
   const int G = gridDim.x;
-  const bool grouped = Ch<NS, INNER, MT, FR>::BG && smc > 0 && G % smc == 0;
+  const bool grouped = Ch<NS, INNER, MT, FR, BGX>::BG && smc > 0 && G % smc == 0;
   const int per = grouped ? G / smc : 1;
   // round r covers units [r G, r G + G): a permutation of the blocks in every round, so a
   // partial last round skips exactly the units past n_items
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
     if (u >= n_items) continue;
     const int v = u / nseg;
     const int4 sg = seg[u - v * nseg];
-    chain_item<NS, INNER, P, MT, TF, FR>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x,
+    chain_item<NS, INNER, P, MT, TF, FR, BGX>(g, co, rhs, th, out, rdot, dotting, ring, v, sg.x,
                                          sg.y, sg.z, pol_s, pol_k, dot, 0, g.nb, co.ff, co.fb,
                                          nullptr, bars, &phase, yv, rupd, alpha, &rmax);
   }
@@ -936,16 +936,16 @@ cudaError_t launch_build_chain(const Geo& g, int npc, const double* fac, const d
   return cudaGetLastError();
 }
 
-template <int NS, bool INNER, int P, int MT, bool TF = false>
+template <int NS, bool INNER, int P, int MT, bool TF = false, bool BGX = false>
 static cudaError_t chain_launch(const Geo& g, const ChainOps& co, const double* rhs,
                                 const double* th, double* out, const double* rdot, int sm_count,
                                 double* partials, PcgState* st, int dotmode, cudaStream_t s) {
   constexpr size_t smem =
-      (size_t)(P + 1) * Ch<NS, INNER, MT>::SLOT * sizeof(double) + (TF ? (P + 1) * 8 : 0);
+      (size_t)(P + 1) * Ch<NS, INNER, MT, false, BGX>::SLOT * sizeof(double) + (TF ? (P + 1) * 8 : 0);
   const int n_items = g.V * (MT == 1 ? co.nseg : co.nseg16);
   static int cache[64] = {0};
   int per_sm = 1;
-  cudaError_t e = kernel_occupancy(k_chain<NS, INNER, P, MT, TF>, 32, smem, cache, per_sm);
+  cudaError_t e = kernel_occupancy(k_chain<NS, INNER, P, MT, TF, false, BGX>, 32, smem, cache, per_sm);
   if (e != cudaSuccess) return e;
   int cap = per_sm;
   const int want = env_or(INNER ? "GQ_CHAIN_WARPS_INNER" : "GQ_CHAIN_WARPS_OUTER",
@@ -953,7 +953,7 @@ static cudaError_t chain_launch(const Geo& g, const ChainOps& co, const double* 
   if (want > 0) cap = std::min(cap, want);
   const int blocks = std::max(1, std::min(n_items, cap * sm_count));
   const int smc = env_or("GQ_CHAIN8_GROUP", 1) ? sm_count : 0;   // n = 8 item grouping
-  k_chain<NS, INNER, P, MT, TF><<<blocks, 32, smem, s>>>(g, co, rhs, th, out, rdot, n_items,
+  k_chain<NS, INNER, P, MT, TF, false, BGX><<<blocks, 32, smem, s>>>(g, co, rhs, th, out, rdot, n_items,
                                                       partials, st, dotmode, nullptr, nullptr,
                                                       smc);
   return cudaGetLastError();
@@ -973,6 +973,13 @@ static cudaError_t chain_p(const Geo& g, const ChainOps& co, const double* rhs, 
       if (pd == 5)
         return chain_launch<NS, INNER, 5, MT, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
       return chain_launch<NS, INNER, 3, MT, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    }
+  }
+  if constexpr (NS == 2 && MT == 1) {
+    if (env_or("GQ_CHAIN_BG", 0) == 1) {   // B fragments from global (experiment)
+      if (pd == 7) return chain_launch<NS, INNER, 7, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+      if (pd == 4) return chain_launch<NS, INNER, 4, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+      return chain_launch<NS, INNER, 3, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
     }
   }
   switch (pd) {
