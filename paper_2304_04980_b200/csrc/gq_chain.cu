@@ -1014,10 +1014,16 @@ cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const dou
                  : chain_mt<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 8) {
     // P = 2 (10 KB inner / 5 KB outer record slots; factor tiles are not staged)
-    const int p = env_or("GQ_CHAIN8_P", 2);
-    if (inner)
+    // measured on config 5 (tools/c5time.py): inner P = 1 (smaller rings leave more of the
+    // SM's L1 to the factor tiles: 4.1 -> 3.55 ms), outer P = 2 (2.36 vs 2.6 ms at P = 1)
+    const int p = env_or(inner ? "GQ_CHAIN8_P_INNER" : "GQ_CHAIN8_P_OUTER",
+                         env_or("GQ_CHAIN8_P", inner ? 1 : 2));
+    if (inner) {
+      if (p == 1) return chain_launch<8, true, 1, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
       return p == 3 ? chain_launch<8, true, 3, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
                     : chain_launch<8, true, 2, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    }
+    if (p == 1) return chain_launch<8, false, 1, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
     return p == 3 ? chain_launch<8, false, 3, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
                   : chain_launch<8, false, 2, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   }
