@@ -231,3 +231,27 @@ def test_nbjm_budget_and_device_vectors():
     with pytest.raises(MaxIterationsExceeded) as info2:
         pc.solve(ga.offset, tol=1e-30, max_outer=4)
     assert rel_err(info.value.iterate.cpu().numpy(), info2.value.iterate) < 1e-15
+
+
+@pytest.mark.parametrize("case", ["n8", "n4", "n1_oddk"])
+def test_nbjm_vs_oracle_other_block_sizes(case):
+    """Standalone nested Jacobi on the n = 8 (DMMA chain + k_st8), n = 4 and n = 1 paths
+    against the oracle restatement (outer-sweep count and solution)."""
+    from oracle.gridlq_oracle import Oracle
+    from paper_2304_04980_b200 import (GpuNestedJacobiPreconditioner, GpuSchurOperator,
+                                       generators)
+
+    if case == "n8":
+        ga = generators.config5(0, K=4, N=6, T=3)
+    elif case == "n4":
+        ga = generators.config3(0, K=4, N=4, T=4)
+    else:
+        ga = generators.random_case(5, 3, 4, 1, 1, seed=5)
+    op = GpuSchurOperator(ga, 2, 1)
+    pc = GpuNestedJacobiPreconditioner(op, 2, 1)
+    tol = 1e-9 * float(np.max(np.abs(ga.offset)))
+    xo, no, conv = Oracle(ga, 2, 1).nbjm_solve(ga.offset, tol=tol, max_outer=3000)
+    assert conv
+    x, n = pc.solve(ga.offset, tol=tol, max_outer=3000)
+    assert n == no
+    assert rel_err(x, xo) < 1e-9
