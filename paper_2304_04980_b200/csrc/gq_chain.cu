@@ -977,6 +977,8 @@ static cudaError_t chain_p(const Geo& g, const ChainOps& co, const double* rhs, 
   }
   if constexpr (NS == 2 && MT == 1) {
     if (env_or("GQ_CHAIN_BG", 0) == 1) {   // B fragments from global (experiment)
+      if (pd == 1) return chain_launch<NS, INNER, 1, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+      if (pd == 2) return chain_launch<NS, INNER, 2, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
       if (pd == 7) return chain_launch<NS, INNER, 7, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
       if (pd == 4) return chain_launch<NS, INNER, 4, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
       return chain_launch<NS, INNER, 3, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
