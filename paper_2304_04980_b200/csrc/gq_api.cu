@@ -419,11 +419,22 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
     CKB(launch_build_omega(g, c->npc, c->psi, c->omega, c->stream));
     CKB(dalloc(&c->cff, chain_ff_doubles(g, c->npc)));
     CKB(dalloc(&c->cfb, chain_fb_doubles(g, c->npc)));
-    CKB(dalloc(&c->seg, s8.size()));
+    // CTA items of the n = 8 CTA-shared kernel: runs of one class, <= 8 segments each
+    std::vector<int4> grp;
+    for (size_t i = 0; i < s8.size();) {
+      size_t e = i + 1;
+      while (e < s8.size() && e - i < 8 && s8[e].z == s8[i].z) ++e;
+      grp.push_back(make_int4((int)i, (int)(e - i), s8[i].z, 0));
+      i = e;
+    }
+    CKB(dalloc(&c->seg, s8.size() + grp.size()));
     CKB(cudaMemcpy(c->seg, s8.data(), s8.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CKB(cudaMemcpy(c->seg + s8.size(), grp.data(), grp.size() * sizeof(int4),
+                   cudaMemcpyHostToDevice));
     CKB(launch_build_chain(g, c->npc, c->fac, c->omega, c->cff, c->cfb, c->stream));
     CKB(cudaStreamSynchronize(c->stream));
-    c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg, (int)s8.size(), c->omega};
+    c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg, (int)s8.size(), c->omega,
+                     c->seg + s8.size(), (int)grp.size()};
     c->chain = true;
     c->st8 = st8_supported(g, c->nxc);
   }
@@ -466,6 +477,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                              c->dfac ? dfac_max_blocks(c->sm_count) : 0LL,
                              c->st8 ? st8_max_blocks(c->sm_count) : 0LL,
                              c->st2 ? st2_max_blocks(c->sm_count) : 0LL,
+                             c->chain ? (long long)c->sm_count * 2 : 0LL,
                              c->chain ? chain_fr_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->grid ? (long long)c->gsh.blocks : 0LL});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));

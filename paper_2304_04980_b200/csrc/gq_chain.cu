@@ -1014,6 +1014,8 @@ cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const dou
   if (g.n == 4)
     return inner ? chain_mt<4, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
                  : chain_mt<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  if (g.n == 8 && co.grp != nullptr && chain8c_enabled())
+    return launch_chain8c(g, co, inner, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 8) {
     // P = 2 (10 KB inner / 5 KB outer record slots; factor tiles are not staged)
     // measured on config 5 (tools/c5time.py): inner P = 1 (smaller rings leave more of the

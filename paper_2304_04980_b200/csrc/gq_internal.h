@@ -111,7 +111,14 @@ struct ChainOps {
   const int4* seg16;   // [nseg16] the same with chunks of <= 16 stages (two M-tiles per warp)
   int nseg16;
   const double* omega = nullptr;   // [npc][N][K][5][n][n] cross-pair Psi blocks (n = 8 inner)
+  const int4* grp = nullptr;       // n = 8 CTA items: (first seg, segs <= 8, class, 0)
+  int ngrp = 0;
 };
+// n = 8 pair-chain sweeps with CTA-shared factor tiles (gq_chain8c.cu)
+bool chain8c_enabled();
+cudaError_t launch_chain8c(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
+                           const double* th, double* out, const double* rdot, int sm_count,
+                           double* partials, PcgState* st, int dotmode, cudaStream_t s);
 bool chain_supported(int n);
 size_t chain_ff_doubles(const Geo& g, int npc);
 size_t chain_fb_doubles(const Geo& g, int npc);
