@@ -371,16 +371,38 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
         return segs;
       };
       const std::vector<int4> s8 = chunks(8), s16 = chunks(16);
+      // n = 2 CTA-shared sweeps (opt-in): groups of <= 5 class-1 segments; stage 0 apart
+      std::vector<int4> grp;
+      bool two_class = g.n == 2 && g.T1 >= 2 && pcls[0] != pcls[1];
+      for (int t = 2; t < g.T1 && two_class; ++t) two_class = pcls[t] == pcls[1];
+      if (two_class)
+        for (size_t i = 1; i < s8.size();) {
+          const size_t e = std::min(s8.size(), i + 5);
+          grp.push_back(make_int4((int)i, (int)(e - i), s8[i].z, 0));
+          i = e;
+        }
       CKB(dalloc(&c->cff, chain_ff_doubles(g, c->npc)));
       CKB(dalloc(&c->cfb, chain_fb_doubles(g, c->npc)));
-      CKB(dalloc(&c->seg, s8.size() + s16.size()));
+      CKB(dalloc(&c->seg, s8.size() + s16.size() + grp.size()));
       CKB(cudaMemcpy(c->seg, s8.data(), s8.size() * sizeof(int4), cudaMemcpyHostToDevice));
       CKB(cudaMemcpy(c->seg + s8.size(), s16.data(), s16.size() * sizeof(int4),
                      cudaMemcpyHostToDevice));
+      if (!grp.empty())
+        CKB(cudaMemcpy(c->seg + s8.size() + s16.size(), grp.data(), grp.size() * sizeof(int4),
+                       cudaMemcpyHostToDevice));
       CKB(launch_build_chain(g, c->npc, c->fac, c->omega, c->cff, c->cfb, c->stream));
       CKB(cudaStreamSynchronize(c->stream));
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
+      if (!grp.empty()) {
+        bool ok0 = false;
+        CKB(cta_check_stage0(g, pcls[0], c->cff, c->cfb, ok0, c->stream));
+        if (ok0) {
+          c->co.grp = c->seg + s8.size() + s16.size();
+          c->co.ngrp = (int)grp.size();
+          c->co.c0 = pcls[0];
+        }
+      }
       c->chain = true;
       if (cta_supported(g, pcls.data())) {
         bool ok = false;

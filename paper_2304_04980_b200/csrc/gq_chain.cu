@@ -1008,6 +1008,8 @@ static cudaError_t chain_mt(const Geo& g, const ChainOps& co, const double* rhs,
 cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
                          const double* th, double* out, const double* rdot, int sm_count,
                          double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  if (g.n == 2 && co.grp != nullptr && chain2c_enabled())
+    return launch_chain2c(g, co, inner, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 2)
     return inner ? chain_mt<2, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
                  : chain_mt<2, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);

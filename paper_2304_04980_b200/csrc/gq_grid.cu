@@ -68,8 +68,8 @@ __device__ bool warp_grid_sum2(double v, double* partials, unsigned int* counter
   return true;
 }
 
-template <int MODE, int P, int MB = 1>
-__global__ void __launch_bounds__(32, MB) k_grid(Geo g, FastOps fo, const double* __restrict__ x,
+template <int MODE, int P>
+__global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __restrict__ x,
                                              const double* __restrict__ rin,
                                              double* __restrict__ y, int nchunk, int nstrip,
                                              int rows, int n_items, double* partials,
@@ -341,14 +341,14 @@ GridShape grid_shape(const Geo& g, int sm_count) {
   return sh;
 }
 
-template <int MODE, int P, int MB = 1>
+template <int MODE, int P>
 static cudaError_t grid_launch(const Geo& g, const FastOps& fo, const double* x, const double* rin,
                                double* y, const GridShape& ub, double* partials, PcgState* st,
                                int dotmode, cudaStream_t s) {
   constexpr size_t smem = (size_t)(P + 1) * Gd<MODE>::SLOT * sizeof(double);
   static int cache[64] = {0};
   int per_sm = 1;
-  cudaError_t e = kernel_occupancy(k_grid<MODE, P, MB>, 32, smem, cache, per_sm);
+  cudaError_t e = kernel_occupancy(k_grid<MODE, P>, 32, smem, cache, per_sm);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -372,7 +372,7 @@ static cudaError_t grid_launch(const Geo& g, const FastOps& fo, const double* x,
   const int nstrip = (g.K + rows - 1) / rows;
   const int n_items = (int)(cols * nstrip);
   const int blocks = (int)std::min<long long>({(long long)n_items, slots, (long long)ub.blocks});
-  k_grid<MODE, P, MB><<<blocks, 32, smem, s>>>(g, fo, x, rin, y, ub.nchunk, nstrip, rows, n_items,
+  k_grid<MODE, P><<<blocks, 32, smem, s>>>(g, fo, x, rin, y, ub.nchunk, nstrip, rows, n_items,
                                            partials, st, dotmode);
   return cudaGetLastError();
 }
@@ -381,14 +381,6 @@ cudaError_t launch_grid(const Geo& g, const FastOps& fo, int mode, const double*
                         const double* rin, double* y, const GridShape& sh, double* partials,
                         PcgState* st, int dotmode, cudaStream_t s) {
   const int p = genv("GQ_GRID_P", 2);
-  // register cap experiment: minimum resident blocks per SM for the Delta kernel
-  const int mb = genv("GQ_GRID_MINB", 1);
-  if (mode == kDelta && p == 2 && mb == 16)
-    return grid_launch<kDelta, 2, 16>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
-  if (mode == kDelta && p == 2 && mb == 20)
-    return grid_launch<kDelta, 2, 20>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
-  if (mode == kOuterRhs && p == 2 && mb == 16)
-    return grid_launch<kOuterRhs, 2, 16>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
   if (mode == kDelta) {
     if (p == 2) return grid_launch<kDelta, 2>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
     if (p == 4) return grid_launch<kDelta, 4>(g, fo, x, rin, y, sh, partials, st, dotmode, s);

@@ -111,9 +111,15 @@ struct ChainOps {
   const int4* seg16;   // [nseg16] the same with chunks of <= 16 stages (two M-tiles per warp)
   int nseg16;
   const double* omega = nullptr;   // [npc][N][K][5][n][n] cross-pair Psi blocks (n = 8 inner)
-  const int4* grp = nullptr;       // n = 8 CTA items: (first seg, segs <= 8, class, 0)
+  const int4* grp = nullptr;       // CTA items (n = 8: all classes; n = 2: class-1 runs)
   int ngrp = 0;
+  int c0 = -1;                     // n = 2 CTA sweeps: stage-0 class solved block-diagonally
 };
+// n = 2 pair-chain sweeps with CTA-shared factor tiles (gq_chain2c.cu, opt-in)
+bool chain2c_enabled();
+cudaError_t launch_chain2c(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
+                           const double* th, double* out, const double* rdot, int sm_count,
+                           double* partials, PcgState* st, int dotmode, cudaStream_t s);
 // n = 8 pair-chain sweeps with CTA-shared factor tiles (gq_chain8c.cu)
 bool chain8c_enabled();
 cudaError_t launch_chain8c(const Geo& g, const ChainOps& co, bool inner, const double* rhs,

@@ -26,6 +26,8 @@ VARIANTS = {
     "cta_r4": {"GQ_CTA": "1", "GQ_CTA_R_INNER": "4", "GQ_CTA_R_OUTER": "7"},
     "cta_persist": {"GQ_CTA": "1", "GQ_CTA_PERSIST": "1"},
     "cta_w1": {"GQ_CTA": "1", "GQ_CTA_W": "1"},                 # per-warp TMA pipeline
+    "chain2c": {"GQ_CHAIN2C": "1"},              # n = 2 sweeps with CTA-shared factor tiles
+    "chain2c_nofr": {"GQ_CHAIN2C": "1", "GQ_NO_FUSE_R": "1"},
     "fuse_x": {"GQ_FUSE_X": "1"},                # x update fused into the direction update
     "no_fuse_r": {"GQ_NO_FUSE_R": "1"},          # separate r update kernel
     "no_fuse": {"GQ_NO_FUSE_R": "1", "GQ_NO_FORK": "1"},
