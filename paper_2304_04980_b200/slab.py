@@ -1,0 +1,379 @@
+"""Stage-slab sharded PCGM.
+
+The reference solves the whole multiplier system in one process (``pcg.py:50-149``).  The
+path partitions naturally along the stage axis t:
+
+* Delta couples stage t only to t-1 and t+1 (``kkt_assembly.py:389-403``);
+* the pair-chain solves and Omega~ are stage-local (``nested_jacobi.py:65-103``);
+* Xi~ couples t to t +- 1 again (``kkt_assembly.py:414-425``);
+* PCG itself needs three scalar reductions per step (``pcg.py:100,112,128``).
+
+So each slab owns a contiguous stage range [lo, hi) and keeps one halo stage on each side
+that has a neighbour.  A slab is an ordinary problem of its own: the stage window
+[lo - 1, hi + 1) of the global data, with the global stage-class maps sliced to it.  Every
+row that the slab owns then sees exactly the global operator blocks (its Psi_t, Xi_{t-1},
+Xi_t and the pair factors of its class); only the halo rows differ, and those are never
+read.  Per PCG step the slabs exchange one stage of the direction d (before Delta d) and
+one stage of delta per extra outer sweep (before Xi~ delta): ``S`` halo exchanges of
+``K*N*n`` doubles per side, plus the three scalar reductions.
+
+Slabs map onto processes in contiguous blocks (one process per GPU, ``torch.distributed``
+over NCCL for the halos and scalars; gloo on CPU for the host-logic tests).  Several slabs
+may live in one process: their halos are device copies.  Scalar reductions sum per-slab
+partials in slab order, so a run is bitwise independent of the slab-to-process layout.
+
+The local compute of a slab goes through the C ABI on its own ``gq_ctx``
+(``gq_apply_delta``, ``gq_apply_outer_coupling``, ``gq_apply_precond`` with one outer
+sweep); the oracle can stand in for it only inside the tests.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import time
+
+import numpy as np
+
+from .counts import counters
+from .errors import BreakdownError, DimensionMismatchError, MaxIterationsExceeded
+from .problem import GridArrays, as_arrays
+from .solver import SolveReport, _op_counts
+
+
+def slab_bounds(T: int, slabs: int) -> list:
+    """Owned stage ranges [lo, hi) of ``slabs`` contiguous slabs over stages 0..T
+    (sizes differ by at most one, the larger ones first)."""
+    stages = T + 1
+    if slabs < 1 or slabs > stages:
+        raise ValueError(f"need 1 <= slabs <= T + 1 = {stages}, got {slabs}")
+    base, extra = divmod(stages, slabs)
+    out, lo = [], 0
+    for s in range(slabs):
+        hi = lo + base + (1 if s < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+@dataclasses.dataclass(frozen=True)
+class Slab:
+    """One slab: owned global stages [lo, hi), local window [a, b) = owned + halos."""
+
+    index: int
+    lo: int
+    hi: int
+    a: int
+    b: int
+    nh: int            # doubles per stage (K * N * n)
+
+    @property
+    def local_dim(self):
+        return (self.b - self.a) * self.nh
+
+    @property
+    def own(self):
+        """Owned part of a local vector (reference order: stages are contiguous)."""
+        return slice((self.lo - self.a) * self.nh, (self.hi - self.a) * self.nh)
+
+    @property
+    def global_own(self):
+        return slice(self.lo * self.nh, self.hi * self.nh)
+
+    def stage(self, t):
+        """Local slice of global stage t (t in [a, b))."""
+        o = (t - self.a) * self.nh
+        return slice(o, o + self.nh)
+
+
+def make_slabs(ga: GridArrays, slabs: int) -> list:
+    nh = ga.K * ga.N * ga.n
+    out = []
+    for s, (lo, hi) in enumerate(slab_bounds(ga.T, slabs)):
+        out.append(Slab(s, lo, hi, max(lo - 1, 0), min(hi + 1, ga.T + 1), nh))
+    return out
+
+
+def slab_arrays(ga: GridArrays, sl: Slab) -> GridArrays:
+    """The slab's window [a, b) as a problem of its own: same blocks, the global stage-class
+    maps sliced to the window (``dyn_class`` covers the transitions a..b-2)."""
+    return dataclasses.replace(
+        ga, T=sl.b - sl.a - 1,
+        dyn_class=np.ascontiguousarray(ga.dyn_class[sl.a:sl.b - 1]),
+        cost_class=np.ascontiguousarray(ga.cost_class[sl.a:sl.b]),
+        offset=np.ascontiguousarray(ga.offset[sl.a * sl.nh:sl.b * sl.nh]))
+
+
+class DeviceSlabOps:
+    """Local compute of one slab on the B200: its own gq_ctx, one outer sweep per
+    preconditioner call (the outer loop runs in ``SlabPcg`` with halo exchanges)."""
+
+    def __init__(self, sub: GridArrays, inner_sweeps: int):
+        import torch
+
+        from . import _lib
+        from .solver import _Context
+
+        self.ctx = _Context(sub, inner_sweeps, 1)
+        # order the library's work after torch's on the same stream
+        stream = torch.cuda.current_stream()
+        _lib.check(self.ctx.lib.gq_set_stream(self.ctx.h, ctypes.c_void_p(stream.cuda_stream)))
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def delta(self, x):
+        return self.ctx.unary("gq_apply_delta", x)
+
+    def outer(self, x):
+        return self.ctx.unary("gq_apply_outer_coupling", x)
+
+    def inner(self, r):
+        return self.ctx.unary("gq_apply_precond", r)
+
+
+class SlabComm:
+    """Halo exchange and scalar reductions between the slabs of one partition.
+
+    ``owner[s]`` is the process rank holding slab s; this process holds the slabs with
+    ``owner[s] == rank``.  ``group`` is a torch.distributed process group (None: the
+    default group when initialised, else a single process)."""
+
+    def __init__(self, n_slabs: int, world: int = 1, rank: int = 0, group=None, device=None):
+        import torch
+
+        if n_slabs % world:
+            raise ValueError(f"{n_slabs} slabs do not divide over {world} processes")
+        per = n_slabs // world
+        self.owner = [s // per for s in range(n_slabs)]
+        self.rank, self.world, self.group = rank, world, group
+        self.local = [s for s in range(n_slabs) if self.owner[s] == rank]
+        self.n = n_slabs
+        self.device = device if device is not None else torch.device("cpu")
+        self.exchanges = 0
+
+    @classmethod
+    def from_env(cls, n_slabs: int, group=None, device=None):
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return cls(n_slabs, dist.get_world_size(group), dist.get_rank(group), group, device)
+        return cls(n_slabs, 1, 0, None, device)
+
+    def exchange(self, slabs, vecs):
+        """Fill every halo stage of ``vecs`` (slab -> local vector) from the neighbour's
+        owned boundary stage.  Reads touch owned stages only and writes halo stages only,
+        so the in-process copies need no ordering."""
+        import torch.distributed as dist
+
+        self.exchanges += 1
+        reqs = []
+        for s in self.local:
+            sl = slabs[s]
+            for nb, mine, theirs in ((s - 1, sl.lo - 1, sl.lo), (s + 1, sl.hi, sl.hi - 1)):
+                if nb < 0 or nb >= self.n:
+                    continue
+                halo = vecs[s][sl.stage(mine)]            # my halo = their boundary stage
+                if self.owner[nb] == self.rank:
+                    halo.copy_(vecs[nb][slabs[nb].stage(mine)])
+                else:
+                    peer = self.owner[nb]
+                    reqs.append(dist.isend(vecs[s][sl.stage(theirs)], peer, group=self.group))
+                    reqs.append(dist.irecv(halo, peer, group=self.group))
+        for r in reqs:
+            r.wait()
+
+    def _reduce(self, partials, op):
+        import torch
+        import torch.distributed as dist
+
+        if self.world == 1:
+            vals = [partials[s] for s in range(self.n)]
+        else:
+            buf = torch.zeros(self.n, dtype=torch.float64, device=self.device)
+            for s in self.local:
+                buf[s] = partials[s]
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)   # x + 0 is exact
+            vals = buf.tolist()
+        if op == "sum":
+            acc = 0.0
+            for v in vals:        # slab order: independent of the process layout
+                acc += v
+            return acc
+        return max(vals)
+
+    def sum(self, partials):
+        return self._reduce(partials, "sum")
+
+    def max(self, partials):
+        return self._reduce(partials, "max")
+
+    def gather(self, slabs, vecs, dim):
+        """The global vector (every process gets it): owned parts summed into zeros."""
+        import torch
+        import torch.distributed as dist
+
+        any_vec = vecs[self.local[0]]
+        out = torch.zeros(dim, dtype=any_vec.dtype, device=any_vec.device)
+        for s in self.local:
+            out[slabs[s].global_own] = vecs[s][slabs[s].own]
+        if self.world > 1:
+            dist.all_reduce(out, op=dist.ReduceOp.SUM, group=self.group)
+        return out
+
+
+class SlabPcg:
+    """PCGM over a stage-slab partition (``pcg.py:50-149`` control flow).
+
+    ``ops_factory(sub_arrays, inner_sweeps)`` builds a slab's local compute; the default is
+    ``DeviceSlabOps`` (the B200 path)."""
+
+    def __init__(self, problem, slabs=None, inner_sweeps=2, outer_sweeps=2, comm=None,
+                 ops_factory=None, precondition=True):
+        import torch
+
+        self.arrays = as_arrays(problem)
+        ga = self.arrays
+        if precondition and inner_sweeps % 2:
+            raise ValueError("preconditioner use requires an even inner budget "
+                             f"(got {inner_sweeps}); odd budgets are standalone-only")
+        if inner_sweeps < 1 or outer_sweeps < 1:
+            raise ValueError("sweep budgets must be at least 1")
+        if comm is None:
+            dev = torch.device("cuda", torch.cuda.current_device()) if ops_factory is None \
+                else torch.device("cpu")
+            if slabs is None:
+                import torch.distributed as dist
+
+                slabs = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+            comm = SlabComm.from_env(slabs, device=dev)
+        self.comm = comm
+        self.slabs = make_slabs(ga, comm.n)
+        self.L, self.S = int(inner_sweeps), int(outer_sweeps)
+        self.precondition = precondition
+        factory = ops_factory or DeviceSlabOps
+        self.ops = {s: factory(slab_arrays(ga, self.slabs[s]), self.L) for s in comm.local}
+        self.dim = ga.dim
+        self.device = comm.device if ops_factory is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+
+    # -- local vectors ------------------------------------------------------------------
+    def _scatter(self, v):
+        """Global vector -> {slab: local vector}, owned stages filled, halos zero."""
+        import torch
+
+        out = {}
+        for s in self.comm.local:
+            sl = self.slabs[s]
+            loc = torch.zeros(sl.local_dim, dtype=torch.float64, device=self.device)
+            loc[sl.own] = v[sl.global_own]
+            out[s] = loc
+        return out
+
+    def _dot(self, a, b):
+        return self.comm.sum({s: float(a[s][self.slabs[s].own] @ b[s][self.slabs[s].own])
+                              for s in self.comm.local})
+
+    def precond(self, r):
+        """q = P r (``nested_jacobi.py:105-122``): delta^0 = inner(r); for the further outer
+        sweeps delta = inner(r + Xi~ delta) with the delta halos exchanged first."""
+        delta = {s: self.ops[s].inner(r[s]) for s in self.comm.local}
+        for _ in range(self.S - 1):
+            self.comm.exchange(self.slabs, delta)
+            delta = {s: self.ops[s].inner(r[s] + self.ops[s].outer(delta[s]))
+                     for s in self.comm.local}
+        return delta
+
+    def delta(self, x):
+        self.comm.exchange(self.slabs, x)
+        return {s: self.ops[s].delta(x[s]) for s in self.comm.local}
+
+    # -- the solve ----------------------------------------------------------------------
+    def solve(self, rhs, tol=1e-9, max_steps=None, x0=None, callback=None):
+        """Same contract as ``pcg_solve`` (``pcg.py:50-149``): returns (x, SolveReport);
+        DimensionMismatchError / ValueError on bad input, BreakdownError on non-positive
+        curvature, MaxIterationsExceeded carrying the iterate and report."""
+        import torch
+
+        dim = self.dim
+        host = not (isinstance(rhs, torch.Tensor) and rhs.device.type != "cpu")
+        rv = torch.as_tensor(np.asarray(rhs, dtype=float) if host and not isinstance(rhs, torch.Tensor)
+                             else rhs, dtype=torch.float64)
+        if rv.dim() != 1 or rv.numel() != dim:
+            raise DimensionMismatchError("right-hand side does not match operator dimension")
+        if not bool(torch.isfinite(rv).all()):
+            raise ValueError("right-hand side contains non-finite entries")
+        if tol <= 0:
+            raise ValueError("tolerance must be positive")
+        if max_steps is None:
+            max_steps = dim + 50
+        if max_steps < 1:
+            raise ValueError("need at least one step")
+        start = time.perf_counter()
+        rv = rv.to(self.device)
+        own = {s: self.slabs[s].own for s in self.comm.local}
+        loc = self.comm.local
+        r = self._scatter(rv)
+        if x0 is None:
+            x = {s: torch.zeros_like(r[s]) for s in loc}
+        else:
+            x0v = torch.as_tensor(np.asarray(x0, dtype=float) if not isinstance(x0, torch.Tensor)
+                                  else x0, dtype=torch.float64).to(self.device)
+            if x0v.dim() != 1 or x0v.numel() != dim:
+                raise DimensionMismatchError("x0 does not match operator dimension")
+            x = self._scatter(x0v)
+            ax = self.delta(x)
+            for s in loc:
+                r[s][own[s]] = r[s][own[s]] - ax[s][own[s]]
+        d = self.precond(r) if self.precondition else {s: r[s].clone() for s in loc}
+        mu = self._dot(d, r)
+        hist, steps, converged = [], 0, False
+        for _ in range(int(max_steps)):
+            y = self.delta(d)
+            curv = self._dot(y, d)
+            if curv <= 0.0:
+                raise BreakdownError(f"non-positive curvature {curv:.3e} at step {steps + 1}")
+            alpha = mu / curv
+            for s in loc:
+                o = own[s]
+                x[s][o] += alpha * d[s][o]
+                r[s][o] = r[s][o] - alpha * y[s][o]
+            res = self.comm.max({s: float(r[s][own[s]].abs().max()) for s in loc})
+            hist.append(res)
+            steps += 1
+            if callback is not None:
+                callback(steps, self._out(x, host), self._out(r, host))
+            if res < tol:
+                converged = True
+                break
+            q = self.precond(r) if self.precondition else r
+            mu_next = self._dot(q, r)
+            beta = mu_next / mu
+            d = {s: q[s] + beta * d[s] for s in loc}
+            mu = mu_next
+        xg = self._out(x, host)
+        ga = self.arrays
+        pf = counters(ga, self.L, self.S)["apply_flops"] if self.precondition else 0.0
+        counts = _op_counts(dim, counters(ga, self.L, self.S)["matvec_flops"], pf, steps,
+                            converged, x0 is not None)
+        report = SolveReport(steps=steps, residual_inf_history=hist, converged=converged,
+                             tolerance=tol, wall_time_s=time.perf_counter() - start,
+                             op_counts=counts)
+        if not converged:
+            raise MaxIterationsExceeded(
+                f"conjugate gradient did not reach {tol:g} within {steps} steps "
+                f"(residual {report.final_residual:.3e})",
+                iterate=xg, iterations=steps, report=report)
+        return xg, report
+
+    def _out(self, v, host):
+        g = self.comm.gather(self.slabs, v, self.dim)
+        return g.cpu().numpy() if host else g
+
+
+def pcg_solve_slabs(problem, rhs, tol=1e-9, max_steps=None, x0=None, inner_sweeps=2,
+                    outer_sweeps=2, slabs=None, precondition=True, callback=None):
+    """Stage-slab sharded ``pcg_solve``: ``slabs`` slabs over the processes of the default
+    torch.distributed group (one process per GPU), or all in this process when no group is
+    initialised.  Returns the global iterate on every process."""
+    solver = SlabPcg(problem, slabs=slabs, inner_sweeps=inner_sweeps, outer_sweeps=outer_sweeps,
+                     precondition=precondition)
+    return solver.solve(rhs, tol=tol, max_steps=max_steps, x0=x0, callback=callback)
