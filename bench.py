@@ -10,9 +10,11 @@ BASELINE config 4 (mass-spring-damper 256 x 256 grid, T=200, n=2, m=1, S=L=2; se
 synthetic data, no dataset involved).  Every vector is 210.8 MB, larger than the 126 MB
 L2, so no L2 flush is needed between timed steps.
 
-Multi-GPU (torchrun): the PCGM step does not shard in round 1 (SURVEY.md 8(e) lists
-stage-slab sharding as "next"), so N ranks run N independent replicas ("replicas only");
-value = total steps of all ranks / max-over-ranks device time.
+Multi-GPU (torchrun): by default N ranks run N independent replicas of the one-context
+graph solve ("replicas only"); value = total steps of all ranks / max-over-ranks device
+time.  --slabs runs the stage-slab sharded solve instead (paper_2304_04980_b200/slab.py,
+SURVEY.md 8(e)/(f)4): one slab per rank, halos and scalars over NCCL, value = steps of the
+one global solve / max-over-ranks time ("strong" scaling).
 
 --impl reference times the CPU restatement of the reference algorithm (oracle/, the
 reference itself is pure Python + NumPy and cannot run at this size: SURVEY.md 6) on
@@ -334,6 +336,62 @@ def run_ours(args, ws, rank, local):
     return line
 
 
+def run_slabs(args, ws, rank, local):
+    """Stage-slab sharded PCGM: one slab per rank (host-orchestrated; see slab.py)."""
+    import torch
+
+    from paper_2304_04980_b200 import MaxIterationsExceeded, generators
+    from paper_2304_04980_b200.slab import SlabComm, SlabPcg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ga = generators.CONFIGS[args.config](args.seed)
+    t0 = time.perf_counter()
+    solver = SlabPcg(ga, inner_sweeps=args.L, outer_sweeps=args.S,
+                     comm=SlabComm.from_env(ws, device=dev))
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    rhs = torch.tensor(ga.offset, device=dev, dtype=torch.float64)
+    W, K = args.warmup, args.steps
+
+    def run(steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record()
+        try:
+            solver.solve(rhs, tol=1e-300, max_steps=steps)
+        except MaxIterationsExceeded:
+            pass
+        ev[1].record()
+        torch.cuda.synchronize()
+        return max_over_ranks(ev[0].elapsed_time(ev[1]), dev, ws)
+
+    run(W)
+    ms_w = run(W)
+    with ClockSampler(local) as clk:
+        ms_wk = run(W + K)
+    ms = max(ms_wk - ms_w, 1e-9)
+    sl = solver.slabs
+    return {
+        "metric": METRIC, "value": K / (ms * 1e-3), "unit": UNIT, "n_gpus": ws, "steps": K,
+        "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator, no dataset)",
+        "config": {"workload": CONFIG_NAMES.get(args.config, str(args.config)),
+                   "K": ga.K, "N": ga.N, "T": ga.T, "n": ga.n, "m": ga.m,
+                   "outer_sweeps_S": args.S, "inner_sweeps_L": args.L, "dim": ga.dim,
+                   "parallelism": f"stage slabs x{ws}",
+                   "slabs": [[x.lo, x.hi] for x in sl], "setup_s": round(setup_s, 3),
+                   "timing": "t(W+K steps) - t(W steps), both from a fresh start",
+                   "l2": "inputs larger than L2"},
+        "clocks": clk.summary(),
+    }
+
+
 def _oracle_steps(ga, S, L, steps, threads, budget_s=None):
     """Time PCGM steps of the C oracle (oracle/gridlq_oracle.c, restating pcg.py's loop);
     setup and the initial preconditioner apply are excluded.  Returns (seconds per
@@ -405,6 +463,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slabs", action="store_true",
+                    help="stage-slab sharded solve, one slab per rank (strong scaling)")
     args = ap.parse_args()
     if args.S is None:
         args.S = 3 if args.config == 3 else 2
@@ -421,7 +481,7 @@ def main():
 
         dist.init_process_group("nccl")
     try:
-        line = run_ours(args, ws, rank, local)
+        line = (run_slabs if args.slabs else run_ours)(args, ws, rank, local)
         if rank == 0:
             print(json.dumps(line), flush=True)
     finally:

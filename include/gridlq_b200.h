@@ -105,6 +105,33 @@ int gq_pcg(gq_ctx* ctx, const double* rhs, const double* x0, double tol, int64_t
            int32_t use_precond, double* x_out, double* hist_out, int64_t hist_capacity,
            int64_t* steps, int32_t* converged);
 
+/* Stage-slab mode (pcg.py:50-149 split at its reductions).
+ * The context holds the stage window of one slab: owned stages [own_lo, own_hi) plus at most
+ * one halo stage per side (own_lo in {0, 1}, own_hi in {T, T+1} of the window).  A solve is
+ *   gq_slab_start(r0 = the slab's initial residual, zero on halo stages; x0 or NULL)
+ *   init:  for s < S: INIT_OUTER(s) [exchange DL(s%2) if s < S-1]; reduce MU (sum); INIT_FINISH
+ *   step:  exchange D; DELTA; reduce CURV (sum); UPDATE; reduce RES (max);
+ *          for s < S: OUTER(s) [exchange DL(s%2) if s < S-1]; reduce MU (sum); DIRECTION
+ * (CG: S = 1).  "exchange v" = every slab packs its owned boundary stages of v
+ * (gq_slab_pack) and unpacks the neighbours' into its halo stages (gq_slab_unpack); a halo
+ * buffer holds K*N*n doubles in (column, row, state) order.  "reduce" = combine the device
+ * scalar gq_slab_scalar_ptr(ctx, which) over all slabs and write the result back into each.
+ * All calls enqueue on the context stream and return without synchronising, except
+ * gq_slab_status.  Replaces nothing in the reference (it has no multi-process path). */
+enum { GQ_SLAB_INIT_OUTER = 0, GQ_SLAB_INIT_FINISH = 1, GQ_SLAB_DELTA = 2, GQ_SLAB_UPDATE = 3,
+       GQ_SLAB_OUTER = 4, GQ_SLAB_DIRECTION = 5 };
+enum { GQ_SLAB_VEC_D = 0, GQ_SLAB_VEC_DL0 = 1, GQ_SLAB_VEC_DL1 = 2 };
+enum { GQ_SLAB_CURV = 0, GQ_SLAB_RES = 1, GQ_SLAB_MU = 2 };
+int gq_slab_enable(gq_ctx* ctx, int32_t own_lo, int32_t own_hi);
+int gq_slab_start(gq_ctx* ctx, const double* r0, const double* x0, int32_t use_precond,
+                  double tol, int64_t max_steps);
+int gq_slab_phase(gq_ctx* ctx, int32_t kind, int32_t outer);
+int gq_slab_pack(gq_ctx* ctx, int32_t which, int32_t stage, double* buf);
+int gq_slab_unpack(gq_ctx* ctx, int32_t which, int32_t stage, const double* buf);
+void* gq_slab_scalar_ptr(gq_ctx* ctx, int32_t which);
+int gq_slab_status(gq_ctx* ctx, int64_t* step, int32_t* done, int32_t* converged,
+                   int32_t* breakdown);
+
 /* Primal recovery and first-order optimality residuals (recovery.py:50-80).
  *   gq_recover:      x = -Qinv (A~' lam), u = -Rinv (B~' lam), objective 0.5 (x'Qx + u'Ru)
  *                    [recovery.py:50-65; kkt_assembly.py:84-160]

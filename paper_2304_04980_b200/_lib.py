@@ -18,6 +18,11 @@ LIB_PATH = os.path.join(HERE, "libgridlq_b200.so")
 GQ_OK, GQ_MAX_ITER, GQ_BREAKDOWN, GQ_DIM_MISMATCH, GQ_INVALID_ARG, GQ_NOT_SPD, \
     GQ_CUDA_ERROR, GQ_UNSUPPORTED = range(8)
 GQ_VEC_X, GQ_VEC_R = 0, 1
+# stage-slab mode (include/gridlq_b200.h)
+GQ_SLAB_INIT_OUTER, GQ_SLAB_INIT_FINISH, GQ_SLAB_DELTA, GQ_SLAB_UPDATE, GQ_SLAB_OUTER, \
+    GQ_SLAB_DIRECTION = range(6)
+GQ_SLAB_VEC_D, GQ_SLAB_VEC_DL0, GQ_SLAB_VEC_DL1 = range(3)
+GQ_SLAB_CURV, GQ_SLAB_RES, GQ_SLAB_MU = range(3)
 
 EXPORTS = (
     "gq_last_error", "gq_version", "gq_create", "gq_destroy", "gq_dim", "gq_set_stream",
@@ -25,7 +30,8 @@ EXPORTS = (
     "gq_apply_inner_coupling", "gq_pair_solve", "gq_apply_precond", "gq_pcg_start",
     "gq_pcg_run", "gq_pcg_read", "gq_pcg_history", "gq_pcg_scalars", "gq_pcg",
     "gq_profile_steps", "gq_kernel_name", "gq_launches_per_step", "gq_input_dim",
-    "gq_recover", "gq_kkt_residual", "gq_nbjm_solve",
+    "gq_recover", "gq_kkt_residual", "gq_nbjm_solve", "gq_slab_enable", "gq_slab_start",
+    "gq_slab_phase", "gq_slab_pack", "gq_slab_unpack", "gq_slab_scalar_ptr", "gq_slab_status",
 )
 
 
@@ -87,6 +93,14 @@ def load():
         "gq_kkt_residual": (ctypes.c_int, [vp, dp, dp, dp, dp, dp]),
         "gq_nbjm_solve": (ctypes.c_int, [vp, dp, ctypes.c_double, i64, dp,
                                          ctypes.POINTER(ctypes.c_int64)]),
+        "gq_slab_enable": (ctypes.c_int, [vp, i32, i32]),
+        "gq_slab_start": (ctypes.c_int, [vp, dp, dp, i32, ctypes.c_double, i64]),
+        "gq_slab_phase": (ctypes.c_int, [vp, i32, i32]),
+        "gq_slab_pack": (ctypes.c_int, [vp, i32, i32, dp]),
+        "gq_slab_unpack": (ctypes.c_int, [vp, i32, i32, dp]),
+        "gq_slab_scalar_ptr": (ctypes.c_void_p, [vp, i32]),
+        "gq_slab_status": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_int64)]
+                           + [ctypes.POINTER(ctypes.c_int32)] * 3),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

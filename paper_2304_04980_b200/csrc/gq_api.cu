@@ -88,6 +88,9 @@ struct gq_ctx {
   bool started = false;
   int use_precond = 1;
   std::vector<std::string> knames;
+  // stage-slab mode: local halo stages (-1: none), a pinned scratch for status reads
+  bool slab = false;
+  int slab_t0 = -1, slab_t1 = -1;
 };
 
 extern "C" const char* gq_last_error(void) { return g_err.c_str(); }
@@ -593,13 +596,14 @@ static int export_vec(gq_ctx* c, const double* src, double* dst) {
   return GQ_OK;
 }
 
-// S outer x L inner sweeps from zero: out = P r  (nested_jacobi.py:105-122)
-static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* st, int dotmode,
-                           std::vector<std::string>* names,
-                           const std::function<int()>& mark = nullptr,
-                           const double* fuse_y = nullptr) {
-  for (int s = 0; s < c->S; ++s) {
-    if ((c->fast || c->chain) && s > 0) {
+// Outer sweep s of the preconditioner, inner sweeps [l0, L) (the stage-slab phases run an
+// outer sweep in pieces; enqueue_precond runs them all).
+static int enqueue_outer(gq_ctx* c, int s, int l0, int l1, const double* rin, double* out,
+                         PcgState* st,
+                         int dotmode, std::vector<std::string>* names,
+                         const std::function<int()>& mark, const double* fuse_y) {
+  {
+    if ((c->fast || c->chain) && s > 0 && l0 == 0) {
       // rhs_s = r + Xi~ delta_{s-1}, materialised once per outer sweep (nested_jacobi.py:119-121)
       if (c->st2) {
         CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kOuterRhs, c->dl[(s - 1) % 2],
@@ -624,7 +628,7 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
         if (rc) return rc;
       }
     }
-    for (int l = 0; l < c->L; ++l) {
+    for (int l = l0; l < l1; ++l) {
       const bool last = (l == c->L - 1);
       double* ob = last ? (s == c->S - 1 ? out : c->dl[s % 2]) : c->th[l % 2];
       const double* tp = l > 0 ? c->th[(l - 1) % 2] : nullptr;
@@ -660,6 +664,18 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
         if (rc) return rc;
       }
     }
+  }
+  return GQ_OK;
+}
+
+// S outer x L inner sweeps from zero: out = P r  (nested_jacobi.py:105-122)
+static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* st, int dotmode,
+                           std::vector<std::string>* names,
+                           const std::function<int()>& mark = nullptr,
+                           const double* fuse_y = nullptr) {
+  for (int s = 0; s < c->S; ++s) {
+    const int rc = enqueue_outer(c, s, 0, c->L, rin, out, st, dotmode, names, mark, fuse_y);
+    if (rc) return rc;
   }
   return GQ_OK;
 }
@@ -827,15 +843,8 @@ extern "C" int gq_apply_precond(gq_ctx* c, const double* r, double* q) {
 
 // ---- PCG ----------------------------------------------------------------------------------
 
-static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* names,
-                        std::vector<cudaEvent_t>* evs) {
-  size_t ei = 0;
-  auto mark = [&]() -> int {
-    if (evs) CK(cudaEventRecord((*evs)[ei++], c->stream));
-    return GQ_OK;
-  };
-  int rc = mark();
-  if (rc) return rc;
+// y = Delta d with the curvature y.d and alpha (first kernel of a PCG step, pcg.py:99-108)
+static int enqueue_delta_step(gq_ctx* c) {
   if (c->st2)
     CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kDelta, c->d, nullptr, c->y,
                   c->sm_count, c->partials, c->st, kDotStep, c->stream));
@@ -854,6 +863,19 @@ static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* na
   else
     CK(launch_stencil(c->g, c->op, kDelta, c->d, c->y, c->sh_delta, c->partials, c->st,
                       kDotStep, c->stream));
+  return GQ_OK;
+}
+
+static int enqueue_step(gq_ctx* c, int use_precond, std::vector<std::string>* names,
+                        std::vector<cudaEvent_t>* evs) {
+  size_t ei = 0;
+  auto mark = [&]() -> int {
+    if (evs) CK(cudaEventRecord((*evs)[ei++], c->stream));
+    return GQ_OK;
+  };
+  int rc = mark();
+  if (rc) return rc;
+  if ((rc = enqueue_delta_step(c))) return rc;
   if (names) names->push_back("delta");
   if ((rc = mark())) return rc;
   // x += alpha d only feeds the result.  By default it is a separate kernel on a parallel
@@ -1051,6 +1073,153 @@ extern "C" int gq_pcg_scalars(gq_ctx* c, double* mu, double* curv, double* alpha
   if (curv) *curv = c->h_st->curv;
   if (alpha) *alpha = c->h_st->alpha;
   if (beta) *beta = c->h_st->beta;
+  return GQ_OK;
+}
+
+// ---- stage-slab mode (driven by slab.py) ------------------------
+// The context holds a stage window of the global problem.  A PCG step is split into phases
+// at the points where the slabs must agree: the host exchanges halo stages (d before Delta,
+// delta^s between outer sweeps) and reduces the partial scalars (curvature, max|r|, q.r)
+// between phases; each phase starts with the kernel that turns the reduced value into the
+// global decision (gq_slab.cu).  Phases are enqueued on the context stream without a sync.
+
+extern "C" int gq_slab_enable(gq_ctx* c, int32_t own_lo, int32_t own_hi) {
+  if (!c) return fail(GQ_INVALID_ARG, "null context");
+  const int T1 = c->g.T1;
+  if (own_lo < 0 || own_lo > 1 || own_hi <= own_lo || own_hi > T1 || own_hi < T1 - 1)
+    return fail(GQ_INVALID_ARG, "slab window: owned stages must be the window minus at most one "
+                                "halo stage per side");
+  c->slab = true;
+  c->slab_t0 = own_lo > 0 ? 0 : -1;
+  c->slab_t1 = own_hi < T1 ? T1 - 1 : -1;
+  c->fuse_x = false;
+  c->started = false;
+  return GQ_OK;
+}
+
+extern "C" int gq_slab_start(gq_ctx* c, const double* r0, const double* x0, int32_t use_precond,
+                             double tol, int64_t max_steps) {
+  if (!c || !r0) return fail(GQ_INVALID_ARG, "null argument");
+  if (!c->slab) return fail(GQ_INVALID_ARG, "gq_slab_enable has not been called");
+  if (use_precond && (c->L % 2))
+    return fail(GQ_INVALID_ARG, "preconditioner use requires an even inner budget (got " +
+                                    std::to_string(c->L) + "); odd budgets are standalone-only");
+  if (!(tol > 0)) return fail(GQ_INVALID_ARG, "tolerance must be positive");
+  if (max_steps < 1) return fail(GQ_INVALID_ARG, "need at least one step");
+  int rc = ensure_hist(c, max_steps);
+  if (rc) return rc;
+  c->use_precond = use_precond ? 1 : 0;
+  memset(c->h_st, 0, sizeof(PcgState));
+  c->h_st->hist = c->hist;
+  c->h_st->tol = tol;
+  c->h_st->max_steps = max_steps;
+  CK(cudaMemcpyAsync(c->st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
+  // r0 is the slab's initial residual (rhs, or rhs - Delta x0 formed by the caller), zero on
+  // the halo stages; x0 only seeds the iterate
+  if ((rc = import_vec(c, r0, c->r))) return rc;
+  if (x0) {
+    if ((rc = import_vec(c, x0, c->x))) return rc;
+  } else {
+    CK(cudaMemsetAsync(c->x, 0, c->g.dim * 8, c->stream));
+  }
+  c->started = true;
+  return GQ_OK;
+}
+
+extern "C" int gq_slab_phase(gq_ctx* c, int32_t kind, int32_t s) {
+  if (!c || !c->slab || !c->started) return fail(GQ_INVALID_ARG, "slab solve not started");
+  const bool pc = c->use_precond != 0;
+  const bool fr = pc && c->fuse_r;
+  const std::function<int()> none;
+  int rc = GQ_OK;
+  switch (kind) {
+    case GQ_SLAB_INIT_OUTER:   // d = P r, mu = d.r (pcg.py:87-93), outer sweep s
+      if (pc) {
+        if (s < 0 || s >= c->S) return fail(GQ_INVALID_ARG, "outer sweep index out of range");
+        rc = enqueue_outer(c, s, 0, c->L, c->r, c->q, c->st, kDotInit, nullptr, none, nullptr);
+      } else {
+        CK(cudaMemcpyAsync(c->d, c->r, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+        CK(launch_dot(c->g, c->d, c->r, c->vblocks, c->partials, c->st, kDotInit, c->stream));
+      }
+      break;
+    case GQ_SLAB_INIT_FINISH:
+      if (pc) CK(cudaMemcpyAsync(c->d, c->q, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+      break;
+    case GQ_SLAB_DELTA:        // y = Delta d, partial y.d over the owned stages
+      if ((rc = enqueue_delta_step(c))) return rc;
+      CK(launch_slab_ydelta(c->g, c->slab_t0, c->slab_t1, c->y, c->d, c->partials, c->st,
+                            c->vblocks, c->stream));
+      break;
+    case GQ_SLAB_UPDATE:       // alpha; x += alpha d; r -= alpha y with the partial max|r|
+      CK(launch_slab_scalar(0, c->st, c->stream));
+      CK(launch_update_x(c->g, c->x, c->d, c->vblocks, c->st, c->stream));
+      if (fr)
+        rc = enqueue_outer(c, 0, 0, 1, c->r, c->q, c->st, kDotStep, nullptr, none, c->y);
+      else
+        CK(launch_update_r(c->g, c->r, c->y, c->vblocks, c->partials, c->st, c->stream));
+      break;
+    case GQ_SLAB_OUTER: {      // convergence test; outer sweep s of q = P r (+ partial q.r)
+      const int S = pc ? c->S : 1;
+      if (s < 0 || s >= S) return fail(GQ_INVALID_ARG, "outer sweep index out of range");
+      if (s == 0) CK(launch_slab_scalar(1, c->st, c->stream));
+      if (s == S - 1) CK(launch_slab_scalar(2, c->st, c->stream));
+      if (pc)
+        rc = enqueue_outer(c, s, (s == 0 && fr) ? 1 : 0, c->L, c->r, c->q, c->st, kDotStep,
+                           nullptr, none, nullptr);
+      else
+        CK(launch_dot(c->g, c->r, c->r, c->vblocks, c->partials, c->st, kDotStep, c->stream));
+      break;
+    }
+    case GQ_SLAB_DIRECTION:    // beta; d = q + beta d
+      CK(launch_slab_scalar(3, c->st, c->stream));
+      CK(launch_dirupdate(c->g, c->d, pc ? c->q : c->r, c->vblocks, c->st, c->stream));
+      break;
+    default:
+      return fail(GQ_INVALID_ARG, "unknown slab phase");
+  }
+  return rc;
+}
+
+static double* slab_vec(gq_ctx* c, int which) {
+  return which == GQ_SLAB_VEC_D ? c->d : which == GQ_SLAB_VEC_DL0 ? c->dl[0]
+       : which == GQ_SLAB_VEC_DL1 ? c->dl[1] : nullptr;
+}
+
+extern "C" int gq_slab_pack(gq_ctx* c, int32_t which, int32_t t, double* buf) {
+  if (!c || !buf) return fail(GQ_INVALID_ARG, "null argument");
+  double* v = slab_vec(c, which);
+  if (!v || t < 0 || t >= c->g.T1) return fail(GQ_INVALID_ARG, "bad halo vector or stage");
+  CK(launch_stage_pack(c->g, t, v, buf, c->sm_count, c->stream));
+  return GQ_OK;
+}
+
+extern "C" int gq_slab_unpack(gq_ctx* c, int32_t which, int32_t t, const double* buf) {
+  if (!c || !buf) return fail(GQ_INVALID_ARG, "null argument");
+  double* v = slab_vec(c, which);
+  if (!v || t < 0 || t >= c->g.T1) return fail(GQ_INVALID_ARG, "bad halo vector or stage");
+  CK(launch_stage_unpack(c->g, t, buf, v, c->sm_count, c->stream));
+  return GQ_OK;
+}
+
+extern "C" void* gq_slab_scalar_ptr(gq_ctx* c, int32_t which) {
+  if (!c || !c->st) return nullptr;
+  switch (which) {
+    case GQ_SLAB_CURV: return &c->st->curv;
+    case GQ_SLAB_RES: return &c->st->res;
+    case GQ_SLAB_MU: return &c->st->mu;
+    default: return nullptr;
+  }
+}
+
+extern "C" int gq_slab_status(gq_ctx* c, int64_t* step, int32_t* done, int32_t* converged,
+                              int32_t* breakdown) {
+  if (!c) return fail(GQ_INVALID_ARG, "null context");
+  CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (step) *step = c->h_st->step;
+  if (done) *done = c->h_st->done;
+  if (converged) *converged = c->h_st->converged;
+  if (breakdown) *breakdown = c->h_st->breakdown;
   return GQ_OK;
 }
 

@@ -60,6 +60,7 @@ struct Ops {
 // everything that changes between runs from here.
 struct PcgState {
   double mu, curv, alpha, beta, res, tol;
+  double mu_prev;   // stage-slab mode: mu of the previous step while q.r is reduced
   long long step, max_steps;
   double* hist;
   int done, converged, breakdown;

@@ -1,0 +1,136 @@
+// Stage-slab mode kernels (host logic in gq_api.cu and slab.py).
+//
+// A slab context holds the stage window [a, b) of the global problem: its owned stages
+// [own_lo, own_hi) plus one halo stage on each side that has a neighbour.  The step kernels
+// run unchanged on the whole window; these kernels make the slab's scalars owned-only and
+// turn the slab-local decisions of the step kernels into global ones once the host has
+// reduced the partial scalars over all slabs (pcg.py:100-131):
+//
+//   k_slab_ydelta  after Delta: y.d over the halo stages is subtracted from the partial
+//                  curvature and y is zeroed there, so r (and with it max|r| and q.r) stays
+//                  zero on the halo stages for the whole solve
+//   k_slab_alpha   after the curvature sum: breakdown test and alpha = mu / c
+//   k_slab_conv    after the max|r| reduction: history entry and convergence test
+//   k_slab_savemu / k_slab_beta   around the q.r sum: beta = mu' / mu
+//   k_stage_pack / k_stage_unpack  one stage of a stage-inner vector <-> a contiguous halo
+//                  buffer in (column, row, state) order
+#include <algorithm>
+
+#include "gq_internal.h"
+
+namespace gq {
+
+__global__ void __launch_bounds__(256) k_slab_ydelta(Geo g, int t0, int t1, double* __restrict__ y,
+                                                     const double* __restrict__ d,
+                                                     double* partials, PcgState* st) {
+  if (st->skip) return;   // the step did not run (budget or an earlier stop)
+  const long long per = g.nk * g.n;
+  const int nh = (t0 >= 0) + (t1 >= 0);
+  double acc = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < per * nh;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int h = (int)(e / per);
+    const long long w = e - h * per;
+    const int t = (h == 0 && t0 >= 0) ? t0 : t1;
+    const long long node = w / g.n;
+    const long long o = (node * g.T1 + t) * g.n + (w - node * g.n);
+    acc = fma(y[o], d[o], acc);
+    y[o] = 0.0;
+  }
+  double tot;
+  if (grid_reduce<false>(acc, partials, &st->counter[3], tot) && threadIdx.x == 0)
+    st->curv = st->curv - tot;
+}
+
+__global__ void k_slab_alpha(PcgState* st) {
+  if (st->skip) return;
+  const double c = st->curv;                // pcg.py:101-108, now the global curvature
+  if (c <= 0.0) {
+    st->breakdown = 1;
+    st->done = 1;
+  } else {
+    st->breakdown = 0;
+    st->done = 0;
+    st->alpha = st->mu / c;
+  }
+}
+
+__global__ void k_slab_conv(PcgState* st) {
+  if (st->skip || st->breakdown) return;
+  const double res = st->res;               // pcg.py:113-121, now the global max|r|
+  st->hist[st->step - 1] = res;
+  if (res < st->tol) {
+    st->converged = 1;
+    st->done = 1;
+  } else {
+    st->converged = 0;
+    st->done = 0;
+  }
+}
+
+__global__ void k_slab_savemu(PcgState* st) {
+  if (halted(st)) return;
+  st->mu_prev = st->mu;
+}
+
+__global__ void k_slab_beta(PcgState* st) {
+  if (halted(st)) return;
+  st->beta = st->mu / st->mu_prev;          // pcg.py:127-131 with the global q.r
+}
+
+__global__ void __launch_bounds__(256) k_stage_pack(Geo g, int t, const double* __restrict__ v,
+                                                    double* __restrict__ buf) {
+  const long long per = g.nk * g.n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < per;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long node = e / g.n;
+    buf[e] = v[(node * g.T1 + t) * g.n + (e - node * g.n)];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_stage_unpack(Geo g, int t, const double* __restrict__ buf,
+                                                      double* __restrict__ v) {
+  const long long per = g.nk * g.n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < per;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long node = e / g.n;
+    v[(node * g.T1 + t) * g.n + (e - node * g.n)] = buf[e];
+  }
+}
+
+static unsigned stage_blocks(const Geo& g, int sm_count) {
+  const long long per = g.nk * g.n;
+  return (unsigned)std::max(1LL, std::min<long long>((per + 255) / 256, 4LL * sm_count));
+}
+
+cudaError_t launch_slab_ydelta(const Geo& g, int t0, int t1, double* y, const double* d,
+                               double* partials, PcgState* st, int blocks, cudaStream_t s) {
+  if (t0 < 0 && t1 < 0) return cudaSuccess;
+  // `blocks` partials fit the context's partials buffer (the vector-kernel grid)
+  k_slab_ydelta<<<(unsigned)blocks, 256, 0, s>>>(g, t0, t1, y, d, partials, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slab_scalar(int which, PcgState* st, cudaStream_t s) {
+  switch (which) {
+    case 0: k_slab_alpha<<<1, 1, 0, s>>>(st); break;
+    case 1: k_slab_conv<<<1, 1, 0, s>>>(st); break;
+    case 2: k_slab_savemu<<<1, 1, 0, s>>>(st); break;
+    default: k_slab_beta<<<1, 1, 0, s>>>(st); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_pack(const Geo& g, int t, const double* v, double* buf, int sm_count,
+                              cudaStream_t s) {
+  k_stage_pack<<<stage_blocks(g, sm_count), 256, 0, s>>>(g, t, v, buf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_unpack(const Geo& g, int t, const double* buf, double* v, int sm_count,
+                                cudaStream_t s) {
+  k_stage_unpack<<<stage_blocks(g, sm_count), 256, 0, s>>>(g, t, buf, v);
+  return cudaGetLastError();
+}
+
+}  // namespace gq

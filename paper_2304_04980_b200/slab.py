@@ -19,12 +19,23 @@ one stage of delta per extra outer sweep (before Xi~ delta): ``S`` halo exchange
 
 Slabs map onto processes in contiguous blocks (one process per GPU, ``torch.distributed``
 over NCCL for the halos and scalars; gloo on CPU for the host-logic tests).  Several slabs
-may live in one process: their halos are device copies.  Scalar reductions sum per-slab
-partials in slab order, so a run is bitwise independent of the slab-to-process layout.
+may live in one process: their halos are device copies.  The composed driver sums per-slab
+partials in slab order, so its runs are bitwise independent of the slab-to-process layout;
+the native one reduces in-process first, then over the group.
 
-The local compute of a slab goes through the C ABI on its own ``gq_ctx``
-(``gq_apply_delta``, ``gq_apply_outer_coupling``, ``gq_apply_precond`` with one outer
-sweep); the oracle can stand in for it only inside the tests.
+Two drivers share this partition:
+
+* native (the default on a GPU): every slab's ``gq_ctx`` runs the PCG step kernels of the
+  one-GPU path in stage-slab mode (``gq_slab_*`` in include/gridlq_b200.h).  A step is six
+  phases enqueued on the device stream; between them the halos move by pack -> NCCL
+  send/recv (or a device copy) -> unpack and the partial scalars are reduced on the device
+  (curvature and q.r summed, max|r| maxed).  The host never waits inside a step; it polls
+  the convergence flag after 2, 4, ..., 64 steps like ``gq_pcg_run``.
+* composed (``native=False``, or an ``ops_factory``): the step is written here with torch
+  vector ops over three per-slab applies through the C ABI (``gq_apply_delta``,
+  ``gq_apply_outer_coupling``, ``gq_apply_precond`` with one outer sweep).  It is the
+  readable statement of the algorithm and the form the CPU tests drive, with the oracle
+  standing in for the applies (test-only).
 """
 
 from __future__ import annotations
@@ -130,6 +141,16 @@ class DeviceSlabOps:
         return self.ctx.unary("gq_apply_precond", r)
 
 
+class _WarmStartOps:
+    """Delta through a native slab's context (warm start only: r = rhs - Delta x0)."""
+
+    def __init__(self, nat):
+        self.nat = nat
+
+    def delta(self, x):
+        return self.nat.ctx.unary("gq_apply_delta", x)
+
+
 class SlabComm:
     """Halo exchange and scalar reductions between the slabs of one partition.
 
@@ -220,6 +241,43 @@ class SlabComm:
         return out
 
 
+class _DevScalar:
+    """A device double inside a gq_ctx, exposed to torch (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr):
+        self.__cuda_array_interface__ = {"shape": (1,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3}
+
+
+class _NativeSlab:
+    """One slab's gq_ctx in stage-slab mode, with its halo buffers and scalar views."""
+
+    def __init__(self, sub: GridArrays, sl: Slab, inner_sweeps, outer_sweeps):
+        import torch
+
+        from . import _lib
+        from .solver import _Context
+
+        self.sl = sl
+        self.ctx = _Context(sub, inner_sweeps, outer_sweeps)
+        lib, h = self.ctx.lib, self.ctx.h
+        stream = torch.cuda.current_stream()
+        _lib.check(lib.gq_set_stream(h, ctypes.c_void_p(stream.cuda_stream)))
+        _lib.check(lib.gq_slab_enable(h, sl.lo - sl.a, sl.hi - sl.a), "slab")
+        self.scalar = {}
+        for w in (_lib.GQ_SLAB_CURV, _lib.GQ_SLAB_RES, _lib.GQ_SLAB_MU):
+            ptr = lib.gq_slab_scalar_ptr(h, w)
+            self.scalar[w] = torch.as_tensor(_DevScalar(ptr), device="cuda")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.send = {side: torch.empty(sl.nh, dtype=torch.float64, device=dev) for side in (0, 1)}
+        self.recv = {side: torch.empty(sl.nh, dtype=torch.float64, device=dev) for side in (0, 1)}
+
+    def call(self, fn, *args):
+        from . import _lib
+
+        _lib.check(getattr(self.ctx.lib, fn)(self.ctx.h, *args), fn)
+
+
 class SlabPcg:
     """PCGM over a stage-slab partition (``pcg.py:50-149`` control flow).
 
@@ -227,7 +285,7 @@ class SlabPcg:
     ``DeviceSlabOps`` (the B200 path)."""
 
     def __init__(self, problem, slabs=None, inner_sweeps=2, outer_sweeps=2, comm=None,
-                 ops_factory=None, precondition=True):
+                 ops_factory=None, precondition=True, native=None):
         import torch
 
         self.arrays = as_arrays(problem)
@@ -249,8 +307,17 @@ class SlabPcg:
         self.slabs = make_slabs(ga, comm.n)
         self.L, self.S = int(inner_sweeps), int(outer_sweeps)
         self.precondition = precondition
-        factory = ops_factory or DeviceSlabOps
-        self.ops = {s: factory(slab_arrays(ga, self.slabs[s]), self.L) for s in comm.local}
+        self.native = (ops_factory is None) if native is None else bool(native)
+        if self.native and ops_factory is not None:
+            raise ValueError("the native slab driver runs the device kernels; drop ops_factory")
+        if self.native:
+            self.nat = {s: _NativeSlab(slab_arrays(ga, self.slabs[s]), self.slabs[s], self.L,
+                                       self.S) for s in comm.local}
+            # the composed applies are only needed for a warm start's r = rhs - Delta x0
+            self.ops = {s: _WarmStartOps(self.nat[s]) for s in comm.local}
+        else:
+            factory = ops_factory or DeviceSlabOps
+            self.ops = {s: factory(slab_arrays(ga, self.slabs[s]), self.L) for s in comm.local}
         self.dim = ga.dim
         self.device = comm.device if ops_factory is not None else \
             torch.device("cuda", torch.cuda.current_device())
@@ -312,6 +379,7 @@ class SlabPcg:
         own = {s: self.slabs[s].own for s in self.comm.local}
         loc = self.comm.local
         r = self._scatter(rv)
+        x0s = None
         if x0 is None:
             x = {s: torch.zeros_like(r[s]) for s in loc}
         else:
@@ -323,6 +391,9 @@ class SlabPcg:
             ax = self.delta(x)
             for s in loc:
                 r[s][own[s]] = r[s][own[s]] - ax[s][own[s]]
+            x0s = x
+        if self.native:
+            return self._solve_native(r, x0s, tol, int(max_steps), host, start, callback)
         d = self.precond(r) if self.precondition else {s: r[s].clone() for s in loc}
         mu = self._dot(d, r)
         hist, steps, converged = [], 0, False
@@ -349,14 +420,143 @@ class SlabPcg:
             beta = mu_next / mu
             d = {s: q[s] + beta * d[s] for s in loc}
             mu = mu_next
-        xg = self._out(x, host)
+        return self._finish(self._out(x, host), hist, steps, converged, tol, start,
+                            x0 is not None)
+
+    # -- native stage-slab mode ------------------------------------------------------------
+    def _nexchange(self, which):
+        """Halo exchange of a device work vector (gq_slab_pack / NCCL or copy / unpack)."""
+        import torch.distributed as dist
+
+        comm, nat, slabs = self.comm, self.nat, self.slabs
+        comm.exchanges += 1
+        sides = {}
+        for s in comm.local:
+            sl = slabs[s]
+            for side, nb, mine, theirs in ((0, s - 1, sl.lo - 1, sl.lo), (1, s + 1, sl.hi, sl.hi - 1)):
+                if 0 <= nb < comm.n:
+                    sides.setdefault(s, []).append((side, nb, mine - sl.a, theirs - sl.a))
+                    nat[s].call("gq_slab_pack", which, theirs - sl.a,
+                                ctypes.c_void_p(nat[s].send[side].data_ptr()))
+        reqs, later = [], []
+        for s, lst in sides.items():
+            for side, nb, halo_t, _ in lst:
+                if comm.owner[nb] == comm.rank:
+                    src = nat[nb].send[1 - side]
+                    nat[s].call("gq_slab_unpack", which, halo_t, ctypes.c_void_p(src.data_ptr()))
+                else:
+                    peer = comm.owner[nb]
+                    reqs.append(dist.isend(nat[s].send[side], peer, group=comm.group))
+                    reqs.append(dist.irecv(nat[s].recv[side], peer, group=comm.group))
+                    later.append((s, side, halo_t))
+        for q in reqs:
+            q.wait()
+        for s, side, halo_t in later:
+            nat[s].call("gq_slab_unpack", which, halo_t, ctypes.c_void_p(nat[s].recv[side].data_ptr()))
+
+    def _nreduce(self, which, op):
+        """Combine one device scalar over all slabs (slab order in-process, then NCCL)."""
+        import torch
+        import torch.distributed as dist
+
+        vals = [self.nat[s].scalar[which] for s in self.comm.local]
+        if len(vals) == 1:
+            tot = vals[0]
+        else:
+            tot = vals[0].clone()
+            for v in vals[1:]:
+                tot = tot + v if op == "sum" else torch.maximum(tot, v)
+        if self.comm.world > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX,
+                            group=self.comm.group)
+        for v in vals:
+            if v is not tot:
+                v.copy_(tot)
+
+    def _nphase(self, kind, s=0):
+        for k in self.comm.local:
+            self.nat[k].call("gq_slab_phase", kind, s)
+
+    def _nstep(self, S):
+        from . import _lib
+
+        self._nexchange(_lib.GQ_SLAB_VEC_D)
+        self._nphase(_lib.GQ_SLAB_DELTA)
+        self._nreduce(_lib.GQ_SLAB_CURV, "sum")
+        self._nphase(_lib.GQ_SLAB_UPDATE)
+        self._nreduce(_lib.GQ_SLAB_RES, "max")
+        for s in range(S):
+            self._nphase(_lib.GQ_SLAB_OUTER, s)
+            if s < S - 1:
+                self._nexchange(_lib.GQ_SLAB_VEC_DL0 + s % 2)
+        self._nreduce(_lib.GQ_SLAB_MU, "sum")
+        self._nphase(_lib.GQ_SLAB_DIRECTION)
+
+    def _solve_native(self, r, x0s, tol, max_steps, host, start, callback=None):
+        import torch
+
+        from . import _lib
+
+        loc = self.comm.local
+        S = self.S if self.precondition else 1
+        for s in loc:
+            xp = ctypes.c_void_p(x0s[s].data_ptr()) if x0s is not None else None
+            self.nat[s].call("gq_slab_start", ctypes.c_void_p(r[s].data_ptr()), xp,
+                             int(self.precondition), float(tol), int(max_steps))
+        for s in range(S):
+            self._nphase(_lib.GQ_SLAB_INIT_OUTER, s)
+            if s < S - 1:
+                self._nexchange(_lib.GQ_SLAB_VEC_DL0 + s % 2)
+        self._nreduce(_lib.GQ_SLAB_MU, "sum")
+        self._nphase(_lib.GQ_SLAB_INIT_FINISH)
+        first = self.nat[loc[0]]
+        step, done = ctypes.c_int64(), ctypes.c_int32()
+        conv, brk = ctypes.c_int32(), ctypes.c_int32()
+        issued, chunk = 0, 1 if callback is not None else 2
+        while True:
+            todo = min(chunk, max_steps - issued)
+            for _ in range(todo):
+                self._nstep(S)
+            issued += todo
+            first.call("gq_slab_status", ctypes.byref(step), ctypes.byref(done),
+                       ctypes.byref(conv), ctypes.byref(brk))
+            if callback is not None and not brk.value and step.value == issued:
+                callback(int(step.value), self._nread(_lib.GQ_VEC_X, host),
+                         self._nread(_lib.GQ_VEC_R, host))
+            if done.value or step.value >= max_steps or issued >= max_steps:
+                break
+            if callback is None:
+                chunk = min(chunk * 2, 64)
+        steps = int(step.value)
+        hist = np.empty(steps)
+        if steps:
+            first.call("gq_pcg_history", hist.ctypes.data, steps)
+        if brk.value:
+            raise BreakdownError(f"non-positive curvature at step {steps + 1}; operator or "
+                                 "preconditioner is not positive definite")
+        xg = self._nread(_lib.GQ_VEC_X, host)
+        converged = bool(conv.value)
+        return self._finish(xg, hist.tolist(), steps, converged, tol, start, x0s is not None)
+
+    def _nread(self, which, host):
+        """Global x or r assembled from the slabs' owned stages."""
+        import torch
+
+        vs = {}
+        for s in self.comm.local:
+            vs[s] = torch.empty(self.slabs[s].local_dim, dtype=torch.float64, device=self.device)
+            self.nat[s].call("gq_pcg_read", which, ctypes.c_void_p(vs[s].data_ptr()))
+        return self._out(vs, host)
+
+    def _finish(self, xg, hist, steps, converged, tol, start, warm):
         ga = self.arrays
-        pf = counters(ga, self.L, self.S)["apply_flops"] if self.precondition else 0.0
-        counts = _op_counts(dim, counters(ga, self.L, self.S)["matvec_flops"], pf, steps,
-                            converged, x0 is not None)
-        report = SolveReport(steps=steps, residual_inf_history=hist, converged=converged,
-                             tolerance=tol, wall_time_s=time.perf_counter() - start,
-                             op_counts=counts)
+        cnt = counters(ga, self.L, self.S)
+        counts = _op_counts(self.dim, cnt["matvec_flops"],
+                            cnt["apply_flops"] if self.precondition else 0.0, steps, converged,
+                            warm)
+        report = SolveReport(steps=steps, residual_inf_history=[float(h) for h in hist],
+                             converged=converged, tolerance=tol,
+                             wall_time_s=time.perf_counter() - start, op_counts=counts)
         if not converged:
             raise MaxIterationsExceeded(
                 f"conjugate gradient did not reach {tol:g} within {steps} steps "
@@ -370,10 +570,10 @@ class SlabPcg:
 
 
 def pcg_solve_slabs(problem, rhs, tol=1e-9, max_steps=None, x0=None, inner_sweeps=2,
-                    outer_sweeps=2, slabs=None, precondition=True, callback=None):
+                    outer_sweeps=2, slabs=None, precondition=True, callback=None, native=None):
     """Stage-slab sharded ``pcg_solve``: ``slabs`` slabs over the processes of the default
     torch.distributed group (one process per GPU), or all in this process when no group is
     initialised.  Returns the global iterate on every process."""
     solver = SlabPcg(problem, slabs=slabs, inner_sweeps=inner_sweeps, outer_sweeps=outer_sweeps,
-                     precondition=precondition)
+                     precondition=precondition, native=native)
     return solver.solve(rhs, tol=tol, max_steps=max_steps, x0=x0, callback=callback)

@@ -187,19 +187,41 @@ def test_slab_pcg_gloo(name, slabs):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", SMALL + ["config2", "config4r", "config3r"])
 @pytest.mark.parametrize("slabs", [2, 3])
-def test_gpu_slab_pcg(name, slabs):
+@pytest.mark.parametrize("native", [True, False])
+def test_gpu_slab_pcg(name, slabs, native):
+    """Both drivers (native stage-slab phases; composed applies) against the golden runs."""
     ga, rec = load_golden(name)
     if slabs > ga.T + 1:
         pytest.skip("fewer stages than slabs")
     solver = SlabPcg(ga, inner_sweeps=rec["L"], outer_sweeps=rec["S"],
                      comm=SlabComm(slabs, device=torch.device("cuda")),
-                     precondition=bool(rec["precond"]))
+                     precondition=bool(rec["precond"]), native=native)
     try:
         x, rep = solver.solve(ga.offset, tol=rec["tol"], max_steps=rec["max_steps"],
                               x0=rec.get("x0"))
     except MaxIterationsExceeded as exc:
         x, rep = exc.iterate, exc.report
     check_run(name, rec, x, rep.residual_inf_history, rep.steps, rep.converged, {})
+
+
+@pytest.mark.gpu
+def test_gpu_native_slab_callback_and_errors():
+    """Native driver: per-step callback iterates match the golden snapshots; a budget
+    exhausted run raises MaxIterationsExceeded with the iterate; every stage its own slab."""
+    ga, rec = load_golden("config1")
+    snaps = {}
+    solver = SlabPcg(ga, comm=SlabComm(3, device=torch.device("cuda")))
+    with pytest.raises(MaxIterationsExceeded) as ei:
+        solver.solve(ga.offset, tol=rec["tol"], max_steps=rec["max_steps"],
+                     callback=lambda k, x, r: snaps.__setitem__(k, x.copy()))
+    check_run("config1", rec, ei.value.iterate, ei.value.report.residual_inf_history,
+              ei.value.report.steps, ei.value.report.converged,
+              {int(s): snaps[int(s)] for s in rec["snap_steps"] if int(s) in snaps})
+    assert sorted(snaps) == list(range(1, rec["steps"] + 1))
+    ga, rec = load_golden("time_varying")
+    solver = SlabPcg(ga, comm=SlabComm(ga.T + 1, device=torch.device("cuda")))
+    x, rep = solver.solve(ga.offset, tol=rec["tol"], max_steps=rec["max_steps"])
+    check_run("time_varying", rec, x, rep.residual_inf_history, rep.steps, rep.converged, {})
 
 
 @pytest.mark.gpu
@@ -216,12 +238,13 @@ def test_gpu_slabs_match_single_context():
         x1, r1 = pcg_solve(op, pc, ga.offset, tol=1e-300, max_steps=25)
     except MaxIterationsExceeded as exc:
         x1, r1 = exc.iterate, exc.report
-    solver = SlabPcg(ga, comm=SlabComm(4, device=torch.device("cuda")))
-    try:
-        x2, r2 = solver.solve(ga.offset, tol=1e-300, max_steps=25)
-    except MaxIterationsExceeded as exc:
-        x2, r2 = exc.iterate, exc.report
-    assert r2.steps == r1.steps == 25
-    assert rel_err(x2, x1) < 1e-9
-    h1, h2 = np.array(r1.residual_inf_history), np.array(r2.residual_inf_history)
-    assert np.all(np.abs(h2 - h1) <= 1e-9 * h1 + 1e-14 * h1[0])
+    for native in (True, False):
+        solver = SlabPcg(ga, comm=SlabComm(4, device=torch.device("cuda")), native=native)
+        try:
+            x2, r2 = solver.solve(ga.offset, tol=1e-300, max_steps=25)
+        except MaxIterationsExceeded as exc:
+            x2, r2 = exc.iterate, exc.report
+        assert r2.steps == r1.steps == 25
+        assert rel_err(x2, x1) < 1e-9
+        h1, h2 = np.array(r1.residual_inf_history), np.array(r2.residual_inf_history)
+        assert np.all(np.abs(h2 - h1) <= 1e-9 * h1 + 1e-14 * h1[0])
