@@ -197,9 +197,11 @@ class SlabComm:
                     halo.copy_(vecs[nb][slabs[nb].stage(mine)])
                 else:
                     peer = self.owner[nb]
-                    reqs.append(dist.isend(vecs[s][sl.stage(theirs)], peer, group=self.group))
-                    reqs.append(dist.irecv(halo, peer, group=self.group))
-        for r in reqs:
+                    reqs.append(dist.P2POp(dist.isend, vecs[s][sl.stage(theirs)], peer,
+                                           group=self.group))
+                    reqs.append(dist.P2POp(dist.irecv, halo, peer, group=self.group))
+        # one NCCL group for all sends and receives: both directions in flight together
+        for r in (dist.batch_isend_irecv(reqs) if reqs else []):
             r.wait()
 
     def _reduce(self, partials, op):
@@ -446,10 +448,10 @@ class SlabPcg:
                     nat[s].call("gq_slab_unpack", which, halo_t, ctypes.c_void_p(src.data_ptr()))
                 else:
                     peer = comm.owner[nb]
-                    reqs.append(dist.isend(nat[s].send[side], peer, group=comm.group))
-                    reqs.append(dist.irecv(nat[s].recv[side], peer, group=comm.group))
+                    reqs.append(dist.P2POp(dist.isend, nat[s].send[side], peer, group=comm.group))
+                    reqs.append(dist.P2POp(dist.irecv, nat[s].recv[side], peer, group=comm.group))
                     later.append((s, side, halo_t))
-        for q in reqs:
+        for q in (dist.batch_isend_irecv(reqs) if reqs else []):
             q.wait()
         for s, side, halo_t in later:
             nat[s].call("gq_slab_unpack", which, halo_t, ctypes.c_void_p(nat[s].recv[side].data_ptr()))

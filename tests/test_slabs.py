@@ -248,3 +248,101 @@ def test_gpu_slabs_match_single_context():
         assert rel_err(x2, x1) < 1e-9
         h1, h2 = np.array(r1.residual_inf_history), np.array(r2.residual_inf_history)
         assert np.all(np.abs(h2 - h1) <= 1e-9 * h1 + 1e-14 * h1[0])
+
+
+# ---- native driver host logic (halo routing and scalar reductions) on CPU -----------------
+
+class _FakeNative:
+    """Stands in for _NativeSlab on CPU: a reference-order window vector per halo vector
+    id; gq_slab_pack / gq_slab_unpack move one stage between it and a halo buffer."""
+
+    def __init__(self, sl, value):
+        self.sl = sl
+        self.vec = {w: torch.zeros(sl.local_dim, dtype=torch.float64) for w in (0, 1, 2)}
+        for w in self.vec:   # owned stages carry (global stage, vector id, value)
+            for t in range(sl.lo, sl.hi):
+                self.vec[w][sl.stage(t)] = 1000.0 * t + 10.0 * w + torch.arange(sl.nh) * 1e-3
+        self.send = {k: torch.empty(sl.nh, dtype=torch.float64) for k in (0, 1)}
+        self.recv = {k: torch.empty(sl.nh, dtype=torch.float64) for k in (0, 1)}
+        self.scalar = {w: torch.tensor([value + w], dtype=torch.float64) for w in (0, 1, 2)}
+
+    def _buf(self, ptr, others):
+        for n in others:
+            for b in list(n.send.values()) + list(n.recv.values()):
+                if b.data_ptr() == ptr.value:
+                    return b
+        raise KeyError(ptr)
+
+    def call(self, fn, which, t, ptr):
+        lt = self.sl.a + t
+        if fn == "gq_slab_pack":
+            self._buf(ptr, [self]).copy_(self.vec[which][self.sl.stage(lt)])
+        else:
+            self.vec[which][self.sl.stage(lt)] = self._buf(ptr, _FakeNative.everyone)
+
+
+def _native_logic(comm, ga):
+    s = object.__new__(SlabPcg)
+    s.comm, s.slabs = comm, make_slabs(ga, comm.n)
+    _FakeNative.everyone = []
+    s.nat = {k: _FakeNative(s.slabs[k], float(k + 1)) for k in comm.local}
+    _FakeNative.everyone = list(s.nat.values())
+    for w in (0, 1, 2):
+        s._nexchange(w)
+    s._nreduce(0, "sum")
+    s._nreduce(1, "max")
+    out = {}
+    for k, nat in s.nat.items():
+        sl = nat.sl
+        halos = {}
+        for t in (sl.lo - 1, sl.hi):
+            if sl.a <= t < sl.b:
+                halos[t] = [nat.vec[w][sl.stage(t)].tolist() for w in (0, 1, 2)]
+        out[k] = (halos, float(nat.scalar[0]), float(nat.scalar[1]))
+    return out
+
+
+def _check_native_logic(out, ga, n):
+    nh = ga.K * ga.N * ga.n
+    for k, (halos, ssum, smax) in out.items():
+        assert ssum == sum(float(j + 1) for j in range(n))          # curvature slot: summed
+        assert smax == float(n) + 1.0                                # residual slot: max
+        for t, vs in halos.items():
+            for w, v in enumerate(vs):
+                assert np.allclose(v, 1000.0 * t + 10.0 * w + np.arange(nh) * 1e-3)
+
+
+def test_native_exchange_and_reduce_in_process():
+    ga, _ = load_golden("config1")
+    out = _native_logic(SlabComm(4), ga)
+    assert sorted(out) == [0, 1, 2, 3]
+    _check_native_logic(out, ga, 4)
+
+
+def _native_gloo_worker(rank, ws, port, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        ga, _ = load_golden("config1")
+        res = _native_logic(SlabComm.from_env(4), ga)
+        out[rank] = {k: v for k, v in res.items()}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_native_exchange_and_reduce_gloo():
+    """The native driver's halo routing (pack -> isend/irecv -> unpack across processes,
+    device copy inside one) and scalar reductions, world_size 2 with 2 slabs each."""
+    import torch.multiprocessing as mp
+
+    out = mp.Manager().list([None, None])
+    mp.spawn(_native_gloo_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    ga, _ = load_golden("config1")
+    merged = {}
+    for part in out:
+        merged.update(part)
+    assert sorted(merged) == [0, 1, 2, 3]
+    _check_native_logic(merged, ga, 4)
