@@ -36,6 +36,8 @@ static int fail(int code, const std::string& msg) {
       return fail(GQ_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+constexpr int kStageChunks = 8;   // pinned-staging pipeline depth (import_vec / export_vec)
+
 struct gq_ctx {
   Geo g{};
   int m = 0, L = 2, S = 2, n_dyn = 0, n_cost = 0, npc = 0, nxc = 0, sm_count = 148;
@@ -77,6 +79,7 @@ struct gq_ctx {
   PcgState* st = nullptr;
   PcgState* h_st = nullptr;   // pinned mirror
   double* h_stage = nullptr;  // pinned staging vector for pageable host buffers
+  cudaEvent_t ev_stage[kStageChunks] = {};   // its chunked copies
   double* hist = nullptr;
   long long hist_cap = 0;
   SetupErr* err = nullptr;
@@ -122,6 +125,8 @@ static void release(gq_ctx* c) {
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  for (cudaEvent_t& e : c->ev_stage)
+    if (e) cudaEventDestroy(e);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);
@@ -522,6 +527,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
 
 // user vector (reference layout, host or device) -> internal vector `dst`
 static int ensure_stage(gq_ctx* c);
+static size_t stage_chunk_begin(const gq_ctx* c, int k);
 static bool is_pageable_host(const void* p);
 static void parallel_copy(double* dst, const double* src, size_t n);
 
@@ -532,10 +538,16 @@ static int import_vec(gq_ctx* c, const double* src, double* dst) {
       int rc = ensure_stage(c);
       if (rc) return rc;
       CK(cudaStreamSynchronize(c->stream));   // the stage may still feed an earlier copy
-      parallel_copy(c->h_stage, src, (size_t)c->g.dim);
-      src = c->h_stage;
+      // chunked: the host copy of chunk k+1 overlaps the DMA of chunk k
+      for (int k = 0; k < kStageChunks; ++k) {
+        const size_t b = stage_chunk_begin(c, k), e = stage_chunk_begin(c, k + 1);
+        parallel_copy(c->h_stage + b, src + b, e - b);
+        CK(cudaMemcpyAsync(c->tmp1 + b, c->h_stage + b, (e - b) * 8, cudaMemcpyHostToDevice,
+                           c->stream));
+      }
+    } else {
+      CK(cudaMemcpyAsync(c->tmp1, src, c->g.dim * 8, cudaMemcpyHostToDevice, c->stream));
     }
-    CK(cudaMemcpyAsync(c->tmp1, src, c->g.dim * 8, cudaMemcpyHostToDevice, c->stream));
     ref = c->tmp1;
   }
   CK(launch_to_internal(c->g, ref, dst, c->stream));
@@ -574,7 +586,13 @@ static void parallel_copy(double* dst, const double* src, size_t n) {
 
 static int ensure_stage(gq_ctx* c) {
   if (!c->h_stage) CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_stage), c->g.dim * 8));
+  for (int k = 0; k < kStageChunks; ++k)
+    if (!c->ev_stage[k]) CK(cudaEventCreateWithFlags(&c->ev_stage[k], cudaEventDisableTiming));
   return GQ_OK;
+}
+
+static size_t stage_chunk_begin(const gq_ctx* c, int k) {
+  return (size_t)c->g.dim * (size_t)k / kStageChunks;
 }
 
 static int export_vec(gq_ctx* c, const double* src, double* dst) {
@@ -585,9 +603,18 @@ static int export_vec(gq_ctx* c, const double* src, double* dst) {
     if (is_pageable_host(dst) && c->g.dim * 8 >= (8LL << 20)) {
       int rc = ensure_stage(c);
       if (rc) return rc;
-      CK(cudaMemcpyAsync(c->h_stage, c->tmp1, c->g.dim * 8, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      parallel_copy(dst, c->h_stage, (size_t)c->g.dim);
+      // chunked: the host copy of chunk k overlaps the DMA of the chunks after it
+      for (int k = 0; k < kStageChunks; ++k) {
+        const size_t b = stage_chunk_begin(c, k), e = stage_chunk_begin(c, k + 1);
+        CK(cudaMemcpyAsync(c->h_stage + b, c->tmp1 + b, (e - b) * 8, cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaEventRecord(c->ev_stage[k], c->stream));
+      }
+      for (int k = 0; k < kStageChunks; ++k) {
+        const size_t b = stage_chunk_begin(c, k), e = stage_chunk_begin(c, k + 1);
+        CK(cudaEventSynchronize(c->ev_stage[k]));
+        parallel_copy(dst + b, c->h_stage + b, e - b);
+      }
       return GQ_OK;
     }
     CK(cudaMemcpyAsync(dst, c->tmp1, c->g.dim * 8, cudaMemcpyDeviceToHost, c->stream));

@@ -462,12 +462,12 @@ class SlabPcg:
         import torch.distributed as dist
 
         vals = [self.nat[s].scalar[which] for s in self.comm.local]
-        if len(vals) == 1:
-            tot = vals[0]
-        else:
-            tot = vals[0].clone()
-            for v in vals[1:]:
-                tot = tot + v if op == "sum" else torch.maximum(tot, v)
+        if len(vals) == 1 and self.comm.world == 1:
+            return
+        # a torch-allocated scalar carries the collective (the slots live in library memory)
+        tot = vals[0].clone()
+        for v in vals[1:]:
+            tot = tot + v if op == "sum" else torch.maximum(tot, v)
         if self.comm.world > 1:
             dist.all_reduce(tot, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX,
                             group=self.comm.group)

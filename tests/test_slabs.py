@@ -346,3 +346,28 @@ def test_native_exchange_and_reduce_gloo():
         merged.update(part)
     assert sorted(merged) == [0, 1, 2, 3]
     _check_native_logic(merged, ga, 4)
+
+
+@pytest.mark.gpu
+def test_gpu_native_slabs_headline_size():
+    """BASELINE config 4 at full size (256 x 256, T = 200) in 4 native slabs against the
+    one-context graph solve over 6 steps: iterates to 1e-9, history to 1e-9."""
+    from paper_2304_04980_b200 import GpuNestedJacobiPreconditioner, GpuSchurOperator, pcg_solve
+    from paper_2304_04980_b200.generators import config4
+
+    ga = config4(0)
+    rhs = torch.from_numpy(ga.offset).cuda()
+    op = GpuSchurOperator(ga)
+    pc = GpuNestedJacobiPreconditioner(op)
+    with pytest.raises(MaxIterationsExceeded) as e1:
+        pcg_solve(op, pc, rhs, tol=1e-300, max_steps=6)
+    x1 = e1.value.iterate.cpu().numpy()
+    h1 = np.array(e1.value.report.residual_inf_history)
+    del op, pc
+    solver = SlabPcg(ga, comm=SlabComm(4, device=torch.device("cuda")))
+    with pytest.raises(MaxIterationsExceeded) as e2:
+        solver.solve(rhs, tol=1e-300, max_steps=6)
+    x2 = e2.value.iterate.cpu().numpy()
+    h2 = np.array(e2.value.report.residual_inf_history)
+    assert rel_err(x2, x1) < 1e-9
+    assert np.all(np.abs(h2 - h1) <= 1e-9 * h1 + 1e-14 * h1[0])
