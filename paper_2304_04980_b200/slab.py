@@ -287,7 +287,7 @@ class SlabPcg:
     ``DeviceSlabOps`` (the B200 path)."""
 
     def __init__(self, problem, slabs=None, inner_sweeps=2, outer_sweeps=2, comm=None,
-                 ops_factory=None, precondition=True, native=None):
+                 ops_factory=None, precondition=True, native=None, graph=None):
         import torch
 
         self.arrays = as_arrays(problem)
@@ -313,8 +313,14 @@ class SlabPcg:
         if self.native and ops_factory is not None:
             raise ValueError("the native slab driver runs the device kernels; drop ops_factory")
         if self.native:
-            self.nat = {s: _NativeSlab(slab_arrays(ga, self.slabs[s]), self.slabs[s], self.L,
-                                       self.S) for s in comm.local}
+            # all native work runs on one dedicated stream (it is also the capture stream)
+            self.stream = torch.cuda.Stream()
+            with torch.cuda.stream(self.stream):
+                self.nat = {s: _NativeSlab(slab_arrays(ga, self.slabs[s]), self.slabs[s], self.L,
+                                           self.S) for s in comm.local}
+            # one CUDA graph per sharded step when every slab is in this process
+            self.graph = (comm.world == 1) if graph is None else bool(graph)
+            self._graphs = {}
             # the composed applies are only needed for a warm start's r = rhs - Delta x0
             self.ops = {s: _WarmStartOps(self.nat[s]) for s in comm.local}
         else:
@@ -378,6 +384,20 @@ class SlabPcg:
             raise ValueError("need at least one step")
         start = time.perf_counter()
         rv = rv.to(self.device)
+        if self.native:
+            cur = torch.cuda.current_stream()
+            self.stream.wait_stream(cur)
+            try:
+                with torch.cuda.stream(self.stream):
+                    return self._solve_body(rv, x0, tol, max_steps, host, start, callback)
+            finally:      # results (and the iterate of MaxIterationsExceeded) are on that stream
+                cur.wait_stream(self.stream)
+        return self._solve_body(rv, x0, tol, max_steps, host, start, callback)
+
+    def _solve_body(self, rv, x0, tol, max_steps, host, start, callback):
+        import torch
+
+        dim = self.dim
         own = {s: self.slabs[s].own for s in self.comm.local}
         loc = self.comm.local
         r = self._scatter(rv)
@@ -515,10 +535,21 @@ class SlabPcg:
         step, done = ctypes.c_int64(), ctypes.c_int32()
         conv, brk = ctypes.c_int32(), ctypes.c_int32()
         issued, chunk = 0, 1 if callback is not None else 2
+        use_graph = self.graph and callback is None
         while True:
             todo = min(chunk, max_steps - issued)
             for _ in range(todo):
-                self._nstep(S)
+                g = self._graphs.get(S) if use_graph else None
+                if g is not None:
+                    g.replay()
+                else:
+                    self._nstep(S)      # eager (also warms the launch caches before capture)
+                    if use_graph:
+                        g = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(g, stream=self.stream,
+                                              capture_error_mode="thread_local"):
+                            self._nstep(S)
+                        self._graphs[S] = g
             issued += todo
             first.call("gq_slab_status", ctypes.byref(step), ctypes.byref(done),
                        ctypes.byref(conv), ctypes.byref(brk))

@@ -238,8 +238,9 @@ def test_gpu_slabs_match_single_context():
         x1, r1 = pcg_solve(op, pc, ga.offset, tol=1e-300, max_steps=25)
     except MaxIterationsExceeded as exc:
         x1, r1 = exc.iterate, exc.report
-    for native in (True, False):
-        solver = SlabPcg(ga, comm=SlabComm(4, device=torch.device("cuda")), native=native)
+    for native, graph in ((True, True), (True, False), (False, None)):
+        solver = SlabPcg(ga, comm=SlabComm(4, device=torch.device("cuda")), native=native,
+                         graph=graph)
         try:
             x2, r2 = solver.solve(ga.offset, tol=1e-300, max_steps=25)
         except MaxIterationsExceeded as exc:
@@ -367,6 +368,10 @@ def test_gpu_native_slabs_headline_size():
     solver = SlabPcg(ga, comm=SlabComm(4, device=torch.device("cuda")))
     with pytest.raises(MaxIterationsExceeded) as e2:
         solver.solve(rhs, tol=1e-300, max_steps=6)
+    # the captured step graph is reused by the next solve on the same solver
+    with pytest.raises(MaxIterationsExceeded) as e3:
+        solver.solve(rhs, tol=1e-300, max_steps=6)
+    assert torch.equal(e3.value.iterate, e2.value.iterate)
     x2 = e2.value.iterate.cpu().numpy()
     h2 = np.array(e2.value.report.residual_inf_history)
     assert rel_err(x2, x1) < 1e-9
