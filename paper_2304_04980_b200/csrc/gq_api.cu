@@ -402,7 +402,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       CKB(cudaStreamSynchronize(c->stream));
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
-      if (!grp.empty()) {
+      if (!grp.empty() && chain2c_enabled()) {   // opt-in CTA-shared factor sweeps
         bool ok0 = false;
         CKB(cta_check_stage0(g, pcls[0], c->cff, c->cfb, ok0, c->stream));
         if (ok0) {
@@ -1175,7 +1175,7 @@ extern "C" int gq_slab_phase(gq_ctx* c, int32_t kind, int32_t s) {
     case GQ_SLAB_DELTA:        // y = Delta d, partial y.d over the owned stages
       if ((rc = enqueue_delta_step(c))) return rc;
       CK(launch_slab_ydelta(c->g, c->slab_t0, c->slab_t1, c->y, c->d, c->partials, c->st,
-                            c->vblocks, c->stream));
+                            std::min(c->vblocks, c->sm_count), c->stream));
       break;
     case GQ_SLAB_UPDATE:       // alpha; x += alpha d; r -= alpha y with the partial max|r|
       CK(launch_slab_scalar(0, c->st, c->stream));
