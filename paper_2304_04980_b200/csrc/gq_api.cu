@@ -1119,7 +1119,18 @@ extern "C" int gq_slab_enable(gq_ctx* c, int32_t own_lo, int32_t own_hi) {
   c->slab = true;
   c->slab_t0 = own_lo > 0 ? 0 : -1;
   c->slab_t1 = own_hi < T1 ? T1 - 1 : -1;
+  // Delta leaves the halo rows of y unwritten (zero from gq_slab_start on), so y.d, r,
+  // max|r| and q.r cover the owned stages only
+  c->g.hx0 = c->slab_t0;
+  c->g.hx1 = c->slab_t1;
   c->fuse_x = false;
+  c->dfac = false;   // the opt-in Delta variants have no halo mask
+  c->st2 = false;
+  for (auto& ge : c->gexec)
+    if (ge) {
+      cudaGraphExecDestroy(ge);
+      ge = nullptr;
+    }
   c->started = false;
   return GQ_OK;
 }
@@ -1144,6 +1155,8 @@ extern "C" int gq_slab_start(gq_ctx* c, const double* r0, const double* x0, int3
   // r0 is the slab's initial residual (rhs, or rhs - Delta x0 formed by the caller), zero on
   // the halo stages; x0 only seeds the iterate
   if ((rc = import_vec(c, r0, c->r))) return rc;
+  for (int t : {c->slab_t0, c->slab_t1})
+    if (t >= 0) CK(launch_stage_zero(c->g, t, c->y, c->sm_count, c->stream));
   if (x0) {
     if ((rc = import_vec(c, x0, c->x))) return rc;
   } else {
@@ -1174,8 +1187,6 @@ extern "C" int gq_slab_phase(gq_ctx* c, int32_t kind, int32_t s) {
       break;
     case GQ_SLAB_DELTA:        // y = Delta d, partial y.d over the owned stages
       if ((rc = enqueue_delta_step(c))) return rc;
-      CK(launch_slab_ydelta(c->g, c->slab_t0, c->slab_t1, c->y, c->d, c->partials, c->st,
-                            std::min(c->vblocks, c->sm_count), c->stream));
       break;
     case GQ_SLAB_UPDATE:       // alpha; x += alpha d; r -= alpha y with the partial max|r|
       CK(launch_slab_scalar(0, c->st, c->stream));

@@ -45,7 +45,13 @@ struct Geo {
   int V, nb;          // column pairs, 2-row blocks per pair chain
   long long nk;       // K*N
   long long dim;      // K*N*n*T1
+  int hx0 = -1, hx1 = -1;   // stage-slab halo stages: Delta leaves them unwritten (-1: none)
 };
+
+// Delta output rows a slab owns (every row outside stage-slab mode)
+__host__ __device__ __forceinline__ bool slab_owned(const Geo& g, int t) {
+  return t != g.hx0 && t != g.hx1;
+}
 
 struct Ops {
   const double* psi;   // [npc][N][K][13][n][n]   Psi_t(a, a+off13[o])

@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(128) k_stencil3(Geo g, FastOps fo, const doubl
   }
   const int t = chunk * kHaloChunk + lane - 1;
   const bool tv = active && t >= 0 && t < g.T1;
-  const bool useful = tv && lane >= 1 && lane <= kHaloChunk;
+  const bool useful = tv && lane >= 1 && lane <= kHaloChunk &&
+                      (MODE != kDelta || slab_owned(g, t));
   const unsigned vmask = __ballot_sync(0xffffffffu, tv);
   const int pc = tv ? fo.psi_cls[t] : 0;
   const int cA = __shfl_sync(0xffffffffu, pc, first_lane(vmask));

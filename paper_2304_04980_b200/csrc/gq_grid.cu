@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __
   const int K = g.K;
   const int t = chunk * kHaloChunk + lane - 1;
   const bool tv = t >= 0 && t < g.T1;
-  const bool useful = tv && lane >= 1 && lane <= kHaloChunk;
+  const bool useful = tv && lane >= 1 && lane <= kHaloChunk &&
+                      (MODE != kDelta || slab_owned(g, t));
   const unsigned vmask = __ballot_sync(0xffffffffu, tv);
   const int pc = tv ? fo.psi_cls[t] : 0;
   const int cA = __shfl_sync(0xffffffffu, pc, vmask ? __ffs(vmask) - 1 : 0);

@@ -6,9 +6,9 @@
 // turn the slab-local decisions of the step kernels into global ones once the host has
 // reduced the partial scalars over all slabs (pcg.py:100-131):
 //
-//   k_slab_ydelta  after Delta: y.d over the halo stages is subtracted from the partial
-//                  curvature and y is zeroed there, so r (and with it max|r| and q.r) stays
-//                  zero on the halo stages for the whole solve
+// Delta itself leaves the halo rows of y unwritten in stage-slab mode (Geo::hx0/hx1); they
+// are zeroed once at the start (k_stage_zero), so y.d covers the owned stages only and r --
+// with it max|r| and q.r -- stays zero on the halo stages for the whole solve.
 //   k_slab_alpha   after the curvature sum: breakdown test and alpha = mu / c
 //   k_slab_conv    after the max|r| reduction: history entry and convergence test
 //   k_slab_savemu / k_slab_beta   around the q.r sum: beta = mu' / mu
@@ -19,28 +19,6 @@
 #include "gq_internal.h"
 
 namespace gq {
-
-__global__ void __launch_bounds__(256) k_slab_ydelta(Geo g, int t0, int t1, double* __restrict__ y,
-                                                     const double* __restrict__ d,
-                                                     double* partials, PcgState* st) {
-  if (st->skip) return;   // the step did not run (budget or an earlier stop)
-  const long long per = g.nk * g.n;
-  const int nh = (t0 >= 0) + (t1 >= 0);
-  double acc = 0.0;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < per * nh;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int h = (int)(e / per);
-    const long long w = e - h * per;
-    const int t = (h == 0 && t0 >= 0) ? t0 : t1;
-    const long long node = w / g.n;
-    const long long o = (node * g.T1 + t) * g.n + (w - node * g.n);
-    acc = fma(y[o], d[o], acc);
-    y[o] = 0.0;
-  }
-  double tot;
-  if (grid_reduce<false>(acc, partials, &st->counter[3], tot) && threadIdx.x == 0)
-    st->curv = st->curv - tot;
-}
 
 __global__ void k_slab_alpha(PcgState* st) {
   if (st->skip) return;
@@ -88,6 +66,15 @@ __global__ void __launch_bounds__(256) k_stage_pack(Geo g, int t, const double* 
   }
 }
 
+__global__ void __launch_bounds__(256) k_stage_zero(Geo g, int t, double* __restrict__ v) {
+  const long long per = g.nk * g.n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < per;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long node = e / g.n;
+    v[(node * g.T1 + t) * g.n + (e - node * g.n)] = 0.0;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_stage_unpack(Geo g, int t, const double* __restrict__ buf,
                                                       double* __restrict__ v) {
   const long long per = g.nk * g.n;
@@ -103,14 +90,6 @@ static unsigned stage_blocks(const Geo& g, int sm_count) {
   return (unsigned)std::max(1LL, std::min<long long>((per + 255) / 256, 4LL * sm_count));
 }
 
-cudaError_t launch_slab_ydelta(const Geo& g, int t0, int t1, double* y, const double* d,
-                               double* partials, PcgState* st, int blocks, cudaStream_t s) {
-  if (t0 < 0 && t1 < 0) return cudaSuccess;
-  // `blocks` partials fit the context's partials buffer (the vector-kernel grid)
-  k_slab_ydelta<<<(unsigned)blocks, 256, 0, s>>>(g, t0, t1, y, d, partials, st);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_slab_scalar(int which, PcgState* st, cudaStream_t s) {
   switch (which) {
     case 0: k_slab_alpha<<<1, 1, 0, s>>>(st); break;
@@ -124,6 +103,11 @@ cudaError_t launch_slab_scalar(int which, PcgState* st, cudaStream_t s) {
 cudaError_t launch_stage_pack(const Geo& g, int t, const double* v, double* buf, int sm_count,
                               cudaStream_t s) {
   k_stage_pack<<<stage_blocks(g, sm_count), 256, 0, s>>>(g, t, v, buf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_zero(const Geo& g, int t, double* v, int sm_count, cudaStream_t s) {
+  k_stage_zero<<<stage_blocks(g, sm_count), 256, 0, s>>>(g, t, v);
   return cudaGetLastError();
 }
 

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(32) k_st8(Geo g, Ops op, const int4* __restric
         out.x = rv.x + ((0.0 - e[0].x) - e[1].x);
         out.y = rv.y + ((0.0 - e[0].y) - e[1].y);
       }
-      if (tv) {
+      if (tv && (MODE != kDelta || slab_owned(g, t))) {
         *reinterpret_cast<double2*>(y + (long long)j * cs + (long long)i * rs + (long long)t * NS + 2 * qd) = out;
         if (MODE == kDelta && dotmode != kDotNone) {
           dot = fma(out.x, xself.x, dot);

@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(256) k_stencil(Geo g, Ops op, const double* __
   }
   const int t = chunk * CH + lane - (HALO ? 1 : 0);
   const bool tv = active && t >= 0 && t < g.T1;
-  const bool useful = tv && (!HALO || (lane >= 1 && lane <= kHaloChunk));
+  const bool useful = tv && (!HALO || (lane >= 1 && lane <= kHaloChunk)) &&
+                      (MODE != kDelta || slab_owned(g, t));
   const int pc = tv ? op.psi_cls[t] : 0;
   const int xce = (tv && t < g.T) ? op.xi_cls[t] : -1;      // e_t uses Xi_t
   const int xcf = (tv && t >= 1) ? op.xi_cls[t - 1] : -1;   // f_t uses Xi_{t-1}
