@@ -170,6 +170,13 @@ class SlabComm:
         self.n = n_slabs
         self.device = device if device is not None else torch.device("cpu")
         self.exchanges = 0
+        # gloo carries host tensors only: the native driver stages its device halos and
+        # scalars through the host (the multi-process GPU test; NCCL takes device buffers)
+        self.host_staged = False
+        if world > 1:
+            import torch.distributed as dist
+
+            self.host_staged = dist.get_backend(group) == "gloo"
 
     @classmethod
     def from_env(cls, n_slabs: int, group=None, device=None):
@@ -183,10 +190,11 @@ class SlabComm:
         """Fill every halo stage of ``vecs`` (slab -> local vector) from the neighbour's
         owned boundary stage.  Reads touch owned stages only and writes halo stages only,
         so the in-process copies need no ordering."""
+        import torch
         import torch.distributed as dist
 
         self.exchanges += 1
-        reqs = []
+        reqs, staged = [], []
         for s in self.local:
             sl = slabs[s]
             for nb, mine, theirs in ((s - 1, sl.lo - 1, sl.lo), (s + 1, sl.hi, sl.hi - 1)):
@@ -197,12 +205,17 @@ class SlabComm:
                     halo.copy_(vecs[nb][slabs[nb].stage(mine)])
                 else:
                     peer = self.owner[nb]
-                    reqs.append(dist.P2POp(dist.isend, vecs[s][sl.stage(theirs)], peer,
-                                           group=self.group))
-                    reqs.append(dist.P2POp(dist.irecv, halo, peer, group=self.group))
+                    snd, rcv = vecs[s][sl.stage(theirs)], halo
+                    if self.host_staged and halo.device.type != "cpu":
+                        snd, rcv = snd.cpu(), torch.empty_like(halo, device="cpu")
+                        staged.append((halo, rcv))
+                    reqs.append(dist.P2POp(dist.isend, snd, peer, group=self.group))
+                    reqs.append(dist.P2POp(dist.irecv, rcv, peer, group=self.group))
         # one NCCL group for all sends and receives: both directions in flight together
         for r in (dist.batch_isend_irecv(reqs) if reqs else []):
             r.wait()
+        for halo, rcv in staged:
+            halo.copy_(rcv)
 
     def _reduce(self, partials, op):
         import torch
@@ -448,6 +461,7 @@ class SlabPcg:
     # -- native stage-slab mode ------------------------------------------------------------
     def _nexchange(self, which):
         """Halo exchange of a device work vector (gq_slab_pack / NCCL or copy / unpack)."""
+        import torch
         import torch.distributed as dist
 
         comm, nat, slabs = self.comm, self.nat, self.slabs
@@ -468,12 +482,17 @@ class SlabPcg:
                     nat[s].call("gq_slab_unpack", which, halo_t, ctypes.c_void_p(src.data_ptr()))
                 else:
                     peer = comm.owner[nb]
-                    reqs.append(dist.P2POp(dist.isend, nat[s].send[side], peer, group=comm.group))
-                    reqs.append(dist.P2POp(dist.irecv, nat[s].recv[side], peer, group=comm.group))
-                    later.append((s, side, halo_t))
+                    snd, rcv = nat[s].send[side], nat[s].recv[side]
+                    if comm.host_staged:     # gloo moves host tensors only
+                        snd, rcv = snd.cpu(), torch.empty_like(rcv, device="cpu")
+                    reqs.append(dist.P2POp(dist.isend, snd, peer, group=comm.group))
+                    reqs.append(dist.P2POp(dist.irecv, rcv, peer, group=comm.group))
+                    later.append((s, side, halo_t, rcv))
         for q in (dist.batch_isend_irecv(reqs) if reqs else []):
             q.wait()
-        for s, side, halo_t in later:
+        for s, side, halo_t, rcv in later:
+            if rcv.device.type == "cpu":
+                nat[s].recv[side].copy_(rcv)
             nat[s].call("gq_slab_unpack", which, halo_t, ctypes.c_void_p(nat[s].recv[side].data_ptr()))
 
     def _nreduce(self, which, op):
@@ -489,8 +508,11 @@ class SlabPcg:
         for v in vals[1:]:
             tot = tot + v if op == "sum" else torch.maximum(tot, v)
         if self.comm.world > 1:
-            dist.all_reduce(tot, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX,
+            buf = tot.cpu() if self.comm.host_staged else tot
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX,
                             group=self.comm.group)
+            if buf is not tot:
+                tot.copy_(buf)
         for v in vals:
             if v is not tot:
                 v.copy_(tot)

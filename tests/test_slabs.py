@@ -376,3 +376,45 @@ def test_gpu_native_slabs_headline_size():
     h2 = np.array(e2.value.report.residual_inf_history)
     assert rel_err(x2, x1) < 1e-9
     assert np.all(np.abs(h2 - h1) <= 1e-9 * h1 + 1e-14 * h1[0])
+
+
+def _gpu_gloo_worker(rank, ws, port, name, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        ga, rec = load_golden(name)
+        solver = SlabPcg(ga, inner_sweeps=rec["L"], outer_sweeps=rec["S"],
+                         comm=SlabComm.from_env(2 * ws, device=torch.device("cuda")),
+                         precondition=bool(rec["precond"]))
+        assert solver.native and not solver.graph
+        try:
+            x, rep = solver.solve(ga.offset, tol=rec["tol"], max_steps=rec["max_steps"],
+                                  x0=rec.get("x0"))
+        except MaxIterationsExceeded as exc:
+            x, rep = exc.iterate, exc.report
+        out[rank] = (np.asarray(x).tolist(), list(rep.residual_inf_history), rep.steps,
+                     rep.converged)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["config1", "time_varying", "warm", "config5r", "cg"])
+def test_gpu_native_slabs_two_processes(name):
+    """The native driver across processes: 2 processes x 2 slabs on the one GPU, halos and
+    scalars through gloo (host-staged; the kernels never wait on each other, only the host
+    does).  Same golden parity as everywhere; both processes return the same solve."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().list([None, None])
+    mp.start_processes(_gpu_gloo_worker, args=(2, _free_port(), name, out), nprocs=2,
+                       join=True, start_method="spawn")
+    ga, rec = load_golden(name)
+    x0, h0, s0, c0 = out[0]
+    x1, h1, s1, c1 = out[1]
+    assert x0 == x1 and h0 == h1 and s0 == s1 and c0 == c1
+    check_run(name, rec, np.array(x0), h0, s0, c0, {})
