@@ -11,6 +11,7 @@ from .problem import (BoundaryData, ConstSeq, GridArrays, GridLayout, GridLQProb
                       SubsystemData, arrays_from_problem, arrays_to_problem, load_problem,
                       problem_from_dict, problem_to_dict, save_problem, validate_arrays)
 from .recovery import TrajectorySolution, kkt_residual, recover_solution
+from .slab import SlabComm, SlabPcg, pcg_solve_slabs
 from .solver import (COUNT_KEYS, GpuNestedJacobiPreconditioner, GpuSchurOperator, SolveReport,
                      apply_delta, build_schur, cg_solve, nbjm_solve, pcg_solve)
 
@@ -25,6 +26,7 @@ __all__ = [
     "SubsystemData", "apply_delta", "arrays_from_problem", "arrays_to_problem", "build_schur",
     "cg_solve", "nbjm_solve", "pcg_solve", "validate_arrays", "TrajectorySolution", "recover_solution",
     "kkt_residual", "load_problem", "save_problem", "problem_from_dict", "problem_to_dict",
+    "SlabComm", "SlabPcg", "pcg_solve_slabs",
 ]
 
 __version__ = "0.1.0"
