@@ -387,8 +387,11 @@ cudaError_t launch_grid(const Geo& g, const FastOps& fo, int mode, const double*
     if (p == 4) return grid_launch<kDelta, 4>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
     return grid_launch<kDelta, 3>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
   }
-  if (p == 2) return grid_launch<kOuterRhs, 2>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
-  if (p == 4) return grid_launch<kOuterRhs, 4>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
+  const int po = genv("GQ_GRID_PO", p);   // outer-rhs ring depth (default: as Delta)
+  if (po == 1) return grid_launch<kOuterRhs, 1>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
+  if (po == 2) return grid_launch<kOuterRhs, 2>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
+  if (po == 4) return grid_launch<kOuterRhs, 4>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
+  if (po == 6) return grid_launch<kOuterRhs, 6>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
   return grid_launch<kOuterRhs, 3>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
 }
 

@@ -10,11 +10,18 @@ rhs = torch.tensor(ga.offset, device="cuda", dtype=torch.float64)
 variants = sys.argv[1:] or [""]
 res = {v: [] for v in variants}
 ops = {}
-for var in variants:
+
+
+def set_env(var):
+    # the library reads GQ_* both at setup and when it captures the step graph (first run)
     env = dict(kv.split("=") for kv in var.split(",") if kv)
     for k in list(os.environ):
         if k.startswith("GQ_"): os.environ.pop(k)
     for k, val in env.items(): os.environ["GQ_" + k] = val
+
+
+for var in variants:
+    set_env(var)
     op = GpuSchurOperator(ga, 2, 2)
     pc = GpuNestedJacobiPreconditioner(op, 2, 2)
     st = torch.cuda.Stream()
@@ -23,6 +30,7 @@ for var in variants:
 steps, conv = ctypes.c_int64(), ctypes.c_int32()
 for rnd in range(int(os.environ.get("ROUNDS", "3"))):
     for var in variants:
+        set_env(var)
         op, pc, st = ops[var]
         ctx = op._ctx; lib = ctx.lib
         _lib.check(lib.gq_pcg_start(ctx.h, ctypes.c_void_p(rhs.data_ptr()), None, 1))
