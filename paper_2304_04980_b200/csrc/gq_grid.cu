@@ -69,11 +69,12 @@ __device__ bool warp_grid_sum2(double v, double* partials, unsigned int* counter
 }
 
 template <int MODE, int P>
-__global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __restrict__ x,
-                                             const double* __restrict__ rin,
-                                             double* __restrict__ y, int nchunk, int nstrip,
-                                             int rows, int n_items, double* partials,
-                                             PcgState* st, int dotmode) {
+__device__ __forceinline__ void grid_body(const Geo& g, const FastOps& fo,
+                                          const double* __restrict__ x,
+                                          const double* __restrict__ rin,
+                                          double* __restrict__ y, int nchunk, int nstrip,
+                                          int rows, int n_items, double* partials,
+                                          PcgState* st, int dotmode) {
   using C = Gd<MODE>;
   constexpr int R = P + 1, REC = C::REC, OPS = C::OPS;
   extern __shared__ __align__(16) double ring[];
@@ -323,6 +324,25 @@ __global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __
   }
 }
 
+template <int MODE, int P>
+__global__ void __launch_bounds__(32) k_grid(Geo g, FastOps fo, const double* __restrict__ x,
+                                             const double* __restrict__ rin,
+                                             double* __restrict__ y, int nchunk, int nstrip,
+                                             int rows, int n_items, double* partials,
+                                             PcgState* st, int dotmode) {
+  grid_body<MODE, P>(g, fo, x, rin, y, nchunk, nstrip, rows, n_items, partials, st, dotmode);
+}
+
+// register-capped build (GQ_GRID_MAXR, default 128 for Delta): more resident warps per SM
+template <int MODE, int P, int MAXR>
+__global__ void __maxnreg__(MAXR) k_grid_r(Geo g, FastOps fo, const double* __restrict__ x,
+                                           const double* __restrict__ rin,
+                                           double* __restrict__ y, int nchunk, int nstrip,
+                                           int rows, int n_items, double* partials,
+                                           PcgState* st, int dotmode) {
+  grid_body<MODE, P>(g, fo, x, rin, y, nchunk, nstrip, rows, n_items, partials, st, dotmode);
+}
+
 // ---- host side -----------------------------------------------------------------------------
 
 static int genv(const char* name, int dflt) {
@@ -342,14 +362,18 @@ GridShape grid_shape(const Geo& g, int sm_count) {
   return sh;
 }
 
-template <int MODE, int P>
+template <int MODE, int P, int MAXR = 0>
 static cudaError_t grid_launch(const Geo& g, const FastOps& fo, const double* x, const double* rin,
                                double* y, const GridShape& ub, double* partials, PcgState* st,
                                int dotmode, cudaStream_t s) {
   constexpr size_t smem = (size_t)(P + 1) * Gd<MODE>::SLOT * sizeof(double);
   static int cache[64] = {0};
   int per_sm = 1;
-  cudaError_t e = kernel_occupancy(k_grid<MODE, P>, 32, smem, cache, per_sm);
+  cudaError_t e;
+  if constexpr (MAXR > 0)
+    e = kernel_occupancy(k_grid_r<MODE, P, MAXR>, 32, smem, cache, per_sm);
+  else
+    e = kernel_occupancy(k_grid<MODE, P>, 32, smem, cache, per_sm);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -373,8 +397,12 @@ static cudaError_t grid_launch(const Geo& g, const FastOps& fo, const double* x,
   const int nstrip = (g.K + rows - 1) / rows;
   const int n_items = (int)(cols * nstrip);
   const int blocks = (int)std::min<long long>({(long long)n_items, slots, (long long)ub.blocks});
-  k_grid<MODE, P><<<blocks, 32, smem, s>>>(g, fo, x, rin, y, ub.nchunk, nstrip, rows, n_items,
-                                           partials, st, dotmode);
+  if constexpr (MAXR > 0)
+    k_grid_r<MODE, P, MAXR><<<blocks, 32, smem, s>>>(
+        g, fo, x, rin, y, ub.nchunk, nstrip, rows, n_items, partials, st, dotmode);
+  else
+    k_grid<MODE, P><<<blocks, 32, smem, s>>>(g, fo, x, rin, y, ub.nchunk, nstrip, rows, n_items,
+                                             partials, st, dotmode);
   return cudaGetLastError();
 }
 
@@ -382,6 +410,17 @@ cudaError_t launch_grid(const Geo& g, const FastOps& fo, int mode, const double*
                         const double* rin, double* y, const GridShape& sh, double* partials,
                         PcgState* st, int dotmode, cudaStream_t s) {
   const int p = genv("GQ_GRID_P", 2);
+  // Delta register cap: 128 (from 136) fits 16 resident warps per SM; measured 592.6 -> 600.1
+  // steps/s (tools/steptime.py, bench.py).  GQ_GRID_MAXR=0 restores the uncapped build.
+  const int maxr = genv("GQ_GRID_MAXR", 128);
+  if (mode == kDelta && p == 2 && maxr == 128)
+    return grid_launch<kDelta, 2, 128>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
+  if (mode == kDelta && p == 2 && maxr == 120)
+    return grid_launch<kDelta, 2, 120>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
+  if (mode == kDelta && p == 2 && maxr == 112)
+    return grid_launch<kDelta, 2, 112>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
+  if (mode == kDelta && p == 2 && maxr == 96)
+    return grid_launch<kDelta, 2, 96>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
   if (mode == kDelta) {
     if (p == 2) return grid_launch<kDelta, 2>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
     if (p == 4) return grid_launch<kDelta, 4>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
