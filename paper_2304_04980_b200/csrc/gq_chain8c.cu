@@ -51,7 +51,7 @@ struct C8 {
 }  // namespace
 
 template <bool INNER, int W>
-__global__ void __launch_bounds__(32 * W, 1) k_chain8c(Geo g, ChainOps co,
+__global__ void __launch_bounds__(32 * W, INNER ? 1 : 2) k_chain8c(Geo g, ChainOps co,
                                                        const double* __restrict__ rhs,
                                                        const double* __restrict__ th, double* out,
                                                        const double* __restrict__ rdot,

@@ -28,11 +28,11 @@ __device__ __forceinline__ double2 ld16(const double* p) {
 }  // namespace
 
 template <int MODE>
-__global__ void __launch_bounds__(32) k_st8(Geo g, Ops op, const int4* __restrict__ seg,
-                                            int nseg, const double* __restrict__ x,
-                                            const double* __restrict__ rin,
-                                            double* __restrict__ y, double* partials,
-                                            PcgState* st, int dotmode) {
+__device__ __forceinline__ void st8_body(const Geo& g, const Ops& op, const int4* __restrict__ seg,
+                                        int nseg, const double* __restrict__ x,
+                                        const double* __restrict__ rin,
+                                        double* __restrict__ y, double* partials,
+                                        PcgState* st, int dotmode) {
   constexpr int NS = 8, B2 = 64;
   if (st != nullptr) {
     if (dotmode == kDotStep) {
@@ -150,6 +150,26 @@ __global__ void __launch_bounds__(32) k_st8(Geo g, Ops op, const int4* __restric
   }
 }
 
+// Delta: uncapped (102 registers; every cap tried was slower: 96 -> 3.80 ms, 80 -> 3.17 ms
+// vs 2.52 ms at config 5).  Outer rhs: capped at 64 registers (from 66 at the default
+// bound, 122 at a looser one), 1.078 -> 0.997 ms.
+template <int MODE>
+__global__ void __launch_bounds__(32) k_st8(Geo g, Ops op, const int4* __restrict__ seg,
+                                            int nseg, const double* __restrict__ x,
+                                            const double* __restrict__ rin,
+                                            double* __restrict__ y, double* partials,
+                                            PcgState* st, int dotmode) {
+  st8_body<MODE>(g, op, seg, nseg, x, rin, y, partials, st, dotmode);
+}
+
+__global__ void __launch_bounds__(32, 32) k_st8_rhs(Geo g, Ops op, const int4* __restrict__ seg,
+                                                   int nseg, const double* __restrict__ x,
+                                                   const double* __restrict__ rin,
+                                                   double* __restrict__ y, double* partials,
+                                                   PcgState* st, int dotmode) {
+  st8_body<kOuterRhs>(g, op, seg, nseg, x, rin, y, partials, st, dotmode);
+}
+
 static int s8env(const char* name, int dflt) {
   const char* s = getenv(name);
   return (s && *s) ? atoi(s) : dflt;
@@ -165,10 +185,14 @@ static cudaError_t st8_launch(const Geo& g, const Ops& op, const int4* seg, int 
                               double* partials, PcgState* st, int dotmode, cudaStream_t s) {
   static int cache[64] = {0};
   int per_sm = 1;
-  cudaError_t e = kernel_occupancy(k_st8<MODE>, 32, 0, cache, per_sm);
+  cudaError_t e = MODE == kDelta ? kernel_occupancy(k_st8<kDelta>, 32, 0, cache, per_sm)
+                                 : kernel_occupancy(k_st8_rhs, 32, 0, cache, per_sm);
   if (e != cudaSuccess) return e;
   const long long blocks = std::min<long long>(g.nk, (long long)per_sm * sm_count);
-  k_st8<MODE><<<(unsigned)blocks, 32, 0, s>>>(g, op, seg, nseg, x, rin, y, partials, st, dotmode);
+  if (MODE == kDelta)
+    k_st8<kDelta><<<(unsigned)blocks, 32, 0, s>>>(g, op, seg, nseg, x, rin, y, partials, st, dotmode);
+  else
+    k_st8_rhs<<<(unsigned)blocks, 32, 0, s>>>(g, op, seg, nseg, x, rin, y, partials, st, dotmode);
   return cudaGetLastError();
 }
 
