@@ -1190,7 +1190,12 @@ extern "C" int gq_slab_phase(gq_ctx* c, int32_t kind, int32_t s) {
       break;
     case GQ_SLAB_UPDATE:       // alpha; x += alpha d; r -= alpha y with the partial max|r|
       CK(launch_slab_scalar(0, c->st, c->stream));
-      CK(launch_update_x(c->g, c->x, c->d, c->vblocks, c->st, c->stream));
+      // x += alpha d on the side stream, joined before d is overwritten (DIRECTION), as in
+      // the one-context step graph
+      CK(cudaEventRecord(c->ev_fork, c->stream));
+      CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+      CK(launch_update_x(c->g, c->x, c->d, c->vblocks, c->st, c->side));
+      CK(cudaEventRecord(c->ev_join, c->side));
       if (fr)
         rc = enqueue_outer(c, 0, 0, 1, c->r, c->q, c->st, kDotStep, nullptr, none, c->y);
       else
@@ -1209,6 +1214,7 @@ extern "C" int gq_slab_phase(gq_ctx* c, int32_t kind, int32_t s) {
       break;
     }
     case GQ_SLAB_DIRECTION:    // beta; d = q + beta d
+      CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
       CK(launch_slab_scalar(3, c->st, c->stream));
       CK(launch_dirupdate(c->g, c->d, pc ? c->q : c->r, c->vblocks, c->st, c->stream));
       break;
