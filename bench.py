@@ -376,6 +376,27 @@ def run_slabs(args, ws, rank, local):
         ms_wk = run(W + K)
     ms = max(ms_wk - ms_w, 1e-9)
     sl = solver.slabs
+
+    # end to end through the public API: host numpy rhs in, host x out (gathered), K steps
+    rhs_host = torch.from_numpy(ga.offset.copy()).pin_memory().numpy()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    try:
+        solver.solve(rhs_host, tol=1e-300, max_steps=K)
+    except MaxIterationsExceeded as exc:
+        assert exc.iterate.shape == (ga.dim,)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, dev, ws)
+
+    # kernels of ours per step and slab: the step kernels of the one-context graph, the four
+    # scalar fix-ups, and a pack + unpack per halo stage per exchange (S exchanges per step)
+    lib = solver.nat[solver.comm.local[0]].ctx.lib
+    per_slab = lib.gq_launches_per_step(solver.nat[solver.comm.local[0]].ctx.h) + 4
+    halos = sum((x.lo > 0) + (x.hi < ga.T + 1) for x in sl) / len(sl)
+    launches = int(round(K * (per_slab + 2 * halos * args.S)))
     return {
         "metric": METRIC, "value": K / (ms * 1e-3), "unit": UNIT, "n_gpus": ws, "steps": K,
         "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
@@ -389,6 +410,13 @@ def run_slabs(args, ws, rank, local):
                    "timing": "t(W+K steps) - t(W steps), both from a fresh start",
                    "l2": "inputs larger than L2"},
         "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "e2e": {
+            "value": K / e2e_s, "unit": UNIT,
+            "h2d_bytes_per_step": 8 * ga.dim / K, "d2h_bytes_per_step": 8 * ga.dim / K,
+            "includes": "SlabPcg.solve on host numpy rhs: H2D + scatter, slab start and "
+                        "initial preconditioner, K steps, gather + D2H of x",
+        },
     }
 
 

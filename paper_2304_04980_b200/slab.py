@@ -387,8 +387,6 @@ class SlabPcg:
                              else rhs, dtype=torch.float64)
         if rv.dim() != 1 or rv.numel() != dim:
             raise DimensionMismatchError("right-hand side does not match operator dimension")
-        if not bool(torch.isfinite(rv).all()):
-            raise ValueError("right-hand side contains non-finite entries")
         if tol <= 0:
             raise ValueError("tolerance must be positive")
         if max_steps is None:
@@ -397,6 +395,8 @@ class SlabPcg:
             raise ValueError("need at least one step")
         start = time.perf_counter()
         rv = rv.to(self.device)
+        if not bool(torch.isfinite(rv).all()):     # pcg.py:65-66, checked where rv lives now
+            raise ValueError("right-hand side contains non-finite entries")
         if self.native:
             cur = torch.cuda.current_stream()
             self.stream.wait_stream(cur)
@@ -597,6 +597,19 @@ class SlabPcg:
         """Global x or r assembled from the slabs' owned stages."""
         import torch
 
+        if host and self.comm.world == 1:
+            # host result in one process: the library's staged export per slab (a direct
+            # device -> pageable copy of a 211 MB vector costs ~95 ms here)
+            out = np.empty(self.dim)
+            for s in self.comm.local:
+                sl = self.slabs[s]
+                if sl.local_dim == self.dim:
+                    self.nat[s].call("gq_pcg_read", which, ctypes.c_void_p(out.ctypes.data))
+                else:
+                    tmp = np.empty(sl.local_dim)
+                    self.nat[s].call("gq_pcg_read", which, ctypes.c_void_p(tmp.ctypes.data))
+                    out[sl.global_own] = tmp[sl.own]
+            return out
         vs = {}
         for s in self.comm.local:
             vs[s] = torch.empty(self.slabs[s].local_dim, dtype=torch.float64, device=self.device)
