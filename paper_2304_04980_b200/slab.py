@@ -558,9 +558,16 @@ class SlabPcg:
         conv, brk = ctypes.c_int32(), ctypes.c_int32()
         issued, chunk = 0, 1 if callback is not None else 2
         use_graph = self.graph and callback is None
+        # device timing of the steps after the first `time_from` (bench.py): CUDA events on
+        # the solver stream around exactly those steps
+        tf = getattr(self, "time_from", None)
+        ev = None
         while True:
             todo = min(chunk, max_steps - issued)
             for _ in range(todo):
+                if tf is not None and issued + _ == tf:
+                    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    ev[0].record()
                 g = self._graphs.get(S) if use_graph else None
                 if g is not None:
                     g.replay()
@@ -573,6 +580,8 @@ class SlabPcg:
                             self._nstep(S)
                         self._graphs[S] = g
             issued += todo
+            if ev is not None and issued >= max_steps:
+                ev[1].record()
             first.call("gq_slab_status", ctypes.byref(step), ctypes.byref(done),
                        ctypes.byref(conv), ctypes.byref(brk))
             if callback is not None and not brk.value and step.value == issued:
@@ -582,6 +591,9 @@ class SlabPcg:
                 break
             if callback is None:
                 chunk = min(chunk * 2, 64)
+        if ev is not None and issued >= max_steps:
+            ev[1].synchronize()
+            self.last_timed = (max_steps - tf, ev[0].elapsed_time(ev[1]))
         steps = int(step.value)
         hist = np.empty(steps)
         if steps:
