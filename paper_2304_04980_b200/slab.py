@@ -554,6 +554,16 @@ class SlabPcg:
         self._nreduce(_lib.GQ_SLAB_MU, "sum")
         self._nphase(_lib.GQ_SLAB_INIT_FINISH)
         first = self.nat[loc[0]]
+        # a host result: fault its pages in while the device iterates (as pcg_solve does)
+        xhost, toucher = None, None
+        if host and self.comm.world == 1 and callback is None:
+            import threading
+
+            from .solver import _touch_pages
+
+            xhost = np.empty(self.dim)
+            toucher = threading.Thread(target=_touch_pages, args=(xhost,), daemon=True)
+            toucher.start()
         step, done = ctypes.c_int64(), ctypes.c_int32()
         conv, brk = ctypes.c_int32(), ctypes.c_int32()
         issued, chunk = 0, 1 if callback is not None else 2
@@ -601,18 +611,21 @@ class SlabPcg:
         if brk.value:
             raise BreakdownError(f"non-positive curvature at step {steps + 1}; operator or "
                                  "preconditioner is not positive definite")
-        xg = self._nread(_lib.GQ_VEC_X, host)
+        if toucher is not None:
+            toucher.join()
+        xg = self._nread(_lib.GQ_VEC_X, host, out=xhost)
         converged = bool(conv.value)
         return self._finish(xg, hist.tolist(), steps, converged, tol, start, x0s is not None)
 
-    def _nread(self, which, host):
+    def _nread(self, which, host, out=None):
         """Global x or r assembled from the slabs' owned stages."""
         import torch
 
         if host and self.comm.world == 1:
             # host result in one process: the library's staged export per slab (a direct
             # device -> pageable copy of a 211 MB vector costs ~95 ms here)
-            out = np.empty(self.dim)
+            if out is None:
+                out = np.empty(self.dim)
             for s in self.comm.local:
                 sl = self.slabs[s]
                 if sl.local_dim == self.dim:
