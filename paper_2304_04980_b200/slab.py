@@ -296,8 +296,15 @@ class _NativeSlab:
 class SlabPcg:
     """PCGM over a stage-slab partition (``pcg.py:50-149`` control flow).
 
-    ``ops_factory(sub_arrays, inner_sweeps)`` builds a slab's local compute; the default is
-    ``DeviceSlabOps`` (the B200 path)."""
+    * ``native`` (default when no ``ops_factory`` is given): every slab's gq_ctx runs the
+      step kernels in stage-slab mode; ``graph`` (default: all slabs in this process)
+      replays the whole sharded step as one captured CUDA graph.
+    * composed (``native=False``): torch vector ops over per-slab applies;
+      ``ops_factory(sub_arrays, inner_sweeps)`` builds them (default ``DeviceSlabOps``; the
+      tests pass an oracle-backed factory).
+    * ``time_from`` (attribute, native only): when set to W, the next solve records CUDA
+      events around its steps W..max_steps-1 into ``last_timed = (steps, ms)`` (bench.py).
+    """
 
     def __init__(self, problem, slabs=None, inner_sweeps=2, outer_sweeps=2, comm=None,
                  ops_factory=None, precondition=True, native=None, graph=None):
