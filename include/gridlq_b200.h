@@ -110,8 +110,11 @@ int gq_pcg(gq_ctx* ctx, const double* rhs, const double* x0, double tol, int64_t
  * one halo stage per side (own_lo in {0, 1}, own_hi in {T, T+1} of the window).  A solve is
  *   gq_slab_start(r0 = the slab's initial residual, zero on halo stages; x0 or NULL)
  *   init:  for s < S: INIT_OUTER(s) [exchange DL(s%2) if s < S-1]; reduce MU (sum); INIT_FINISH
- *   step:  exchange D; DELTA; reduce CURV (sum); UPDATE; reduce RES (max);
- *          for s < S: OUTER(s) [exchange DL(s%2) if s < S-1]; reduce MU (sum); DIRECTION
+ *   step:  exchange D; DELTA; reduce CURV (sum); UPDATE;
+ *          for s < S: OUTER(s) [exchange DL(s%2) if s < S-1];
+ *          reduce RES (max) and MU (sum) -- one collective; DIRECTION
+ * (the max|r| kernels only record max|r| in stage-slab mode; DIRECTION decides convergence
+ * on the global value, so a converged step computes its q = P r for nothing)
  * (CG: S = 1).  "exchange v" = every slab packs its owned boundary stages of v
  * (gq_slab_pack) and unpacks the neighbours' into its halo stages (gq_slab_unpack); a halo
  * buffer holds K*N*n doubles in (column, row, state) order.  "reduce" = combine the device

@@ -1151,6 +1151,7 @@ extern "C" int gq_slab_start(gq_ctx* c, const double* r0, const double* x0, int3
   c->h_st->hist = c->hist;
   c->h_st->tol = tol;
   c->h_st->max_steps = max_steps;
+  c->h_st->defer = 1;   // convergence is decided on the global max|r| (DIRECTION phase)
   CK(cudaMemcpyAsync(c->st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
   // r0 is the slab's initial residual (rhs, or rhs - Delta x0 formed by the caller), zero on
   // the halo stages; x0 only seeds the iterate
@@ -1201,10 +1202,9 @@ extern "C" int gq_slab_phase(gq_ctx* c, int32_t kind, int32_t s) {
       else
         CK(launch_update_r(c->g, c->r, c->y, c->vblocks, c->partials, c->st, c->stream));
       break;
-    case GQ_SLAB_OUTER: {      // convergence test; outer sweep s of q = P r (+ partial q.r)
+    case GQ_SLAB_OUTER: {      // outer sweep s of q = P r (+ partial q.r in the last one)
       const int S = pc ? c->S : 1;
       if (s < 0 || s >= S) return fail(GQ_INVALID_ARG, "outer sweep index out of range");
-      if (s == 0) CK(launch_slab_scalar(1, c->st, c->stream));
       if (s == S - 1) CK(launch_slab_scalar(2, c->st, c->stream));
       if (pc)
         rc = enqueue_outer(c, s, (s == 0 && fr) ? 1 : 0, c->L, c->r, c->q, c->st, kDotStep,
@@ -1213,7 +1213,7 @@ extern "C" int gq_slab_phase(gq_ctx* c, int32_t kind, int32_t s) {
         CK(launch_dot(c->g, c->r, c->r, c->vblocks, c->partials, c->st, kDotStep, c->stream));
       break;
     }
-    case GQ_SLAB_DIRECTION:    // beta; d = q + beta d
+    case GQ_SLAB_DIRECTION:    // convergence test and beta; d = q + beta d
       CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
       CK(launch_slab_scalar(3, c->st, c->stream));
       CK(launch_dirupdate(c->g, c->d, pc ? c->q : c->r, c->vblocks, c->st, c->stream));

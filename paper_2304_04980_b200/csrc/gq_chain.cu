@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
       st->res = res;
       st->hist[st->step] = res;
       st->step += 1;
-      if (res < st->tol) {
+      if (res < st->tol && !st->defer) {
         st->converged = 1;
         st->done = 1;
       }

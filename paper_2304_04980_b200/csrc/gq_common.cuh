@@ -70,6 +70,8 @@ struct PcgState {
   long long step, max_steps;
   double* hist;
   int done, converged, breakdown;
+  int defer;        // stage-slab mode: max|r| kernels record the history but leave the
+                    // convergence decision to k_slab_conv_beta (after the global max)
   int skip;   // set by the first kernel of a step when the step budget is exhausted
   int nonfinite;   // set by the rhs check of gq_pcg_start
   unsigned int counter[4];

@@ -247,7 +247,7 @@ cudaError_t launch_to_internal(const Geo& g, const double* ref, double* dev, cud
 cudaError_t launch_to_reference(const Geo& g, const double* dev, double* ref, cudaStream_t s);
 
 // stage-slab mode (gq_slab.cu): halo-stage zeroing, scalar fix-ups after the host-side
-// reductions (which: 0 alpha, 1 convergence, 2 save mu, 3 beta), halo stage pack/unpack
+// reductions (which: 0 alpha, 2 save mu, 3 convergence + beta), halo stage pack/unpack
 cudaError_t launch_stage_zero(const Geo& g, int t, double* v, int sm_count, cudaStream_t s);
 cudaError_t launch_slab_scalar(int which, PcgState* st, cudaStream_t s);
 cudaError_t launch_stage_pack(const Geo& g, int t, const double* v, double* buf, int sm_count,

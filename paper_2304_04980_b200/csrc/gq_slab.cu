@@ -9,9 +9,12 @@
 // Delta itself leaves the halo rows of y unwritten in stage-slab mode (Geo::hx0/hx1); they
 // are zeroed once at the start (k_stage_zero), so y.d covers the owned stages only and r --
 // with it max|r| and q.r -- stays zero on the halo stages for the whole solve.
-//   k_slab_alpha   after the curvature sum: breakdown test and alpha = mu / c
-//   k_slab_conv    after the max|r| reduction: history entry and convergence test
-//   k_slab_savemu / k_slab_beta   around the q.r sum: beta = mu' / mu
+//   k_slab_alpha      after the curvature sum: breakdown test and alpha = mu / c
+//   k_slab_savemu     before the sweep that forms q.r: keep mu
+//   k_slab_conv_beta  after ONE reduction of (max|r|, q.r): history entry, convergence test
+//                     and beta = mu' / mu.  The max|r| kernels run with PcgState::defer, so
+//                     no slab stops on its own partial; a converged step computes q for
+//                     nothing, which changes no result.
 //   k_stage_pack / k_stage_unpack  one stage of a stage-inner vector <-> a contiguous halo
 //                  buffer in (column, row, state) order
 #include <algorithm>
@@ -33,27 +36,23 @@ __global__ void k_slab_alpha(PcgState* st) {
   }
 }
 
-__global__ void k_slab_conv(PcgState* st) {
-  if (st->skip || st->breakdown) return;
-  const double res = st->res;               // pcg.py:113-121, now the global max|r|
-  st->hist[st->step - 1] = res;
-  if (res < st->tol) {
-    st->converged = 1;
-    st->done = 1;
-  } else {
-    st->converged = 0;
-    st->done = 0;
-  }
-}
-
 __global__ void k_slab_savemu(PcgState* st) {
   if (halted(st)) return;
   st->mu_prev = st->mu;
 }
 
-__global__ void k_slab_beta(PcgState* st) {
-  if (halted(st)) return;
-  st->beta = st->mu / st->mu_prev;          // pcg.py:127-131 with the global q.r
+// after the fused max|r| / q.r reduction: history entry and convergence test
+// (pcg.py:113-121), then beta = mu' / mu (pcg.py:127-131) unless the step converged
+__global__ void k_slab_conv_beta(PcgState* st) {
+  if (st->skip || st->breakdown) return;
+  const double res = st->res;               // the global max|r|
+  st->hist[st->step - 1] = res;
+  if (res < st->tol) {
+    st->converged = 1;
+    st->done = 1;
+    return;
+  }
+  st->beta = st->mu / st->mu_prev;          // the global q.r
 }
 
 __global__ void __launch_bounds__(256) k_stage_pack(Geo g, int t, const double* __restrict__ v,
@@ -93,9 +92,8 @@ static unsigned stage_blocks(const Geo& g, int sm_count) {
 cudaError_t launch_slab_scalar(int which, PcgState* st, cudaStream_t s) {
   switch (which) {
     case 0: k_slab_alpha<<<1, 1, 0, s>>>(st); break;
-    case 1: k_slab_conv<<<1, 1, 0, s>>>(st); break;
     case 2: k_slab_savemu<<<1, 1, 0, s>>>(st); break;
-    default: k_slab_beta<<<1, 1, 0, s>>>(st); break;
+    default: k_slab_conv_beta<<<1, 1, 0, s>>>(st); break;
   }
   return cudaGetLastError();
 }

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) k_update(long long dim, double* __restric
     st->res = res;
     st->hist[st->step] = res;
     st->step += 1;
-    if (res < st->tol) {            // pcg.py:119-121
+    if (res < st->tol && !st->defer) {            // pcg.py:119-121
       st->converged = 1;
       st->done = 1;
     }
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) k_update_r(long long dim, double* __restr
     st->res = res;
     st->hist[st->step] = res;
     st->step += 1;
-    if (res < st->tol) {            // pcg.py:119-121
+    if (res < st->tol && !st->defer) {            // pcg.py:119-121
       st->converged = 1;
       st->done = 1;
     }

@@ -524,6 +524,35 @@ class SlabPcg:
             if v is not tot:
                 v.copy_(tot)
 
+    def _nreduce_res_mu(self):
+        """max|r| (max) and q.r (sum) in ONE collective: every process contributes its
+        (max, sum) pair, all-gathered and combined in rank order on the device."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        res = [self.nat[s].scalar[_lib.GQ_SLAB_RES] for s in self.comm.local]
+        mu = [self.nat[s].scalar[_lib.GQ_SLAB_MU] for s in self.comm.local]
+        if len(res) == 1 and self.comm.world == 1:
+            return
+        pair = torch.cat([res[0], mu[0]])
+        for r_, m_ in zip(res[1:], mu[1:]):
+            pair = torch.stack([torch.maximum(pair[0], r_[0]), pair[1] + m_[0]])
+        if self.comm.world > 1:
+            buf = pair.cpu() if self.comm.host_staged else pair
+            allp = torch.empty(self.comm.world * 2, dtype=torch.float64, device=buf.device)
+            dist.all_gather_into_tensor(allp, buf, group=self.comm.group)
+            allp = allp.view(self.comm.world, 2).to(pair.device)
+            tot_r, tot_m = allp[0, 0], allp[0, 1]
+            for w in range(1, self.comm.world):
+                tot_r = torch.maximum(tot_r, allp[w, 0])
+                tot_m = tot_m + allp[w, 1]
+            pair = torch.stack([tot_r, tot_m])
+        for r_, m_ in zip(res, mu):
+            r_.copy_(pair[0:1])
+            m_.copy_(pair[1:2])
+
     def _nphase(self, kind, s=0):
         for k in self.comm.local:
             self.nat[k].call("gq_slab_phase", kind, s)
@@ -535,12 +564,11 @@ class SlabPcg:
         self._nphase(_lib.GQ_SLAB_DELTA)
         self._nreduce(_lib.GQ_SLAB_CURV, "sum")
         self._nphase(_lib.GQ_SLAB_UPDATE)
-        self._nreduce(_lib.GQ_SLAB_RES, "max")
         for s in range(S):
             self._nphase(_lib.GQ_SLAB_OUTER, s)
             if s < S - 1:
                 self._nexchange(_lib.GQ_SLAB_VEC_DL0 + s % 2)
-        self._nreduce(_lib.GQ_SLAB_MU, "sum")
+        self._nreduce_res_mu()
         self._nphase(_lib.GQ_SLAB_DIRECTION)
 
     def _solve_native(self, r, x0s, tol, max_steps, host, start, callback=None):

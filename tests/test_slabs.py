@@ -290,8 +290,8 @@ def _native_logic(comm, ga):
     _FakeNative.everyone = list(s.nat.values())
     for w in (0, 1, 2):
         s._nexchange(w)
-    s._nreduce(0, "sum")
-    s._nreduce(1, "max")
+    s._nreduce(0, "sum")        # curvature
+    s._nreduce_res_mu()         # max|r| and q.r in one collective
     out = {}
     for k, nat in s.nat.items():
         sl = nat.sl
@@ -299,15 +299,16 @@ def _native_logic(comm, ga):
         for t in (sl.lo - 1, sl.hi):
             if sl.a <= t < sl.b:
                 halos[t] = [nat.vec[w][sl.stage(t)].tolist() for w in (0, 1, 2)]
-        out[k] = (halos, float(nat.scalar[0]), float(nat.scalar[1]))
+        out[k] = (halos, float(nat.scalar[0]), float(nat.scalar[1]), float(nat.scalar[2]))
     return out
 
 
 def _check_native_logic(out, ga, n):
     nh = ga.K * ga.N * ga.n
-    for k, (halos, ssum, smax) in out.items():
+    for k, (halos, ssum, smax, smu) in out.items():
         assert ssum == sum(float(j + 1) for j in range(n))          # curvature slot: summed
         assert smax == float(n) + 1.0                                # residual slot: max
+        assert smu == sum(float(j + 3) for j in range(n))           # q.r slot: summed
         for t, vs in halos.items():
             for w, v in enumerate(vs):
                 assert np.allclose(v, 1000.0 * t + 10.0 * w + np.arange(nh) * 1e-3)
