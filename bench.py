@@ -390,10 +390,12 @@ def run_slabs(args, ws, rank, local):
         assert exc.iterate.shape == (ga.dim,)
     e2e_s = max_over_ranks(time.perf_counter() - t0, dev, ws)
 
-    # kernels of ours per step and slab: the step kernels of the one-context graph, the four
-    # scalar fix-ups, and a pack + unpack per halo stage per exchange (S exchanges per step)
+    # kernels of ours per step and slab: the step kernels of the one-context graph, the three
+    # scalar fix-ups the slab phases enqueue (k_slab_alpha in UPDATE, k_slab_savemu in the
+    # last OUTER, k_slab_conv_beta in DIRECTION: gq_slab_phase), and a pack + unpack per halo
+    # stage per exchange (S exchanges per step)
     lib = solver.nat[solver.comm.local[0]].ctx.lib
-    per_slab = lib.gq_launches_per_step(solver.nat[solver.comm.local[0]].ctx.h) + 4
+    per_slab = lib.gq_launches_per_step(solver.nat[solver.comm.local[0]].ctx.h) + 3
     halos = sum((x.lo > 0) + (x.hi < ga.T + 1) for x in sl) / len(sl)
     launches = int(round(K * (per_slab + 2 * halos * args.S)))
     return {

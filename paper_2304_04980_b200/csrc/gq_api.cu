@@ -59,20 +59,10 @@ struct gq_ctx {
   int4* seg = nullptr;
   ChainOps co{};
   bool chain = false;          // lean DMMA chain sweeps (n in {2, 4})
-  bool dd = false;             // domain-decomposed chain sweeps (n = 2)
   bool fuse_x = false;         // x update fused into the direction update (opt-in)
   bool fuse_r = false;         // r update fused into the first outer sweep (chain kernel)
-  bool cta = false;            // CTA-cooperative TMA-fed chain sweeps (n = 2, opt-in)
-  double* cgt = nullptr;       // their inner-sweep forward tiles
-  CtaOps cto{};
-  double* ddarena = nullptr;
-  DDOps ddo{};
   bool grid = false;           // lean n = 2 grid stencils
-  bool dfac = false;           // factored Delta apply (time-invariant n = 2)
   bool st8 = false;            // n = 8 DMMA block stencils
-  bool st2 = false;            // n = 2 DMMA block stencils over 2 x 2 groups (opt-in)
-  double* st2_tiles = nullptr;
-  double* dfac_ops = nullptr;  // its per-node operator records
   GridShape gsh{};
   bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
   double* partials = nullptr;
@@ -120,7 +110,7 @@ static void release(gq_ctx* c) {
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
                   c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
                   c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->ddarena, c->cgt, c->dfac_ops, c->st2_tiles, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
+                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -379,59 +369,17 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
         return segs;
       };
       const std::vector<int4> s8 = chunks(8), s16 = chunks(16);
-      // n = 2 CTA-shared sweeps (opt-in): groups of <= 5 class-1 segments; stage 0 apart
-      std::vector<int4> grp;
-      bool two_class = g.n == 2 && g.T1 >= 2 && pcls[0] != pcls[1];
-      for (int t = 2; t < g.T1 && two_class; ++t) two_class = pcls[t] == pcls[1];
-      if (two_class)
-        for (size_t i = 1; i < s8.size();) {
-          const size_t e = std::min(s8.size(), i + 5);
-          grp.push_back(make_int4((int)i, (int)(e - i), s8[i].z, 0));
-          i = e;
-        }
       CKB(dalloc(&c->cff, chain_ff_doubles(g, c->npc)));
       CKB(dalloc(&c->cfb, chain_fb_doubles(g, c->npc)));
-      CKB(dalloc(&c->seg, s8.size() + s16.size() + grp.size()));
+      CKB(dalloc(&c->seg, s8.size() + s16.size()));
       CKB(cudaMemcpy(c->seg, s8.data(), s8.size() * sizeof(int4), cudaMemcpyHostToDevice));
       CKB(cudaMemcpy(c->seg + s8.size(), s16.data(), s16.size() * sizeof(int4),
                      cudaMemcpyHostToDevice));
-      if (!grp.empty())
-        CKB(cudaMemcpy(c->seg + s8.size() + s16.size(), grp.data(), grp.size() * sizeof(int4),
-                       cudaMemcpyHostToDevice));
       CKB(launch_build_chain(g, c->npc, c->fac, c->omega, c->cff, c->cfb, c->stream));
       CKB(cudaStreamSynchronize(c->stream));
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
-      if (!grp.empty() && chain2c_enabled()) {   // opt-in CTA-shared factor sweeps
-        bool ok0 = false;
-        CKB(cta_check_stage0(g, pcls[0], c->cff, c->cfb, ok0, c->stream));
-        if (ok0) {
-          c->co.grp = c->seg + s8.size() + s16.size();
-          c->co.ngrp = (int)grp.size();
-          c->co.c0 = pcls[0];
-        }
-      }
       c->chain = true;
-      if (cta_supported(g, pcls.data())) {
-        bool ok = false;
-        CKB(cta_check_stage0(g, pcls[0], c->cff, c->cfb, ok, c->stream));
-        if (ok) {
-          CKB(dalloc(&c->cgt, chain_ff_doubles(g, c->npc)));
-          CKB(launch_build_cta(g, c->npc, c->cff, c->cgt, c->stream));
-          CKB(cudaStreamSynchronize(c->stream));
-          c->cto = CtaOps{c->cff, c->cfb, c->cgt, pcls[0], pcls[1]};
-          c->cta = true;
-        }
-      }
-      if (dd_supported(g)) {
-        const DDShape sh = dd_shape(g);
-        CKB(dalloc(&c->ddarena, dd_doubles(g, c->npc)));
-        CKB(launch_build_dd(g, c->npc, c->psi, c->omega, c->ddarena, c->stream));
-        const size_t blocks = (size_t)c->npc * g.V * g.nb;
-        c->ddo = DDOps{c->ddarena, c->ddarena + blocks * 320, c->ddarena + blocks * (320 + 128),
-                       c->ddarena + blocks * (320 + 128 + 128), sh.m, sh.ns};
-        c->dd = true;
-      }
     }
   }
 
@@ -471,7 +419,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   {
     const char* e = getenv("GQ_NO_FUSE_R");
     // n = 8: the fused outer sweep measured 4.1 ms against 2.4 + 0.5 ms split (config 5)
-    c->fuse_r = c->chain && !c->dd && !c->cta && g.n != 8 && !(e && *e == '1');
+    c->fuse_r = c->chain && g.n != 8 && !(e && *e == '1');
   }
   // work vectors (stage-inner layout) and the reference-layout staging buffers
   const size_t dim = (size_t)g.dim;
@@ -481,18 +429,6 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   c->sh_delta = stencil_shape(g, kDelta, c->sm_count);
   c->grid = c->fast && grid_supported(g.n);
   if (c->grid) c->gsh = grid_shape(g, c->sm_count);
-  if (c->chain && st2_supported(g, c->nxc)) {
-    CKB(dalloc(&c->st2_tiles, st2_doubles(g, c->npc)));
-    CKB(launch_build_st2(g, c->npc, c->op, c->st2_tiles, c->stream));
-    CKB(cudaStreamSynchronize(c->stream));
-    c->st2 = true;
-  }
-  if (dfac_supported(g, D.n_dyn, D.n_cost)) {
-    CKB(dalloc(&c->dfac_ops, (size_t)g.nk * 48));
-    CKB(launch_build_dfac(g, c->A, c->C, c->qinv, c->brb, c->dfac_ops, c->stream));
-    CKB(cudaStreamSynchronize(c->stream));
-    c->dfac = true;
-  }
   c->sh_outer = stencil_shape(g, kOuter, c->sm_count);
   c->sh_inner = stencil_shape(g, kInner, c->sm_count);
   c->sw = sweep_shape(g, false);
@@ -503,10 +439,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                              fast_max_blocks(g, c->sh_delta, c->sm_count),
                              fast_max_blocks(g, c->sh_outer, c->sm_count),
                              c->chain ? chain_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
-                             c->cta ? cta_max_blocks(g) : 0LL,
-                             c->dfac ? dfac_max_blocks(c->sm_count) : 0LL,
                              c->st8 ? st8_max_blocks(c->sm_count) : 0LL,
-                             c->st2 ? st2_max_blocks(c->sm_count) : 0LL,
                              c->chain ? (long long)c->sm_count * 2 : 0LL,
                              c->chain ? chain_fr_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->grid ? (long long)c->gsh.blocks : 0LL});
@@ -632,10 +565,7 @@ static int enqueue_outer(gq_ctx* c, int s, int l0, int l1, const double* rin, do
   {
     if ((c->fast || c->chain) && s > 0 && l0 == 0) {
       // rhs_s = r + Xi~ delta_{s-1}, materialised once per outer sweep (nested_jacobi.py:119-121)
-      if (c->st2) {
-        CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kOuterRhs, c->dl[(s - 1) % 2],
-                      rin, c->rs, c->sm_count, c->partials, st, kDotNone, c->stream));
-      } else if (c->grid) {
+      if (c->grid) {      } else if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->gsh,
                        c->partials, st, kDotNone, c->stream));
       } else if (c->fast) {
@@ -666,12 +596,6 @@ static int enqueue_outer(gq_ctx* c, int s, int l0, int l1, const double* rin, do
         // the staged right-hand side (the separate r-update kernel is skipped)
         CK(launch_chain_fr(c->g, c->co, const_cast<double*>(rin), fuse_y, ob, c->sm_count,
                            c->partials, st, c->stream));
-      } else if (c->cta && !c->dd) {
-        CK(launch_chain_cta(c->g, c->cto, l > 0, s > 0 ? c->rs : rin, tp, ob, rin, c->sm_count,
-                            c->partials, st, dm, c->stream));
-      } else if (c->dd) {
-        CK(launch_chain_dd(c->g, c->co, c->ddo, l > 0, s > 0 ? c->rs : rin, tp, ob, rin,
-                           c->sm_count, c->partials, st, dm, c->stream));
       } else if (c->chain) {
         CK(launch_chain(c->g, c->co, l > 0, s > 0 ? c->rs : rin, tp, ob, rin, c->sm_count,
                         c->partials, st, dm, c->stream));
@@ -713,13 +637,7 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
 static int launch_one_sweep(gq_ctx* c, const double* rhs, const double* th, const double* xi,
                             double* out) {
   const bool inner = th != nullptr;
-  if (c->cta && !c->dd) {
-    CK(launch_chain_cta(c->g, c->cto, inner, rhs, th, out, nullptr, c->sm_count, c->partials,
-                        nullptr, kDotNone, c->stream));
-  } else if (c->dd) {
-    CK(launch_chain_dd(c->g, c->co, c->ddo, inner, rhs, th, out, nullptr, c->sm_count,
-                       c->partials, nullptr, kDotNone, c->stream));
-  } else if (c->chain) {
+  if (c->chain) {  } else if (c->chain) {
     CK(launch_chain(c->g, c->co, inner, rhs, th, out, nullptr, c->sm_count, c->partials,
                     nullptr, kDotNone, c->stream));
   } else if (c->fast) {
@@ -754,11 +672,7 @@ extern "C" int gq_nbjm_solve(gq_ctx* c, const double* rhs, double tol, int64_t m
     const double* rhs_s = c->r;
     const double* xi = nullptr;
     if (s > 0) {
-      if (c->st2) {
-        CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kOuterRhs, delta, c->r, c->rs,
-                      c->sm_count, c->partials, nullptr, kDotNone, c->stream));
-        rhs_s = c->rs;
-      } else if (c->grid) {
+      if (c->grid) {      } else if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->gsh, c->partials,
                        nullptr, kDotNone, c->stream));
         rhs_s = c->rs;
@@ -808,15 +722,9 @@ extern "C" int gq_apply_delta(gq_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, x, c->tmp0);
   if (rc) return rc;
-  if (c->st2)
-    CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kDelta, c->tmp0, nullptr, c->y,
-                  c->sm_count, c->partials, nullptr, kDotNone, c->stream));
-  else if (c->st8)
+  if (c->st8)
     CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kDelta, c->tmp0, nullptr, c->y,
                   c->sm_count, c->partials, nullptr, kDotNone, c->stream));
-  else if (c->dfac)
-    CK(launch_dfac(c->g, c->dfac_ops, c->tmp0, c->y, c->partials, nullptr, kDotNone,
-                   c->sm_count, c->stream));
   else if (c->grid)
     CK(launch_grid(c->g, c->fo, kDelta, c->tmp0, nullptr, c->y, c->gsh, c->partials, nullptr,
                    kDotNone, c->stream));
@@ -872,15 +780,9 @@ extern "C" int gq_apply_precond(gq_ctx* c, const double* r, double* q) {
 
 // y = Delta d with the curvature y.d and alpha (first kernel of a PCG step, pcg.py:99-108)
 static int enqueue_delta_step(gq_ctx* c) {
-  if (c->st2)
-    CK(launch_st2(c->g, c->st2_tiles, c->co.seg, c->co.nseg, kDelta, c->d, nullptr, c->y,
-                  c->sm_count, c->partials, c->st, kDotStep, c->stream));
-  else if (c->st8)
+  if (c->st8)
     CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kDelta, c->d, nullptr, c->y, c->sm_count,
                   c->partials, c->st, kDotStep, c->stream));
-  else if (c->dfac)
-    CK(launch_dfac(c->g, c->dfac_ops, c->d, c->y, c->partials, c->st, kDotStep, c->sm_count,
-                   c->stream));
   else if (c->grid)
     CK(launch_grid(c->g, c->fo, kDelta, c->d, nullptr, c->y, c->gsh, c->partials, c->st,
                    kDotStep, c->stream));
@@ -1047,7 +949,10 @@ extern "C" int gq_pcg_run(gq_ctx* c, double tol, int64_t max_steps, int64_t* ste
   CK(cudaStreamSynchronize(c->stream));
   PcgState& h = *c->h_st;
   if (!h.converged && !h.breakdown && h.step < max_steps) {
-    int rc = ensure_hist(c, max_steps);
+    // the history grows with the steps actually launched (not with max_steps, whose
+    // reference default dim + 50 would reserve O(dim) doubles): each chunk of graph launches
+    // first makes room for its own steps
+    int rc = ensure_hist(c, std::min<long long>(max_steps, h.step + 2));
     if (rc) return rc;
     h.hist = c->hist;
     h.tol = tol;
@@ -1059,6 +964,14 @@ extern "C" int gq_pcg_run(gq_ctx* c, double tol, int64_t max_steps, int64_t* ste
     long long chunk = 2;
     while (true) {
       const long long todo = std::min<long long>(chunk, max_steps - h.step);
+      if (h.step + todo > c->hist_cap) {
+        // the state is quiescent here (read back above): move the history, repoint the state
+        rc = ensure_hist(c, h.step + todo);
+        if (rc) return rc;
+        h.hist = c->hist;
+        CK(cudaMemcpyAsync(&c->st->hist, &c->hist, sizeof(double*), cudaMemcpyHostToDevice,
+                           c->stream));
+      }
       for (long long i = 0; i < todo; ++i) CK(cudaGraphLaunch(c->gexec[c->use_precond], c->stream));
       CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
@@ -1124,8 +1037,6 @@ extern "C" int gq_slab_enable(gq_ctx* c, int32_t own_lo, int32_t own_hi) {
   c->g.hx0 = c->slab_t0;
   c->g.hx1 = c->slab_t1;
   c->fuse_x = false;
-  c->dfac = false;   // the opt-in Delta variants have no halo mask
-  c->st2 = false;
   for (auto& ge : c->gexec)
     if (ge) {
       cudaGraphExecDestroy(ge);

@@ -645,180 +645,6 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
   }
 }
 
-// ---- domain-decomposed sweep (n = 2): one CTA of 8 warps per 8-chain group ----------------
-// Phase 1: warp w solves interior segment w with the restarted factors (the per-warp chain
-// code above, block range [kb, ke)), parks u in `out`, keeps u at the segment ends.
-// Phase 2: separator right-hand sides (warp w) and the separator chain (warp 0).
-// Phase 3: x = u - V x_left - W x_right over each interior; the q.r dot of the last sweep.
-__device__ __forceinline__ double2 ldg2(const double* p) {
-  return __ldg(reinterpret_cast<const double2*>(p));
-}
-
-template <bool INNER, int P, int W>
-__global__ void __launch_bounds__(32 * W) k_chain_dd(Geo g, ChainOps co, DDOps dd,
-                                                  const double* __restrict__ rhs,
-                                                  const double* __restrict__ th, double* out,
-                                                  const double* __restrict__ rdot, int n_items,
-                                                  double* partials, PcgState* st, int dotmode) {
-  using C = Ch<2, INNER, 1>;
-  constexpr int NS = 2, QQ = 64, KT = 3;
-  extern __shared__ __align__(16) double smem_dd[];
-  __shared__ double2 ub[W][2][32];     // u at the first / last block of each interior
-  __shared__ double2 gsm[W][32];       // separator right-hand sides, then x at separators
-  if (halted(st)) return;
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
-  double* ring = smem_dd + (size_t)wid * (P + 1) * C::SLOT;
-  const uint64_t pol_s = pol_first(), pol_k = pol_last();
-  const bool dotting = dotmode != kDotNone;
-  const long long rs = (long long)g.T1 * NS;
-  const long long cs = (long long)g.K * rs;
-  const long long rs2 = 2 * rs;
-  const int nb = g.nb, K = g.K, ns = dd.ns, m = dd.m;
-  const int kb = wid * m;
-  const int ke = wid == ns - 1 ? nb : wid * m + m - 1;
-  double dot = 0.0;
-#pragma unroll 1
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int v = item / co.nseg;
-    const int4 sg = co.seg[item - v * co.nseg];
-    const int t0 = sg.x, nvalid = sg.y, cls = sg.z;
-    const int a = 2 * v;
-    const bool okb = a + 1 < g.N;
-    const long long col_a = (long long)a * cs + (long long)t0 * NS;
-    // lane fragment: features 2qd, 2qd+1 (node qd) of chain rw
-    const int nd = qd;
-    const long long oofs = col_a + (long long)(nd & 1) * cs + (long long)(nd >> 1) * rs + rw * NS;
-    const bool ook = rw < nvalid && ((nd & 1) ? okb : true);
-    const int orow = nd >> 1;
-    const int bofs = rw * 8 + 2 * qd;
-    const long long tbase = ((long long)cls * g.V + v) * nb;   // (class, pair) block base
-
-    // ---- phase 1: interiors ----
-    double2 uc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-    if (wid < ns)
-      chain_item<2, INNER, P, 1>(g, co, rhs, th, out, rdot, false, ring, v, t0, nvalid, cls,
-                                 pol_s, pol_k, dot, kb, ke, dd.ffd, dd.fbd, uc);
-    ub[wid][0][lane] = uc[0];
-    ub[wid][1][lane] = uc[1];
-    __syncthreads();
-
-    // ---- phase 2a: separator right-hand sides g_w = b_g - E_g u_w[last] - E_n' u_{w+1}[first]
-    if (wid < ns - 1) {
-      const int gk = ke;   // separator block
-      const double* T = dd.sept + (((long long)cls * g.V + v) * 8 + wid) * 9 * QQ;
-      double2 acc = make_double2(0.0, 0.0);
-      {
-        const bool ok = ook && 2 * gk + orow < K;
-        acc = ok ? ldg2(rhs + oofs + (long long)gk * rs2) : acc;       // tau_g (D layout)
-      }
-      double2 e0 = make_double2(0.0, 0.0), e1 = e0;
-      const double2 bE = ldg2(T + bofs), bN = ldg2(T + QQ + bofs);
-      dmma(e0, uc[1].x, bE.x);
-      dmma(e1, uc[1].y, bE.y);
-      const double2 un = ub[wid + 1][0][lane];
-      dmma(e0, un.x, bN.x);
-      dmma(e1, un.y, bN.y);
-      if (INNER) {
-#pragma unroll
-        for (int p = 0; p < KT; ++p) {
-          const int r = 4 * p + qd;                  // theta record of this k-pair / lane
-          const int dc = th_dc(r), dr = th_dr(r);
-          const int row = 2 * gk + dr;
-          const bool ok = rw < nvalid && a + dc >= 0 && a + dc < g.N && row >= 0 && row < K;
-          const double2 tq = ok ? ldg2(th + col_a + (long long)dc * cs + (long long)row * rs + rw * NS)
-                                : make_double2(0.0, 0.0);
-          const double2 mb = ldg2(T + 2 * QQ + p * 64 + bofs);
-          dmma(e0, tq.x, mb.x);
-          dmma(e1, tq.y, mb.y);
-        }
-      }
-      gsm[wid][lane] = add2(acc, add2(e0, e1));
-    }
-    __syncthreads();
-
-    // ---- phase 2b: separator chain (ns - 1 blocks), warp 0 ----
-    if (wid == 0 && ns > 1) {
-      const double* T0 = dd.sept + ((long long)cls * g.V + v) * 8 * 9 * QQ;
-      double2 z = make_double2(0.0, 0.0);
-      for (int s2 = 0; s2 < ns - 1; ++s2) {
-        const double* T = T0 + (long long)s2 * 9 * QQ;
-        const double2 gv = gsm[s2][lane];
-        double2 a0 = make_double2(0.0, 0.0), a1 = a0, g0 = a0, g1 = a0;
-        const double2 bL = ldg2(T + 5 * QQ + bofs), bG = ldg2(T + 6 * QQ + bofs);
-        dmma(a0, gv.x, bL.x);
-        dmma(a1, gv.y, bL.y);
-        dmma(g0, z.x, bG.x);
-        dmma(g1, z.y, bG.y);
-        z = add2(add2(a0, a1), add2(g0, g1));
-        gsm[s2][lane] = z;
-      }
-      double2 xg = make_double2(0.0, 0.0);
-      for (int s2 = ns - 2; s2 >= 0; --s2) {
-        const double* T = T0 + (long long)s2 * 9 * QQ;
-        const double2 zv = gsm[s2][lane];
-        double2 a0 = make_double2(0.0, 0.0), a1 = a0, g0 = a0, g1 = a0;
-        const double2 bL = ldg2(T + 7 * QQ + bofs), bH = ldg2(T + 8 * QQ + bofs);
-        dmma(a0, zv.x, bL.x);
-        dmma(a1, zv.y, bL.y);
-        dmma(g0, xg.x, bH.x);
-        dmma(g1, xg.y, bH.y);
-        xg = add2(add2(a0, a1), add2(g0, g1));
-        gsm[s2][lane] = xg;
-        const int gk = s2 * m + m - 1;
-        if (ook && 2 * gk + orow < K) {
-          *reinterpret_cast<double2*>(out + oofs + (long long)gk * rs2) = xg;
-          if (dotting) {
-            const double2 rv = ldg2(rdot + oofs + (long long)gk * rs2);
-            dot = fma(xg.x, rv.x, dot);
-            dot = fma(xg.y, rv.y, dot);
-          }
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- phase 3: interior corrections x = u - V x_left - W x_right ----
-    if (wid < ns) {
-      const double2 xl = wid > 0 ? gsm[wid - 1][lane] : make_double2(0.0, 0.0);
-      const double2 xr = wid < ns - 1 ? gsm[wid][lane] : make_double2(0.0, 0.0);
-      const double* SPb = dd.spt + tbase * 128 + bofs;
-#pragma unroll 2
-      for (int k = kb; k < ke; ++k) {
-        const bool ok = ook && 2 * k + orow < K;
-        double2 x = ok ? __ldcg(reinterpret_cast<const double2*>(out + oofs + (long long)k * rs2))
-                       : make_double2(0.0, 0.0);
-        const double2 bV = ldg2(SPb + (long long)k * 128), bW = ldg2(SPb + (long long)k * 128 + 64);
-        double2 c0 = make_double2(0.0, 0.0), c1 = c0;
-        dmma(c0, xl.x, bV.x);
-        dmma(c1, xl.y, bV.y);
-        dmma(c0, xr.x, bW.x);
-        dmma(c1, xr.y, bW.y);
-        x = add2(x, add2(c0, c1));
-        if (ok) {
-          *reinterpret_cast<double2*>(out + oofs + (long long)k * rs2) = x;
-          if (dotting) {
-            const double2 rv = ldg2(rdot + oofs + (long long)k * rs2);
-            dot = fma(x.x, rv.x, dot);
-            dot = fma(x.y, rv.y, dot);
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (dotting) {
-    double mu;
-    if (grid_reduce<false>(dot, partials, &st->counter[2], mu) && threadIdx.x == 0) {
-      if (dotmode == kDotInit) {
-        st->mu = mu;                       // pcg.py:92
-      } else {
-        st->beta = mu / st->mu;            // pcg.py:127-131
-        st->mu = mu;
-      }
-    }
-  }
-}
-
 // ---- factor tiles ---------------------------------------------------------------------
 // ff[pc][v][k] = L^-1 | -G | -M (M = L^-1 Omega~, Q x 12n), fb[pc][v][k] = L^-T | -H, all as
 // 8x8 tiles; one thread per (block, row).
@@ -947,91 +773,45 @@ static cudaError_t chain_launch(const Geo& g, const ChainOps& co, const double* 
   int per_sm = 1;
   cudaError_t e = kernel_occupancy(k_chain<NS, INNER, P, MT, TF, false, BGX>, 32, smem, cache, per_sm);
   if (e != cudaSuccess) return e;
-  int cap = per_sm;
-  const int want = env_or(INNER ? "GQ_CHAIN_WARPS_INNER" : "GQ_CHAIN_WARPS_OUTER",
-                          env_or("GQ_CHAIN_WARPS", 0));
-  if (want > 0) cap = std::min(cap, want);
-  const int blocks = std::max(1, std::min(n_items, cap * sm_count));
-  const int smc = env_or("GQ_CHAIN8_GROUP", 1) ? sm_count : 0;   // n = 8 item grouping
+  const int blocks = std::max(1, std::min(n_items, per_sm * sm_count));
+  const int smc = sm_count;   // n = 8 item grouping
   k_chain<NS, INNER, P, MT, TF, false, BGX><<<blocks, 32, smem, s>>>(g, co, rhs, th, out, rdot, n_items,
                                                       partials, st, dotmode, nullptr, nullptr,
                                                       smc);
   return cudaGetLastError();
 }
 
-template <int NS, bool INNER, int MT>
+template <int NS, bool INNER>
 static cudaError_t chain_p(const Geo& g, const ChainOps& co, const double* rhs, const double* th,
                            double* out, const double* rdot, int sm_count, double* partials,
                            PcgState* st, int dotmode, cudaStream_t s) {
-  // ring depth (blocks in flight per warp), measured at n = 2 (tools/ab.sh, round 1):
-  // outer P 3 -> 7 took the outer sweep 0.216 -> 0.182 ms, inner P 3 -> 4 took 0.304 ->
-  // 0.287 ms; deeper inner rings lose (P 5: 0.331). n = 4 slots are 2.5x larger: keep P = 3.
-  const int pdef = env_or("GQ_CHAIN_P", NS == 2 ? (INNER ? 4 : 7) : 3);
-  const int pd = env_or(INNER ? "GQ_CHAIN_P_INNER" : "GQ_CHAIN_P_OUTER", pdef);
-  if constexpr (MT == 1) {
-    if (env_or("GQ_CHAIN_TMA", 0) == 1) {
-      if (pd == 5)
-        return chain_launch<NS, INNER, 5, MT, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-      return chain_launch<NS, INNER, 3, MT, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    }
-  }
-  if constexpr (NS == 2 && MT == 1) {
-    if (env_or("GQ_CHAIN_BG", 0) == 1) {   // B fragments from global (experiment)
-      if (pd == 1) return chain_launch<NS, INNER, 1, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-      if (pd == 2) return chain_launch<NS, INNER, 2, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-      if (pd == 7) return chain_launch<NS, INNER, 7, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-      if (pd == 4) return chain_launch<NS, INNER, 4, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-      return chain_launch<NS, INNER, 3, MT, false, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    }
-  }
-  switch (pd) {
-    case 2: return chain_launch<NS, INNER, 2, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    case 4: return chain_launch<NS, INNER, 4, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    case 5: return chain_launch<NS, INNER, 5, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    case 7: return chain_launch<NS, INNER, 7, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    default: break;
-  }
-  return chain_launch<NS, INNER, 3, MT>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-}
-
-template <int NS, bool INNER>
-static cudaError_t chain_mt(const Geo& g, const ChainOps& co, const double* rhs, const double* th,
-                            double* out, const double* rdot, int sm_count, double* partials,
-                            PcgState* st, int dotmode, cudaStream_t s) {
+  // ring depth (blocks in flight per warp), measured at n = 2 (round 1): outer P 3 -> 7 took
+  // the outer sweep 0.216 -> 0.182 ms, inner P 3 -> 4 took 0.304 -> 0.287 ms; deeper inner
+  // rings lose (P 5: 0.331).  n = 4 slots are 2.5x larger: P = 3.
   if constexpr (NS == 2) {
-    if (env_or("GQ_CHAIN_MT", 1) == 2)
-      return chain_p<NS, INNER, 2>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    if (INNER) return chain_launch<NS, INNER, 4, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    return chain_launch<NS, INNER, 7, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   }
-  return chain_p<NS, INNER, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+  return chain_launch<NS, INNER, 3, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
 }
 
 cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
                          const double* th, double* out, const double* rdot, int sm_count,
                          double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  if (g.n == 2 && co.grp != nullptr && chain2c_enabled())
-    return launch_chain2c(g, co, inner, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 2)
-    return inner ? chain_mt<2, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
-                 : chain_mt<2, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    return inner ? chain_p<2, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                 : chain_p<2, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 4)
-    return inner ? chain_mt<4, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
-                 : chain_mt<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    return inner ? chain_p<4, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
+                 : chain_p<4, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 8 && co.grp != nullptr && chain8c_enabled())
     return launch_chain8c(g, co, inner, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 8) {
     // P = 2 (10 KB inner / 5 KB outer record slots; factor tiles are not staged)
     // measured on config 5 (tools/c5time.py): inner P = 1 (smaller rings leave more of the
     // SM's L1 to the factor tiles: 4.1 -> 3.55 ms), outer P = 2 (2.36 vs 2.6 ms at P = 1)
-    const int p = env_or(inner ? "GQ_CHAIN8_P_INNER" : "GQ_CHAIN8_P_OUTER",
-                         env_or("GQ_CHAIN8_P", inner ? 1 : 2));
-    if (inner) {
-      if (p == 1) return chain_launch<8, true, 1, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-      return p == 3 ? chain_launch<8, true, 3, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
-                    : chain_launch<8, true, 2, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    }
-    if (p == 1) return chain_launch<8, false, 1, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    return p == 3 ? chain_launch<8, false, 3, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
-                  : chain_launch<8, false, 2, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    if (inner) return chain_launch<8, true, 1, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
+    return chain_launch<8, false, 2, 1>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -1058,9 +838,7 @@ cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const d
                             double* out, int sm_count, double* partials, PcgState* st,
                             cudaStream_t s) {
   if (g.n == 2)
-    return env_or("GQ_CHAIN_P_OUTER", 7) == 4
-               ? chain_fr_launch<2, 4>(g, co, r, y, out, sm_count, partials, st, s)
-               : chain_fr_launch<2, 7>(g, co, r, y, out, sm_count, partials, st, s);
+    return chain_fr_launch<2, 7>(g, co, r, y, out, sm_count, partials, st, s);
   if (g.n == 4) return chain_fr_launch<4, 3>(g, co, r, y, out, sm_count, partials, st, s);
   if (g.n == 8) return chain_fr_launch<8, 3>(g, co, r, y, out, sm_count, partials, st, s);
   return cudaErrorInvalidValue;
@@ -1068,39 +846,6 @@ cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const d
 
 long long chain_fr_max_blocks(const Geo& g, int nseg, int sm_count) {
   return std::min<long long>((long long)g.V * nseg, 64LL * sm_count);
-}
-
-template <bool INNER, int P, int W>
-static cudaError_t chain_dd_launch(const Geo& g, const ChainOps& co, const DDOps& dd,
-                                   const double* rhs, const double* th, double* out,
-                                   const double* rdot, int sm_count, double* partials,
-                                   PcgState* st, int dotmode, cudaStream_t s) {
-  constexpr size_t smem = (size_t)W * (P + 1) * Ch<2, INNER, 1>::SLOT * sizeof(double);
-  const int n_items = g.V * co.nseg;
-  static int cache[64] = {0};
-  int per_sm = 1;
-  cudaError_t e = kernel_occupancy(k_chain_dd<INNER, P, W>, 32 * W, smem, cache, per_sm);
-  if (e != cudaSuccess) return e;
-  const int blocks = std::max(1, std::min(n_items, per_sm * sm_count));
-  k_chain_dd<INNER, P, W><<<blocks, 32 * W, smem, s>>>(g, co, dd, rhs, th, out, rdot, n_items,
-                                                       partials, st, dotmode);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_chain_dd(const Geo& g, const ChainOps& co, const DDOps& dd, bool inner,
-                            const double* rhs, const double* th, double* out, const double* rdot,
-                            int sm_count, double* partials, PcgState* st, int dotmode,
-                            cudaStream_t s) {
-  const int p = env_or("GQ_DD_P", 2);
-  if (dd.ns > 4) {
-    if (inner) return chain_dd_launch<true, 2, 8>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-    return chain_dd_launch<false, 2, 8>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-  }
-  if (inner)
-    return p == 3 ? chain_dd_launch<true, 3, 4>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
-                  : chain_dd_launch<true, 2, 4>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
-  return p == 3 ? chain_dd_launch<false, 3, 4>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
-                : chain_dd_launch<false, 2, 4>(g, co, dd, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
 }
 
 long long chain_max_blocks(const Geo& g, int nseg, int sm_count) {

@@ -409,29 +409,12 @@ static cudaError_t grid_launch(const Geo& g, const FastOps& fo, const double* x,
 cudaError_t launch_grid(const Geo& g, const FastOps& fo, int mode, const double* x,
                         const double* rin, double* y, const GridShape& sh, double* partials,
                         PcgState* st, int dotmode, cudaStream_t s) {
-  const int p = genv("GQ_GRID_P", 2);
-  // Delta register cap: 128 (from 136) fits 16 resident warps per SM; measured 592.6 -> 600.1
-  // steps/s (tools/steptime.py, bench.py).  GQ_GRID_MAXR=0 restores the uncapped build.
-  const int maxr = genv("GQ_GRID_MAXR", 128);
-  if (mode == kDelta && p == 2 && maxr == 128)
+  // ring depth P = 2 for both modes (round 1 sweeps: Delta P 3 / 4 and outer-rhs P 1 / 3 / 4 / 6
+  // were slower or equal).  Delta capped at 128 registers (from 136): 16 resident warps per
+  // SM, 592.6 -> 600.1 steps/s.
+  if (mode == kDelta)
     return grid_launch<kDelta, 2, 128>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
-  if (mode == kDelta && p == 2 && maxr == 120)
-    return grid_launch<kDelta, 2, 120>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
-  if (mode == kDelta && p == 2 && maxr == 112)
-    return grid_launch<kDelta, 2, 112>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
-  if (mode == kDelta && p == 2 && maxr == 96)
-    return grid_launch<kDelta, 2, 96>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
-  if (mode == kDelta) {
-    if (p == 2) return grid_launch<kDelta, 2>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
-    if (p == 4) return grid_launch<kDelta, 4>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
-    return grid_launch<kDelta, 3>(g, fo, x, rin, y, sh, partials, st, dotmode, s);
-  }
-  const int po = genv("GQ_GRID_PO", p);   // outer-rhs ring depth (default: as Delta)
-  if (po == 1) return grid_launch<kOuterRhs, 1>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
-  if (po == 2) return grid_launch<kOuterRhs, 2>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
-  if (po == 4) return grid_launch<kOuterRhs, 4>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
-  if (po == 6) return grid_launch<kOuterRhs, 6>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
-  return grid_launch<kOuterRhs, 3>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
+  return grid_launch<kOuterRhs, 2>(g, fo, x, rin, y, sh, partials, st, kDotNone, s);
 }
 
 }  // namespace gq

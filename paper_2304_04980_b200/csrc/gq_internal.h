@@ -113,13 +113,8 @@ struct ChainOps {
   const double* omega = nullptr;   // [npc][N][K][5][n][n] cross-pair Psi blocks (n = 8 inner)
   const int4* grp = nullptr;       // CTA items (n = 8: all classes; n = 2: class-1 runs)
   int ngrp = 0;
-  int c0 = -1;                     // n = 2 CTA sweeps: stage-0 class solved block-diagonally
 };
-// n = 2 pair-chain sweeps with CTA-shared factor tiles (gq_chain2c.cu, opt-in)
-bool chain2c_enabled();
-cudaError_t launch_chain2c(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
-                           const double* th, double* out, const double* rdot, int sm_count,
-                           double* partials, PcgState* st, int dotmode, cudaStream_t s);
+
 // n = 8 pair-chain sweeps with CTA-shared factor tiles (gq_chain8c.cu)
 bool chain8c_enabled();
 cudaError_t launch_chain8c(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
@@ -142,64 +137,6 @@ cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const d
                             double* out, int sm_count, double* partials, PcgState* st,
                             cudaStream_t s);
 long long chain_fr_max_blocks(const Geo& g, int nseg, int sm_count);
-
-// ---- domain-decomposed pair-chain solve, n = 2 (gq_dd.cu setup, gq_chain.cu kernel) ----
-struct DDShape {
-  int m = 0, ns = 0;   // blocks per segment (last one a separator), segments per chain
-};
-struct DDOps {
-  const double* ffd;   // [npc][V][nb] interior tiles L^-1 | -G | -M (restarted per interior)
-  const double* fbd;   // [npc][V][nb] L^-T | -H
-  const double* spt;   // [npc][V][nb] spike tiles -V | -W
-  const double* sept;  // [npc][V][8] separator tiles -E_g | -E_n' | -Om(3) | Ls^-1 | -Gs | Ls^-T | -Hs
-  int m, ns;
-};
-bool dd_supported(const Geo& g);
-DDShape dd_shape(const Geo& g);
-size_t dd_doubles(const Geo& g, int npc);
-cudaError_t launch_build_dd(const Geo& g, int npc, const double* psi, const double* omega,
-                            double* arena, cudaStream_t s);
-cudaError_t launch_chain_dd(const Geo& g, const ChainOps& co, const DDOps& dd, bool inner,
-                            const double* rhs, const double* th, double* out, const double* rdot,
-                            int sm_count, double* partials, PcgState* st, int dotmode,
-                            cudaStream_t s);
-
-// ---- CTA-cooperative TMA-fed pair-chain sweeps, n = 2 (gq_cta.cu) ----
-struct CtaOps {
-  const double* ff;    // chain forward tiles (ChainOps::ff), stride 320
-  const double* fb;    // chain backward tiles (ChainOps::fb), stride 128
-  const double* gt;    // inner-sweep forward tiles in k-pair group order, stride 320
-  int c0, c1;          // Psi classes of stage 0 / stages >= 1
-};
-// time-invariant pattern (stage 0 its own class, one class for t >= 1), n = 2, N even
-bool cta_supported(const Geo& g, const int* pcls);
-cudaError_t launch_build_cta(const Geo& g, int npc, const double* ff, double* gt,
-                             cudaStream_t s);
-// ok = the stage-0 class tiles carry no coupling (G, M, H all zero)
-cudaError_t cta_check_stage0(const Geo& g, int c0, const double* ff, const double* fb,
-                             bool& ok, cudaStream_t s);
-cudaError_t launch_chain_cta(const Geo& g, const CtaOps& co, bool inner, const double* rhs,
-                             const double* th, double* out, const double* rdot, int sm_count,
-                             double* partials, PcgState* st, int dotmode, cudaStream_t s);
-long long cta_max_blocks(const Geo& g);
-
-// ---- factored Delta apply, time-invariant n = 2 (gq_dfac.cu) ----
-bool dfac_supported(const Geo& g, int n_dyn, int n_cost);
-cudaError_t launch_build_dfac(const Geo& g, const double* A, const double* C, const double* qinv,
-                              const double* brb, double* rec, cudaStream_t s);
-// y = Delta x (+ y.x curvature, alpha, breakdown when dotmode != kDotNone)
-cudaError_t launch_dfac(const Geo& g, const double* ops, const double* x, double* y,
-                        double* partials, PcgState* st, int dotmode, int sm_count, cudaStream_t s);
-long long dfac_max_blocks(int sm_count);
-
-// ---- n = 2 block stencils on DMMA over 2 x 2 node groups (gq_st2.cu) ----
-bool st2_supported(const Geo& g, int nxc);
-size_t st2_doubles(const Geo& g, int npc);
-cudaError_t launch_build_st2(const Geo& g, int npc, const Ops& op, double* tiles, cudaStream_t s);
-cudaError_t launch_st2(const Geo& g, const double* tiles, const int4* seg, int nseg, int mode,
-                       const double* x, const double* rin, double* y, int sm_count,
-                       double* partials, PcgState* st, int dotmode, cudaStream_t s);
-long long st2_max_blocks(int sm_count);
 
 // ---- n = 8 block stencils on DMMA (gq_st8.cu) ----
 bool st8_supported(const Geo& g, int nxc);

@@ -52,6 +52,10 @@ __global__ void k_slab_conv_beta(PcgState* st) {
     st->done = 1;
     return;
   }
+  // safeguard: a kernel that decided on a slab-local max|r| (one missing the PcgState::defer
+  // check) must not stop this slab while the global residual is still above tol
+  st->converged = 0;
+  st->done = 0;
   st->beta = st->mu / st->mu_prev;          // the global q.r
 }
 

@@ -502,10 +502,31 @@ class SlabPcg:
                 nat[s].recv[side].copy_(rcv)
             nat[s].call("gq_slab_unpack", which, halo_t, ctypes.c_void_p(nat[s].recv[side].data_ptr()))
 
-    def _nreduce(self, which, op):
-        """Combine one device scalar over all slabs (slab order in-process, then NCCL)."""
+    def _gather_combine(self, part, ops):
+        """Combine a vector of per-process partials over the process group: all-gathered and
+        folded in rank order on the device (ops[i] in {"sum", "max"} per entry), so every
+        collective of the slab step follows one deterministic rule whatever the slab-to-
+        process mapping (NCCL's own all-reduce order is not fixed)."""
         import torch
         import torch.distributed as dist
+
+        if self.comm.world == 1:
+            return part
+        buf = part.cpu() if self.comm.host_staged else part
+        k = buf.numel()
+        allp = torch.empty(self.comm.world * k, dtype=torch.float64, device=buf.device)
+        dist.all_gather_into_tensor(allp, buf, group=self.comm.group)
+        allp = allp.view(self.comm.world, k).to(part.device)
+        tot = [allp[0, i] for i in range(k)]
+        for w in range(1, self.comm.world):
+            tot = [torch.maximum(tot[i], allp[w, i]) if ops[i] == "max" else tot[i] + allp[w, i]
+                   for i in range(k)]
+        return torch.stack(tot)
+
+    def _nreduce(self, which, op):
+        """Combine one device scalar over all slabs: local slabs in slab order, then the
+        processes in rank order (_gather_combine)."""
+        import torch
 
         vals = [self.nat[s].scalar[which] for s in self.comm.local]
         if len(vals) == 1 and self.comm.world == 1:
@@ -514,21 +535,14 @@ class SlabPcg:
         tot = vals[0].clone()
         for v in vals[1:]:
             tot = tot + v if op == "sum" else torch.maximum(tot, v)
-        if self.comm.world > 1:
-            buf = tot.cpu() if self.comm.host_staged else tot
-            dist.all_reduce(buf, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX,
-                            group=self.comm.group)
-            if buf is not tot:
-                tot.copy_(buf)
+        tot = self._gather_combine(tot, (op,))
         for v in vals:
-            if v is not tot:
-                v.copy_(tot)
+            v.copy_(tot)
 
     def _nreduce_res_mu(self):
         """max|r| (max) and q.r (sum) in ONE collective: every process contributes its
         (max, sum) pair, all-gathered and combined in rank order on the device."""
         import torch
-        import torch.distributed as dist
 
         from . import _lib
 
@@ -539,16 +553,7 @@ class SlabPcg:
         pair = torch.cat([res[0], mu[0]])
         for r_, m_ in zip(res[1:], mu[1:]):
             pair = torch.stack([torch.maximum(pair[0], r_[0]), pair[1] + m_[0]])
-        if self.comm.world > 1:
-            buf = pair.cpu() if self.comm.host_staged else pair
-            allp = torch.empty(self.comm.world * 2, dtype=torch.float64, device=buf.device)
-            dist.all_gather_into_tensor(allp, buf, group=self.comm.group)
-            allp = allp.view(self.comm.world, 2).to(pair.device)
-            tot_r, tot_m = allp[0, 0], allp[0, 1]
-            for w in range(1, self.comm.world):
-                tot_r = torch.maximum(tot_r, allp[w, 0])
-                tot_m = tot_m + allp[w, 1]
-            pair = torch.stack([tot_r, tot_m])
+        pair = self._gather_combine(pair, ("max", "sum"))
         for r_, m_ in zip(res, mu):
             r_.copy_(pair[0:1])
             m_.copy_(pair[1:2])

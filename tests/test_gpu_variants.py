@@ -16,27 +16,10 @@ VARIANTS = {
     "generic_v1": {"GQ_FORCE_V1": "1"},          # thread-per-chain sweeps, v1 stencils
     "no_chain": {"GQ_NO_CHAIN": "1"},            # FMA / v6 sweeps instead of the chain kernel
     "no_grid": {"GQ_NO_GRID": "1"},              # v2 stencils instead of the n=2 grid kernel
-    "chain_mt2": {"GQ_CHAIN_MT": "2"},           # two M-tiles (16 chains) per warp
-    "chain_p2": {"GQ_CHAIN_P": "2", "GQ_GRID_P": "3"},
-    "chain_p3": {"GQ_CHAIN_P": "3"},             # the pre-tuning ring depth
-    "chain_p5": {"GQ_CHAIN_P": "5"},
-    "chain_tma": {"GQ_CHAIN_TMA": "1"},          # factor tiles by bulk copy + mbarrier
-    "cta": {"GQ_CTA": "1"},                      # CTA-cooperative TMA-fed chain sweeps
-    "cta_r2": {"GQ_CTA": "1", "GQ_CTA_R_INNER": "2", "GQ_CTA_R_OUTER": "3"},
-    "cta_r4": {"GQ_CTA": "1", "GQ_CTA_R_INNER": "4", "GQ_CTA_R_OUTER": "7"},
-    "cta_persist": {"GQ_CTA": "1", "GQ_CTA_PERSIST": "1"},
-    "cta_w1": {"GQ_CTA": "1", "GQ_CTA_W": "1"},                 # per-warp TMA pipeline
-    "chain2c": {"GQ_CHAIN2C": "1"},              # n = 2 sweeps with CTA-shared factor tiles
-    "chain2c_nofr": {"GQ_CHAIN2C": "1", "GQ_NO_FUSE_R": "1"},
     "fuse_x": {"GQ_FUSE_X": "1"},                # x update fused into the direction update
     "no_fuse_r": {"GQ_NO_FUSE_R": "1"},          # separate r update kernel
     "no_fuse": {"GQ_NO_FUSE_R": "1", "GQ_NO_FORK": "1"},
-    "dfac": {"GQ_DFAC": "1"},                    # factored Delta apply (CTA, w shared in smem)
-    "st2": {"GQ_ST2": "1"},                      # n = 2 DMMA stencils over 2 x 2 node groups
-    "dfac16": {"GQ_DFAC": "1", "GQ_DFAC_NW": "16"},
     "no_fork": {"GQ_NO_FORK": "1"},              # x update in line instead of on a branch
-    "dd4": {"GQ_DD": "1"},                       # domain-decomposed chain solve, 4 segments
-    "dd8": {"GQ_DD": "1", "GQ_DD_W": "8"},       # ... 8 segments
 }
 
 
