@@ -62,6 +62,10 @@ struct gq_ctx {
   bool fuse_x = false;         // x update fused into the direction update (opt-in)
   bool fuse_r = false;         // r update fused into the first outer sweep (chain kernel)
   bool grid = false;           // lean n = 2 grid stencils
+  bool dstep = false;          // t-loop factored Delta apply (n = 2)
+  DstepOps dso{};
+  CUtensorMap map_d{}, map_tmp0{};   // TMA views of the Delta inputs (d, unit-apply scratch)
+  CUtensorMap map_y{};               // ... and of its output
   bool st8 = false;            // n = 8 DMMA block stencils
   GridShape gsh{};
   bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
@@ -429,6 +433,17 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   c->sh_delta = stencil_shape(g, kDelta, c->sm_count);
   c->grid = c->fast && grid_supported(g.n);
   if (c->grid) c->gsh = grid_shape(g, c->sm_count);
+  {
+    const char* e = getenv("GQ_NO_DSTEP");
+    const char* f = getenv("GQ_FORCE_V1");
+    if (dstep_supported(g) && !(e && *e == '1') && !(f && *f == '1') &&
+        dstep_make_map(g, c->d, false, &c->map_d) &&
+        dstep_make_map(g, c->tmp0, false, &c->map_tmp0) &&
+        dstep_make_map(g, c->y, true, &c->map_y)) {
+      c->dso = DstepOps{c->A, c->C, c->qinv, c->brb, c->dcls, c->ccls};
+      c->dstep = true;
+    }
+  }
   c->sh_outer = stencil_shape(g, kOuter, c->sm_count);
   c->sh_inner = stencil_shape(g, kInner, c->sm_count);
   c->sw = sweep_shape(g, false);
@@ -441,6 +456,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                              c->chain ? chain_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->st8 ? st8_max_blocks(c->sm_count) : 0LL,
                              c->chain ? (long long)c->sm_count * 2 : 0LL,
+                             c->dstep ? dstep_max_blocks(c->sm_count) : 0LL,
                              c->chain ? chain_fr_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->grid ? (long long)c->gsh.blocks : 0LL});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));
@@ -565,7 +581,7 @@ static int enqueue_outer(gq_ctx* c, int s, int l0, int l1, const double* rin, do
   {
     if ((c->fast || c->chain) && s > 0 && l0 == 0) {
       // rhs_s = r + Xi~ delta_{s-1}, materialised once per outer sweep (nested_jacobi.py:119-121)
-      if (c->grid) {      } else if (c->grid) {
+      if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->gsh,
                        c->partials, st, kDotNone, c->stream));
       } else if (c->fast) {
@@ -637,7 +653,7 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
 static int launch_one_sweep(gq_ctx* c, const double* rhs, const double* th, const double* xi,
                             double* out) {
   const bool inner = th != nullptr;
-  if (c->chain) {  } else if (c->chain) {
+  if (c->chain) {
     CK(launch_chain(c->g, c->co, inner, rhs, th, out, nullptr, c->sm_count, c->partials,
                     nullptr, kDotNone, c->stream));
   } else if (c->fast) {
@@ -672,7 +688,7 @@ extern "C" int gq_nbjm_solve(gq_ctx* c, const double* rhs, double tol, int64_t m
     const double* rhs_s = c->r;
     const double* xi = nullptr;
     if (s > 0) {
-      if (c->grid) {      } else if (c->grid) {
+      if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->gsh, c->partials,
                        nullptr, kDotNone, c->stream));
         rhs_s = c->rs;
@@ -722,7 +738,10 @@ extern "C" int gq_apply_delta(gq_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, x, c->tmp0);
   if (rc) return rc;
-  if (c->st8)
+  if (c->dstep)
+    CK(launch_dstep(c->g, c->map_tmp0, c->map_y, c->dso, c->y, c->partials, nullptr, kDotNone,
+                    c->sm_count, c->stream));
+  else if (c->st8)
     CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kDelta, c->tmp0, nullptr, c->y,
                   c->sm_count, c->partials, nullptr, kDotNone, c->stream));
   else if (c->grid)
@@ -780,7 +799,10 @@ extern "C" int gq_apply_precond(gq_ctx* c, const double* r, double* q) {
 
 // y = Delta d with the curvature y.d and alpha (first kernel of a PCG step, pcg.py:99-108)
 static int enqueue_delta_step(gq_ctx* c) {
-  if (c->st8)
+  if (c->dstep)
+    CK(launch_dstep(c->g, c->map_d, c->map_y, c->dso, c->y, c->partials, c->st, kDotStep, c->sm_count,
+                    c->stream));
+  else if (c->st8)
     CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kDelta, c->d, nullptr, c->y, c->sm_count,
                   c->partials, c->st, kDotStep, c->stream));
   else if (c->grid)

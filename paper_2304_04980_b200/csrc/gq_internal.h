@@ -1,6 +1,7 @@
 // Host-side launchers shared between the kernel translation units and the C-ABI.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "gq_common.cuh"
@@ -146,6 +147,25 @@ cudaError_t launch_st8(const Geo& g, const Ops& op, const int4* seg, int nseg, i
                        const double* x, const double* rin, double* y, int sm_count,
                        double* partials, PcgState* st, int dotmode, cudaStream_t s);
 long long st8_max_blocks(int sm_count);
+
+// ---- t-loop factored Delta apply, n = 2 (gq_dstep.cu) ----
+struct DstepOps {
+  const double* A;      // [nd][N][K][n][n]
+  const double* C;      // [nd][4][N][K][n][n]  couplings (west, east, north, south)
+  const double* qinv;   // [nq][N][K][n][n]
+  const double* brb;    // [nd][N][K][n][n]     B R^-1 B'
+  const int* dcls;      // [T]  dynamics set of stage t -> t+1
+  const int* ccls;      // [T1] cost set of stage t
+};
+bool dstep_supported(const Geo& g);
+long long dstep_max_blocks(int sm_count);
+// TMA view of a stage-inner vector: input boxes (tile + halo) or output boxes (tile)
+bool dstep_make_map(const Geo& g, const double* base, bool out, CUtensorMap* m);
+// y = Delta x for the vector behind `dmap` into the vector behind `ymap` (+ y.x curvature,
+// alpha, breakdown when dotmode != kDotNone); stage-slab halo rows are written as zeros
+cudaError_t launch_dstep(const Geo& g, const CUtensorMap& dmap, const CUtensorMap& ymap,
+                         const DstepOps& op, double* y, double* partials, PcgState* st,
+                         int dotmode, int sm_count, cudaStream_t s);
 
 // ---- lean n = 2 grid stencils (gq_grid.cu) ----
 struct GridShape {
