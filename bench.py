@@ -10,9 +10,12 @@ BASELINE config 4 (mass-spring-damper 256 x 256 grid, T=200, n=2, m=1, S=L=2; se
 synthetic data, no dataset involved).  Every vector is 210.8 MB, larger than the 126 MB
 L2, so no L2 flush is needed between timed steps.
 
-Multi-GPU (torchrun): by default N ranks run N independent replicas of the one-context
-graph solve ("replicas only"); value = total steps of all ranks / max-over-ranks device
-time.  --slabs runs the stage-slab sharded solve instead (paper_2304_04980_b200/slab.py,
+Multi-GPU (torchrun): by default N > 1 ranks run the stage-slab sharded solve of the ONE
+problem (paper_2304_04980_b200/slab.py): one slab of stages per rank, halos
+and the step's scalars over NCCL, value = steps of the global solve / max-over-ranks device
+time ("strong" scaling).  --replicas runs N independent replicas of the one-context graph
+solve instead ("weak"); N = 1 always runs the one-context graph solve.  (--slabs at N = 1
+runs the sharded driver with a single slab.)  The slab solver (paper_2304_04980_b200/slab.py,
 SURVEY.md 8(e)/(f)4): one slab per rank, halos and scalars over NCCL, value = steps of the
 one global solve / max-over-ranks time ("strong" scaling).
 
@@ -74,6 +77,43 @@ def kernel_passes(name, S=2, L=2):
         return (2 + (1 if l_ > 0 else 0) + (1 if last else 0) + (1 if name.endswith("_xi") else 0)
                 + (2 if name.endswith("_r") else 0))   # _r: + read y, write r (r update fused)
     return 0
+
+
+def kernel_flops(name, cnt, dim, S=2, L=2):
+    """Algorithmic fp64 flops of one launch (2 x the reference's multiply counters,
+    counts.py / SURVEY.md Appendix A; 2 flops per element for the CG vector kernels)."""
+    if name == "delta":
+        return 2.0 * cnt["matvec_flops"]
+    if name.startswith("outer_rhs"):
+        return 2.0 * cnt["outer_coupling_flops"]
+    if name.startswith("sweep_s"):
+        l_ = int(name.split("_l")[1].split("_")[0])
+        f = 2.0 * cnt["pair_solve_flops"] + (2.0 * cnt["inner_coupling_flops"] if l_ > 0 else 0.0)
+        s_ = int(name[len("sweep_s"):].split("_")[0])
+        if s_ == S - 1 and l_ == L - 1:
+            f += 2.0 * dim                    # q.r fused into the last sweep
+        if name.endswith("_r"):
+            f += 2.0 * dim                    # r -= alpha y fused into the first sweep
+        return f
+    if name in ("update", "update_x", "dirupdate", "dot"):
+        return 2.0 * dim
+    if name == "dirupdate_x":
+        return 4.0 * dim
+    return 0.0
+
+
+def kernel_pipe(name):
+    """fp64 pipe a kernel family runs on: DMMA (tensor, m8n8k4 f64) or DFMA."""
+    return "dmma" if name.startswith("sweep_s") else "dfma"
+
+
+def load_fp64_peaks():
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peaks.json")) as fh:
+            pk = json.load(fh)
+        return {"dfma": float(pk["dfma_tflops"]), "dmma": float(pk["dmma_tflops"])}
+    except Exception:
+        return {"dfma": 34.0, "dmma": 36.8}
 
 
 def kernel_family(name):
@@ -251,6 +291,9 @@ def run_ours(args, ws, rank, local):
     dim = op.dim
     vec_bytes = 8 * dim
     peak, peak_src = load_peaks()
+    fp64_peaks = load_fp64_peaks()
+    from paper_2304_04980_b200.counts import counters
+    cnt = counters(ga, L, S)
     # dominant kernel = the kernel (one compiled kernel, possibly several launches per step)
     # with the largest total device time per step; its roofline uses the per-launch averages
     fams = {}
@@ -303,7 +346,7 @@ def run_ours(args, ws, rank, local):
             "workload": CONFIG_NAMES.get(args.config, str(args.config)),
             "K": ga.K, "N": ga.N, "T": ga.T, "n": ga.n, "m": ga.m,
             "outer_sweeps_S": S, "inner_sweeps_L": L, "dim": dim,
-            "parallelism": "replicas only" if ws > 1 else "single GPU",
+            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
             "l2": "inputs larger than L2 (one vector = %.1f MB)" % (vec_bytes / 1e6),
             "setup_s": round(setup_s, 3),
         },
@@ -313,13 +356,31 @@ def run_ours(args, ws, rank, local):
             "traffic": top_traffic,
             "algorithmic_bytes_per_launch": top_bytes, "launches_per_step": len(members),
             "ms_per_launch": top_ms,
+            "fp64_tflops": sum(kernel_flops(n, cnt, dim, S, L) for n in members) / len(members)
+                           / (top_ms * 1e-3) / 1e12,
+            "fp64_peak_tflops": fp64_peaks[kernel_pipe(members[0])],
+            "fp64_frac": sum(kernel_flops(n, cnt, dim, S, L) for n in members) / len(members)
+                         / (top_ms * 1e-3) / 1e12 / fp64_peaks[kernel_pipe(members[0])],
         },
         "step_roofline": {
             "bytes_per_step": step_bytes, "C(S,L)": c_factor(S, L), "achieved": step_gbs,
             "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
             "model": "SURVEY.md 8(d): 8*dim*C(S,L) canonical full-vector traffic",
+            "fp64_flops_per_step": 2.0 * (cnt["matvec_flops"] + cnt["apply_flops"]) + 12.0 * dim,
+            "fp64_tflops": (2.0 * (cnt["matvec_flops"] + cnt["apply_flops"]) + 12.0 * dim)
+                           / (step_ms * 1e-3) / 1e12,
         },
         "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
+        # per kernel: HBM GB/s and fraction (algorithmic passes), fp64 TF/s and fraction of
+        # the measured pipe peak (algorithmic flops; profiles/fp64_peaks.json)
+        "kernel_roofline": {
+            k: {"gbs": round(kernel_passes(k, S, L) * vec_bytes / (v * 1e-3) / 1e9, 1),
+                "hbm_frac": round(kernel_passes(k, S, L) * vec_bytes / (v * 1e-3) / 1e9 / peak, 3),
+                "tflops": round(kernel_flops(k, cnt, dim, S, L) / (v * 1e-3) / 1e12, 2),
+                "fp64_pipe": kernel_pipe(k),
+                "fp64_frac": round(kernel_flops(k, cnt, dim, S, L) / (v * 1e-3) / 1e12
+                                   / fp64_peaks[kernel_pipe(k)], 3)}
+            for k, v in kms.items()},
         "kernel_share": {k: round(v / total_ms, 4) for k, v in kms.items()},
         "gpu_launches": K * nk,
         "residual_inf": [float(hist[0]), float(hist[-1])],
@@ -375,6 +436,22 @@ def run_slabs(args, ws, rank, local):
     assert k_timed == K, (k_timed, K)
     ms = max_over_ranks(ms, dev, ws)
     sl = solver.slabs
+    # per-rank communication time of a step (halo exchanges + scalar collectives), from CUDA
+    # events around each of them in a few extra eager steps (not part of the timed region)
+    comm_ms = None
+    if ws > 1:
+        solver.comm_events = []
+        graph_was, solver.graph = solver.graph, False
+        run(3)
+        solver.graph = graph_was
+        torch.cuda.synchronize()
+        evs, solver.comm_events = solver.comm_events, None
+        mine = sum(e0.elapsed_time(e1) for e0, e1 in evs) / 3.0
+        import torch.distributed as dist
+
+        allc = [None] * ws
+        dist.all_gather_object(allc, mine)
+        comm_ms = [round(float(c), 4) for c in allc]
 
     # end to end through the public API: host numpy rhs in, host x out (gathered), K steps
     rhs_host = torch.from_numpy(ga.offset.copy()).pin_memory().numpy()
@@ -407,6 +484,7 @@ def run_slabs(args, ws, rank, local):
                    "K": ga.K, "N": ga.N, "T": ga.T, "n": ga.n, "m": ga.m,
                    "outer_sweeps_S": args.S, "inner_sweeps_L": args.L, "dim": ga.dim,
                    "parallelism": f"stage slabs x{ws}",
+                   "comm_ms_per_step_by_rank": comm_ms,
                    "slabs": [[x.lo, x.hi] for x in sl], "setup_s": round(setup_s, 3),
                    "timing": "CUDA events on the solver stream around steps W..W+K-1 of one solve",
                    "l2": "inputs larger than L2"},
@@ -493,7 +571,10 @@ def main():
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slabs", action="store_true",
-                    help="stage-slab sharded solve, one slab per rank (strong scaling)")
+                    help="stage-slab sharded solve, one slab per rank (strong scaling; the "
+                         "default for N > 1)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas of the one-context solve (weak scaling)")
     args = ap.parse_args()
     if args.S is None:
         args.S = 3 if args.config == 3 else 2
@@ -510,7 +591,8 @@ def main():
 
         dist.init_process_group("nccl")
     try:
-        line = (run_slabs if args.slabs else run_ours)(args, ws, rank, local)
+        slabs = args.slabs or (ws > 1 and not args.replicas)
+        line = (run_slabs if slabs else run_ours)(args, ws, rank, local)
         if rank == 0:
             print(json.dumps(line), flush=True)
     finally:

@@ -309,7 +309,11 @@ def _is_const(seq):
 def _stage_ids(K, N, seq_at, count, shape):
     """Per-stage ids for one field: stages holding identical data for every node share
     an id.  ``seq_at(i, j)`` returns that node's per-stage sequence or None.  Returns
-    (ids[count], per-id stacked arrays [n_ids, N, K, *shape])."""
+    (ids[count], per-id stacked arrays [n_ids, N, K, *shape]).
+
+    Vectorised: each node's sequence is converted with ONE ``np.asarray`` (a C loop over
+    its stages) into a dense [count, N, K, *shape] array, and equal stages are found with
+    one ``np.unique`` over the stage rows -- O(K N) Python calls instead of O(T K N)."""
     seqs = [[seq_at(i, j) for i in range(K)] for j in range(N)]
     if all(_is_const(s) for col in seqs for s in col if s is not None):
         ids = np.zeros(count, dtype=np.int32)
@@ -320,21 +324,22 @@ def _stage_ids(K, N, seq_at, count, shape):
                 if s is not None and len(s):
                     stack[0, j, i] = np.asarray(s[0], dtype=float)
         return ids, stack
-    ids = np.empty(count, dtype=np.int32)
-    uniq, arrays = {}, []
-    for t in range(count):
-        arr = np.zeros((N, K) + shape)
-        for j in range(N):
-            for i in range(K):
-                s = seqs[j][i]
-                if s is not None:
-                    arr[j, i] = np.asarray(s[t], dtype=float)
-        h = hashlib.sha1(arr.tobytes()).hexdigest()
-        if h not in uniq:
-            uniq[h] = len(arrays)
-            arrays.append(arr)
-        ids[t] = uniq[h]
-    return ids, np.stack(arrays)
+    dense = np.zeros((N, K, count) + shape)
+    for j in range(N):
+        for i in range(K):
+            s = seqs[j][i]
+            if s is not None:
+                dense[j, i] = np.asarray(s if not isinstance(s, ConstSeq) else [s[0]] * count,
+                                         dtype=float).reshape((count,) + shape)
+    per_t = np.ascontiguousarray(np.moveaxis(dense, 2, 0))          # [count, N, K, *shape]
+    rows = per_t.reshape(count, -1).view(np.uint8).reshape(count, -1)
+    _, first, inv = np.unique(rows, axis=0, return_index=True, return_inverse=True)
+    # ids numbered by first appearance (the order the stage loop would assign them)
+    order = np.argsort(first, kind="stable")
+    rank = np.empty_like(order)
+    rank[order] = np.arange(len(order))
+    ids = rank[inv.reshape(-1)].astype(np.int32)
+    return ids, per_t[np.sort(first)]
 
 
 _NEIGHBOR = {"west": (0, -1), "east": (0, 1), "north": (-1, 0), "south": (1, 0)}
@@ -477,38 +482,35 @@ def arrays_from_problem(problem) -> GridArrays:
 
 def rhs_offset(problem, n):
     """omega~: initial states at stage 0 plus boundary-trajectory terms at stage t+1
-    (``kkt_assembly.py:275-301``)."""
+    (``kkt_assembly.py:275-301``).  Vectorised over stages: per edge node and direction
+    the T coupling blocks and trajectory samples are stacked once and applied as one
+    batched product (``np.einsum``), not T separate matrix-vector products."""
     K, N, T = problem.K, problem.N, problem.T
-    lay = GridLayout(K, N, T, n)
-    offset = np.zeros(lay.n_total)
+    nk = K * N * n
+    offset = np.zeros((T + 1) * nk)
     bnd = problem.boundary
-    for i in range(K):
-        for j in range(N):
-            offset[lay.x_slice(i, j, 0)] = np.asarray(bnd.init[i][j], dtype=float)
+    init = np.asarray(bnd.init, dtype=float).reshape(K, N, n)        # [i][j][k]
+    offset[:nk] = np.transpose(init, (1, 0, 2)).reshape(-1)          # order (j, i, k)
     if all(getattr(bnd, d) is None for d in DIRECTIONS):
         return offset
-    edges = []
-    for i in range(K):
-        for j in range(N):
-            if i == 0 or i == K - 1 or j == 0 or j == N - 1:
-                edges.append((i, j))
-    for t in range(T):
-        for i, j in edges:
-            sub = problem.sub(i, j)
-            acc = None
-            for direction, at_edge in (("north", i == 0), ("south", i == K - 1),
-                                       ("west", j == 0), ("east", j == N - 1)):
-                blocks = sub.coupling(direction)
-                if not at_edge or blocks is None:
-                    continue
-                traj = getattr(bnd, direction)
-                if traj is None:
-                    continue
-                sig = traj[j if direction in ("north", "south") else i][t]
-                term = np.asarray(blocks[t]) @ np.asarray(sig, dtype=float)
-                acc = term if acc is None else acc + term
-            if acc is not None:
-                offset[lay.x_slice(i, j, t + 1)] += acc
+    stages = offset[nk:].reshape(T, N, K, n)                         # stages 1..T
+    for direction in ("north", "south", "west", "east"):
+        traj = getattr(bnd, direction)
+        if traj is None:
+            continue
+        if direction in ("north", "south"):
+            i = 0 if direction == "north" else K - 1
+            nodes = [(i, j, j) for j in range(N)]
+        else:
+            j = 0 if direction == "west" else N - 1
+            nodes = [(i, j, i) for i in range(K)]
+        for i, j, idx in nodes:
+            blocks = problem.sub(i, j).coupling(direction)
+            if blocks is None:
+                continue
+            Cs = np.asarray(blocks, dtype=float).reshape(T, n, n)
+            sig = np.asarray(traj[idx], dtype=float).reshape(T, n)
+            stages[:, j, i] += np.einsum("tab,tb->ta", Cs, sig)
     return offset
 
 

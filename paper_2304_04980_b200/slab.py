@@ -562,18 +562,33 @@ class SlabPcg:
         for k in self.comm.local:
             self.nat[k].call("gq_slab_phase", kind, s)
 
+    def _comm(self, fn, *args):
+        """Run one exchange / reduction; with ``comm_events`` set (a list, eager steps only)
+        bracket it with CUDA events on the solver stream so bench.py can report the step's
+        communication time per rank."""
+        ce = getattr(self, "comm_events", None)
+        if ce is None:
+            return fn(*args)
+        import torch
+
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn(*args)
+        e1.record()
+        ce.append((e0, e1))
+
     def _nstep(self, S):
         from . import _lib
 
-        self._nexchange(_lib.GQ_SLAB_VEC_D)
+        self._comm(self._nexchange, _lib.GQ_SLAB_VEC_D)
         self._nphase(_lib.GQ_SLAB_DELTA)
-        self._nreduce(_lib.GQ_SLAB_CURV, "sum")
+        self._comm(self._nreduce, _lib.GQ_SLAB_CURV, "sum")
         self._nphase(_lib.GQ_SLAB_UPDATE)
         for s in range(S):
             self._nphase(_lib.GQ_SLAB_OUTER, s)
             if s < S - 1:
-                self._nexchange(_lib.GQ_SLAB_VEC_DL0 + s % 2)
-        self._nreduce_res_mu()
+                self._comm(self._nexchange, _lib.GQ_SLAB_VEC_DL0 + s % 2)
+        self._comm(self._nreduce_res_mu)
         self._nphase(_lib.GQ_SLAB_DIRECTION)
 
     def _solve_native(self, r, x0s, tol, max_steps, host, start, callback=None):

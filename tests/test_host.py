@@ -100,3 +100,42 @@ def test_generators_are_seeded():
     m = G.config4(0, K=8, N=8, T=4)
     # spectral radius check of the MSD dynamics: stable-ish Euler discretisation
     assert m.n == 2 and m.m == 1 and np.all(np.isfinite(m.A))
+
+
+def test_time_varying_ingestion_is_vectorised():
+    """A time-varying GridLQProblem at 64 x 64 x 40 (every field per stage) converts in
+    seconds: per-node sequences are stacked with one np.asarray each and equal stages found
+    with one np.unique (problem._stage_ids), not a Python walk over T K N."""
+    import time
+
+    from paper_2304_04980_b200.problem import (BoundaryData, GridLQProblem, SubsystemData,
+                                               arrays_from_problem)
+
+    K = N = 64
+    T, n, m = 40, 2, 1
+    rng = np.random.default_rng(3)
+    A = [0.3 * rng.standard_normal((n, n)) for _ in range(T)]
+    A[7] = A[3]                                    # two stages share their dynamics
+    B = [rng.standard_normal((n, m)) for _ in range(T)]
+    B[7] = B[3]
+    Q = [np.eye(n) * (1.0 + 0.01 * t) for t in range(T + 1)]
+    R = [np.eye(m)] * T
+    Cw = [0.01 * rng.standard_normal((n, n)) for _ in range(T)]
+    Cw[7] = Cw[3]
+    subs = []
+    for i in range(K):
+        row = []
+        for j in range(N):
+            kw = {d: Cw for d, ok in (("west", j > 0), ("east", j < N - 1), ("north", i > 0),
+                                      ("south", i < K - 1)) if ok}
+            row.append(SubsystemData(n=n, m=m, A=A, B=B, Q=Q, R=R, **kw))
+        subs.append(row)
+    init = [[np.ones(n) for _ in range(N)] for _ in range(K)]
+    prob = GridLQProblem(K, N, T, subs, BoundaryData(init=init))
+    t0 = time.perf_counter()
+    ga = arrays_from_problem(prob)
+    dt = time.perf_counter() - t0
+    assert dt < 20.0, dt
+    assert len(ga.A) == T - 1 and ga.dyn_class[7] == ga.dyn_class[3]
+    assert len(ga.Q) == T + 1
+    assert np.array_equal(ga.A[ga.dyn_class[5], 10, 20], A[5])
