@@ -59,9 +59,6 @@ struct gq_ctx {
   int4* seg = nullptr;
   ChainOps co{};
   bool chain = false;          // lean DMMA chain sweeps (n in {2, 4})
-  bool chainx = false;         // n = 2: CTA-shared factor tiles (gq_chainx.cu)
-  int4* xgrp = nullptr;        // its CTA items
-  int nxgrp = 0;
   bool fuse_x = false;         // x update fused into the direction update (opt-in)
   bool fuse_r = false;         // r update fused into the first outer sweep (chain kernel)
   bool grid = false;           // lean n = 2 grid stencils
@@ -117,7 +114,7 @@ static void release(gq_ctx* c) {
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
                   c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
                   c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->xgrp, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
+                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -387,21 +384,6 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
       c->chain = true;
-      if (chainx_supported(g)) {
-        // CTA items: runs of up to chainx_warps() consecutive chunks of one class
-        std::vector<int4> grp;
-        const int W = chainx_warps();
-        for (size_t i = 0; i < s8.size();) {
-          size_t e = i + 1;
-          while (e < s8.size() && (int)(e - i) < W && s8[e].z == s8[i].z) ++e;
-          grp.push_back(make_int4((int)i, (int)(e - i), s8[i].z, 0));
-          i = e;
-        }
-        CKB(dalloc(&c->xgrp, grp.size()));
-        CKB(cudaMemcpy(c->xgrp, grp.data(), grp.size() * sizeof(int4), cudaMemcpyHostToDevice));
-        c->nxgrp = (int)grp.size();
-        c->chainx = true;
-      }
     }
   }
 
@@ -475,7 +457,6 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
                              c->st8 ? st8_max_blocks(c->sm_count) : 0LL,
                              c->chain ? (long long)c->sm_count * 2 : 0LL,
                              c->dstep ? dstep_max_blocks(c->sm_count) : 0LL,
-                             c->chainx ? (long long)g.V * c->nxgrp : 0LL,
                              c->chain ? chain_fr_max_blocks(g, c->co.nseg, c->sm_count) : 0LL,
                              c->grid ? (long long)c->gsh.blocks : 0LL});
   CKB(dalloc(&c->partials, (size_t)maxb + 32));
@@ -626,18 +607,11 @@ static int enqueue_outer(gq_ctx* c, int s, int l0, int l1, const double* rin, do
       const double* tp = l > 0 ? c->th[(l - 1) % 2] : nullptr;
       const double* dp = s > 0 ? c->dl[(s - 1) % 2] : nullptr;
       const int dm = (last && s == c->S - 1) ? dotmode : kDotNone;
-      if (fuse_y != nullptr && s == 0 && l == 0 && c->chainx) {
-        CK(launch_chainx(c->g, c->co, c->xgrp, c->nxgrp, false, rin, nullptr, ob, nullptr,
-                         c->partials, st, kDotNone, fuse_y, const_cast<double*>(rin),
-                         c->stream));
-      } else if (fuse_y != nullptr && s == 0 && l == 0) {
+      if (fuse_y != nullptr && s == 0 && l == 0) {
         // first sweep of a PCG step: r -= alpha y, max|r| and the convergence test run on
         // the staged right-hand side (the separate r-update kernel is skipped)
         CK(launch_chain_fr(c->g, c->co, const_cast<double*>(rin), fuse_y, ob, c->sm_count,
                            c->partials, st, c->stream));
-      } else if (c->chainx) {
-        CK(launch_chainx(c->g, c->co, c->xgrp, c->nxgrp, l > 0, s > 0 ? c->rs : rin, tp, ob, rin,
-                         c->partials, st, dm, nullptr, nullptr, c->stream));
       } else if (c->chain) {
         CK(launch_chain(c->g, c->co, l > 0, s > 0 ? c->rs : rin, tp, ob, rin, c->sm_count,
                         c->partials, st, dm, c->stream));
@@ -679,10 +653,7 @@ static int enqueue_precond(gq_ctx* c, const double* rin, double* out, PcgState* 
 static int launch_one_sweep(gq_ctx* c, const double* rhs, const double* th, const double* xi,
                             double* out) {
   const bool inner = th != nullptr;
-  if (c->chainx) {
-    CK(launch_chainx(c->g, c->co, c->xgrp, c->nxgrp, inner, rhs, th, out, nullptr, c->partials,
-                     nullptr, kDotNone, nullptr, nullptr, c->stream));
-  } else if (c->chain) {
+  if (c->chain) {
     CK(launch_chain(c->g, c->co, inner, rhs, th, out, nullptr, c->sm_count, c->partials,
                     nullptr, kDotNone, c->stream));
   } else if (c->fast) {

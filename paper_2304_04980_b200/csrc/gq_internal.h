@@ -133,16 +133,6 @@ long long chain_max_blocks(const Geo& g, int nseg, int sm_count);
 // cross-pair Psi blocks for the chain tiles when the fast-path operator rows are not built (n = 8)
 cudaError_t launch_build_omega(const Geo& g, int npc, const double* psi, double* omega,
                                cudaStream_t s);
-// n = 2 sweeps with CTA-shared factor tiles (gq_chainx.cu): grp = CTA items (first chunk,
-// chunk count <= chainx_warps(), class, 0), ngrp per pair; yv != nullptr: outer sweep with
-// the PCG residual update fused in (rhs = r, updated in place through rupd)
-bool chainx_supported(const Geo& g);
-int chainx_warps();
-cudaError_t launch_chainx(const Geo& g, const ChainOps& co, const int4* grp, int ngrp, bool inner,
-                          const double* rhs, const double* th, double* out, const double* rdot,
-                          double* partials, PcgState* st, int dotmode, const double* yv,
-                          double* rupd, cudaStream_t s);
-
 // outer sweep with the PCG residual update fused in (r -= alpha y, max|r|, history)
 cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const double* y,
                             double* out, int sm_count, double* partials, PcgState* st,
