@@ -436,7 +436,8 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   {
     const char* e = getenv("GQ_NO_DSTEP");
     const char* f = getenv("GQ_FORCE_V1");
-    if (dstep_supported(g) && !(e && *e == '1') && !(f && *f == '1') &&
+    if (dstep_supported(g) && dstep_preferred(g, c->sm_count) && !(e && *e == '1') &&
+        !(f && *f == '1') &&
         dstep_make_map(g, c->d, false, &c->map_d) &&
         dstep_make_map(g, c->tmp0, false, &c->map_tmp0) &&
         dstep_make_map(g, c->y, true, &c->map_y)) {

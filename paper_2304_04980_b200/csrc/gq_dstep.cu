@@ -40,6 +40,7 @@
 // Reference: gridlq/kkt_assembly.py:346-403 (SchurOperator.apply), pcg.py:99-108 (the
 // curvature y.d and alpha fused at the end).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -468,6 +469,16 @@ EncodeTiled encoder() {
 
 bool dstep_supported(const Geo& g) {
   return g.n == 2 && g.T >= 1 && g.T1 <= MAXT1 && encoder() != nullptr;
+}
+
+// Worth it when the grid fills the machine: a CTA walks its stages one barrier at a time, so
+// a grid of a few tiles is latency-bound (config 2, 16 x 16: 24 us against 8 us for the
+// lane-per-stage stencil).  GQ_DSTEP=1 forces it (tests: every golden case on this path).
+bool dstep_preferred(const Geo& g, int sm_count) {
+  const char* e = getenv("GQ_DSTEP");
+  if (e && *e == '1') return true;
+  const long long tiles = (long long)((g.K + TI - 1) / TI) * ((g.N + TJ - 1) / TJ);
+  return tiles >= sm_count / 2;
 }
 
 long long dstep_max_blocks(int sm_count) { return sm_count; }

@@ -158,6 +158,7 @@ struct DstepOps {
   const int* ccls;      // [T1] cost set of stage t
 };
 bool dstep_supported(const Geo& g);
+bool dstep_preferred(const Geo& g, int sm_count);   // large enough grid (or GQ_DSTEP=1)
 long long dstep_max_blocks(int sm_count);
 // TMA view of a stage-inner vector: input boxes (tile + halo) or output boxes (tile)
 bool dstep_make_map(const Geo& g, const double* base, bool out, CUtensorMap* m);
