@@ -53,7 +53,13 @@ namespace {
 
 using namespace as;
 
-constexpr int TI = 32, TJ = 8;               // output tile: rows x columns
+#ifndef GQ_DSTEP_TI
+#define GQ_DSTEP_TI 32
+#endif
+constexpr int TI = GQ_DSTEP_TI, TJ = 8;      // output tile: rows x columns
+// CTAs per SM: one 352-thread CTA at TI = 32 (measured: two 192-thread CTAs at TI = 16 run
+// the headline Delta in the same 0.24 ms, with 15% more shared-memory traffic for the halo)
+constexpr int MINB = TI == 16 ? 2 : 1;
 constexpr int ZI = TI + 2, ZJ = TJ + 2;      // z domain (tile + 1-node halo)
 constexpr int PI = TI + 4, PJ = TJ + 4;      // d plane (tile + 2-node halo)
 constexpr int NZ = ZI * ZJ;                  // 340 z nodes, one per thread
@@ -66,8 +72,8 @@ constexpr int YBOX = ROWB * TI * TJ;         // 16384 bytes: one chunk of the ou
 constexpr int NYB = 3;                       // output boxes in flight (TMA stores)
 constexpr int MAXT1 = 4096;                  // stage-class tables kept in shared memory
 constexpr int NZP = 2;                       // z planes (double buffered by stage parity)
-constexpr int SMEM = 1024 /*align*/ + NSLOT * BOX + NYB * YBOX + NZP * NZ * 16 + NSLOT * 8 +
-                     3 * MAXT1 * 4;
+// shared memory without the stage-class tables (3 * T1 ints, appended at launch)
+constexpr int SMEM0 = 1024 /*align*/ + NSLOT * BOX + NYB * YBOX + NZP * NZ * 16 + NSLOT * 8;
 static_assert(BOX % 1024 == 0 && YBOX % 1024 == 0, "boxes keep the 1024-byte swizzle alignment");
 
 // box coordinates: (stage offset in doubles, row, column)
@@ -210,7 +216,7 @@ __device__ __forceinline__ void load_yops(NodeOps& o, const Geo& g, const DstepO
   if (in) ld4(o.BB, op.brb + ((long long)dc * g.nk + node) * 4);
 }
 
-__global__ void __launch_bounds__(NTHR, 1) k_dstep(const __grid_constant__ CUtensorMap dmap,
+__global__ void __launch_bounds__(NTHR, MINB) k_dstep(const __grid_constant__ CUtensorMap dmap,
                                                    const __grid_constant__ CUtensorMap ymap,
                                                    const DsArgs a) {
   extern __shared__ unsigned char smem_raw[];
@@ -502,10 +508,18 @@ bool dstep_make_map(const Geo& g, const double* base, bool out, CUtensorMap* m) 
 cudaError_t launch_dstep(const Geo& g, const CUtensorMap& dmap, const CUtensorMap& ymap,
                          const DstepOps& op, double* y, double* partials, PcgState* st,
                          int dotmode, int sm_count, cudaStream_t s) {
-  static int cache[64] = {0};
+  const size_t smem = (size_t)SMEM0 + 3 * (size_t)g.T1 * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_dstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM0 + 3 * MAXT1 * 4);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   int per_sm = 1;
-  cudaError_t e = kernel_occupancy(k_dstep, NTHR, SMEM, cache, per_sm);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dstep, NTHR, smem);
   if (e != cudaSuccess) return e;
+  per_sm = std::max(per_sm, 1);
   DsArgs a;
   a.g = g;
   a.op = op;
@@ -532,7 +546,7 @@ cudaError_t launch_dstep(const Geo& g, const CUtensorMap& dmap, const CUtensorMa
   a.nr = (g.T1 + best - 1) / best;
   a.n_items = (int)(tiles * a.nr);
   const int blocks = (int)std::min<long long>(a.n_items, slots);
-  k_dstep<<<blocks, NTHR, SMEM, s>>>(dmap, ymap, a);
+  k_dstep<<<blocks, NTHR, smem, s>>>(dmap, ymap, a);
   return cudaGetLastError();
 }
 
