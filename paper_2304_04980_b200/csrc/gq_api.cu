@@ -761,8 +761,15 @@ extern "C" int gq_apply_outer_coupling(gq_ctx* c, const double* x, double* y) {
   if (!c || !x || !y) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, x, c->tmp0);
   if (rc) return rc;
-  CK(launch_stencil(c->g, c->op, kOuter, c->tmp0, c->y, c->sh_outer, c->partials, nullptr,
-                    kDotNone, c->stream));
+  // the kernel the preconditioner runs (rhs = 0 + Xi~ x) where one is selected
+  if (c->grid) {
+    CK(cudaMemsetAsync(c->tmp1, 0, c->g.dim * 8, c->stream));
+    CK(launch_grid(c->g, c->fo, kOuterRhs, c->tmp0, c->tmp1, c->y, c->gsh, c->partials,
+                   nullptr, kDotNone, c->stream));
+  } else {
+    CK(launch_stencil(c->g, c->op, kOuter, c->tmp0, c->y, c->sh_outer, c->partials, nullptr,
+                      kDotNone, c->stream));
+  }
   return export_vec(c, c->y, y);
 }
 
@@ -779,8 +786,9 @@ extern "C" int gq_pair_solve(gq_ctx* c, const double* rhs, double* out) {
   if (!c || !rhs || !out) return fail(GQ_INVALID_ARG, "null argument");
   int rc = import_vec(c, rhs, c->tmp0);
   if (rc) return rc;
-  CK(launch_sweep(c->g, c->op, false, false, c->tmp0, nullptr, nullptr, c->y, c->sw,
-                  c->partials, nullptr, kDotNone, c->stream));
+  // the sweep kernel the preconditioner runs (DMMA chains / lane-per-stage / generic)
+  rc = launch_one_sweep(c, c->tmp0, nullptr, nullptr, c->y);
+  if (rc) return rc;
   return export_vec(c, c->y, out);
 }
 

@@ -72,8 +72,13 @@ constexpr int YBOX = ROWB * TI * TJ;         // 16384 bytes: one chunk of the ou
 constexpr int NYB = 3;                       // output boxes in flight (TMA stores)
 constexpr int MAXT1 = 4096;                  // stage-class tables kept in shared memory
 constexpr int NZP = 2;                       // z planes (double buffered by stage parity)
+// Halo threads run the y body too (never stored) and read z one row / column outside the
+// domain: each plane carries a guard band of ZI + 1 entries on both sides so those reads
+// stay inside the allocation.
+constexpr int ZG = ZI + 1;
+constexpr int PZ = NZ + 2 * ZG;              // plane stride (entries)
 // shared memory without the stage-class tables (3 * T1 ints, appended at launch)
-constexpr int SMEM0 = 1024 /*align*/ + NSLOT * BOX + NYB * YBOX + NZP * NZ * 16 + NSLOT * 8;
+constexpr int SMEM0 = 1024 /*align*/ + NSLOT * BOX + NYB * YBOX + NZP * PZ * 16 + NSLOT * 8;
 static_assert(BOX % 1024 == 0 && YBOX % 1024 == 0, "boxes keep the 1024-byte swizzle alignment");
 
 // box coordinates: (stage offset in doubles, row, column)
@@ -234,8 +239,8 @@ __global__ void __launch_bounds__(NTHR, MINB) k_dstep(const __grid_constant__ CU
   }
   const unsigned base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const unsigned ybase = base + NSLOT * BOX;            // output boxes
-  const unsigned zpl = ybase + NYB * YBOX;              // z planes: NZP x NZ double2
-  const unsigned bars = zpl + NZP * NZ * 16;
+  const unsigned zpl = ybase + NYB * YBOX + ZG * 16;    // z planes: NZP x PZ double2
+  const unsigned bars = ybase + NYB * YBOX + NZP * PZ * 16;
   int* tcls = reinterpret_cast<int*>(smem_raw + (bars + NSLOT * 8 - smem_u32(smem_raw)));
   const int tid = threadIdx.x;
   const int T = g.T;
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(NTHR, MINB) k_dstep(const __grid_constant__ CU
         // y_t - z_t = B_{t-1} R_{t-1}^-1 B_{t-1}' d_t - Ahat_{t-1} z_{t-1}  (none at t = 0)
         double2 yb_ = make_double2(0.0, 0.0);
         if (t >= 1) {   // uniform
-          const unsigned zp = zpl + (unsigned)((t - 1) & 1) * NZ * 16 + zme;
+          const unsigned zp = zpl + (unsigned)((t - 1) & 1) * PZ * 16 + zme;
           const double2 zC = lds2u(zp), zN = lds2u(zp - 16), zS = lds2u(zp + 16);
           const double2 zW = lds2u(zp - ZI * 16), zE = lds2u(zp + ZI * 16);
           yb_ = mv(o.BB, dt);
@@ -384,7 +389,7 @@ __global__ void __launch_bounds__(NTHR, MINB) k_dstep(const __grid_constant__ CU
         v = mac(v, o.M[3], dW);
         v = mac(v, o.M[4], dE);
         const double2 z = mv(o.Qi, v);
-        sts2u(zpl + (unsigned)(t & 1) * NZ * 16 + zme, z);
+        sts2u(zpl + (unsigned)(t & 1) * PZ * 16 + zme, z);
         const double2 yv = add(z, yb_);
         const bool keep = yo && owned;
         const double2 ys = keep ? yv : make_double2(0.0, 0.0);   // slab halo rows stay zero
