@@ -73,12 +73,15 @@ constexpr int NYB = 3;                       // output boxes in flight (TMA stor
 constexpr int MAXT1 = 4096;                  // stage-class tables kept in shared memory
 constexpr int NZP = 2;                       // z planes (double buffered by stage parity)
 // Halo threads run the y body too (never stored) and read z one row / column outside the
-// domain: each plane carries a guard band of ZI + 1 entries on both sides so those reads
-// stay inside the allocation.
-constexpr int ZG = ZI + 1;
-constexpr int PZ = NZ + 2 * ZG;              // plane stride (entries)
+// domain: each plane carries guard bands of >= ZI + 1 entries on both sides so those reads
+// stay inside the allocation.  Front band and stride are multiples of 8 entries, so both
+// planes start 128-byte aligned (a quarter warp's 8 consecutive LDS.128 = one wavefront).
+constexpr int ZG = (ZI + 1 + 7) / 8 * 8;                   // front guard (entries)
+constexpr int PZ = (ZG + NZ + ZI + 1 + 7) / 8 * 8;         // plane stride (entries)
+static_assert(PZ - ZG - NZ >= ZI + 1, "back guard band");
 // shared memory without the stage-class tables (3 * T1 ints, appended at launch)
 constexpr int SMEM0 = 1024 /*align*/ + NSLOT * BOX + NYB * YBOX + NZP * PZ * 16 + NSLOT * 8;
+static_assert((NSLOT * BOX + NYB * YBOX) % 128 == 0, "z planes start 128-byte aligned");
 static_assert(BOX % 1024 == 0 && YBOX % 1024 == 0, "boxes keep the 1024-byte swizzle alignment");
 
 // box coordinates: (stage offset in doubles, row, column)
