@@ -17,6 +17,7 @@
 #include <functional>
 #include <thread>
 
+#include "gq_chain.cuh"
 #include "gq_internal.h"
 #include "../../include/gridlq_b200.h"
 
@@ -364,9 +365,11 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       // class-pure chunks of <= w stages: runs of equal Psi class split into w's
       auto chunks = [&](int w) {
         std::vector<int4> segs;
+        const char* al = getenv("GQ_SEG_ALIGN");
+        const bool align = al && *al == '1';
         for (int t = 0; t < g.T1;) {
           int e = t + 1;
-          while (e < g.T1 && e - t < w && pcls[e] == pcls[t]) ++e;
+          while (e < g.T1 && e - t < w && pcls[e] == pcls[t] && !(align && e % w == 0)) ++e;
           segs.push_back(make_int4(t, e - t, pcls[t], 0));
           t = e;
         }
@@ -383,6 +386,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       CKB(cudaStreamSynchronize(c->stream));
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
+      CKB(chainm_plan(g, c->co, s8.data(), c->stream));
       c->chain = true;
     }
   }

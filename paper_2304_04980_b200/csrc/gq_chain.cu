@@ -28,8 +28,7 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include "gq_async.cuh"
-#include "gq_internal.h"
+#include "gq_chain.cuh"
 
 namespace gq {
 
@@ -41,23 +40,6 @@ __device__ __forceinline__ void stg2_keep(double* p, double2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x),
                "d"(v.y), "l"(pol)
                : "memory");
-}
-
-// theta neighbour records of a block, relative to (column a, row 2k): the twelve nodes
-// outside the pair that the 13-point Psi diamond of its four nodes reaches
-__host__ __device__ constexpr int th_dc(int r) {
-  return r < 2 ? -2 : r < 6 ? -1 : r < 10 ? 2 : 3;
-}
-__host__ __device__ constexpr int th_dr(int r) {
-  return (r == 0 || r == 3 || r == 7 || r == 10) ? 0
-       : (r == 1 || r == 4 || r == 8 || r == 11) ? 1
-       : (r == 2 || r == 6) ? -1 : 2;
-}
-// omega slot u of a node in the pair's left (dc = 0) / right (dc = 1) column -> record index
-// (before adding the node's row offset); matches the u order of k_build_rows
-__host__ __device__ constexpr int th_rec(int dc, int u) {
-  return dc == 0 ? (u == 0 ? 0 : u == 1 ? 2 : u == 2 ? 3 : u == 3 ? 4 : 7)
-                 : (u == 0 ? 3 : u == 1 ? 6 : u == 2 ? 7 : u == 3 ? 8 : 10);
 }
 
 // ---- Warp reduction for one-warp CTAs (deterministic last-block pattern) -------------------
@@ -345,7 +327,7 @@ __device__ __forceinline__ void chain_item(const Geo& g, const ChainOps& co,
           double2 s0 = make_double2(0.0, 0.0), s1 = s0;
 #pragma unroll
           for (int u = 0; u < 5; ++u) {
-            const double2 tq = lds2(sl + aofs(4 + th_rec(dc, u) + dr, 0, 2 * qd));
+            const double2 tq = lds2(sl + aofs(4 + th_rec(dc, u, dr), 0, 2 * qd));
             const double2 b = __ldg(reinterpret_cast<const double2*>(om + u * 64));
             if (u & 1) {
               dmma(s1, tq.x, b.x);
@@ -648,10 +630,6 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
 // ---- factor tiles ---------------------------------------------------------------------
 // ff[pc][v][k] = L^-1 | -G | -M (M = L^-1 Omega~, Q x 12n), fb[pc][v][k] = L^-T | -H, all as
 // 8x8 tiles; one thread per (block, row).
-__host__ __device__ __forceinline__ int tile_at(int r, int c, int kc) {
-  return ((r >> 3) * (kc >> 3) + (c >> 3)) * 64 + (r & 7) * 8 + (c & 7);
-}
-
 template <int NS>
 __global__ void k_build_chain(Geo g, int npc, const double* __restrict__ fac,
                               const double* __restrict__ omega, double* __restrict__ ff,
@@ -693,7 +671,7 @@ __global__ void k_build_chain(Geo g, int npc, const double* __restrict__ fac,
     if (col >= g.N || row >= g.K) continue;
     const double* W = omega + ((long long)pc * g.nk + (long long)col * g.K + row) * 5 * B2;
     for (int u = 0; u < 5; ++u) {
-      const int rec = th_rec(dc, u) + dr;
+      const int rec = th_rec(dc, u, dr);
       for (int c = 0; c < NS; ++c) mrow[rec * NS + c] = fma(l, W[u * B2 + fc * NS + c], mrow[rec * NS + c]);
     }
   }
@@ -798,6 +776,8 @@ static cudaError_t chain_p(const Geo& g, const ChainOps& co, const double* rhs, 
 cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
                          const double* th, double* out, const double* rdot, int sm_count,
                          double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  if (chainm_supported(g, co, sm_count))
+    return launch_chainm(g, co, inner, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 2)
     return inner ? chain_p<2, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
                  : chain_p<2, false>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
@@ -837,6 +817,8 @@ static cudaError_t chain_fr_launch(const Geo& g, const ChainOps& co, double* r, 
 cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const double* y,
                             double* out, int sm_count, double* partials, PcgState* st,
                             cudaStream_t s) {
+  if (chainm_supported(g, co, sm_count))
+    return launch_chainm_fr(g, co, r, y, out, sm_count, partials, st, s);
   if (g.n == 2)
     return chain_fr_launch<2, 7>(g, co, r, y, out, sm_count, partials, st, s);
   if (g.n == 4) return chain_fr_launch<4, 3>(g, co, r, y, out, sm_count, partials, st, s);

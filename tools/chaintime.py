@@ -16,7 +16,7 @@ def timed(pc, v, n=10):
     return e0.elapsed_time(e1) / n
 
 
-ga = generators.config4(0)
+ga = generators.config4(0, T=int(os.environ.get("CT_T", "200")))
 v = None
 for var in (sys.argv[1:] or [""]):
     env = dict(kv.split("=") for kv in var.split(",") if kv)
