@@ -17,7 +17,6 @@
 #include <functional>
 #include <thread>
 
-#include "gq_chain.cuh"
 #include "gq_internal.h"
 #include "../../include/gridlq_b200.h"
 
@@ -53,6 +52,8 @@ struct gq_ctx {
   double *x = nullptr, *r = nullptr, *d = nullptr, *y = nullptr, *q = nullptr;
   double *th[2] = {nullptr, nullptr}, *dl[2] = {nullptr, nullptr};
   double *tmp0 = nullptr, *tmp1 = nullptr;
+  int t0pad = 0;                    // stages of zero padding in front of every work vector
+  std::vector<double*> vec_bases;   // their allocations (the vectors start t0pad stages in)
   double* rs = nullptr;        // r + Xi~ delta of the current outer sweep (fast path)
   double *oprow = nullptr, *omega = nullptr, *fac3 = nullptr, *fac4 = nullptr;
   FastOps fo{};
@@ -113,10 +114,10 @@ static void release(gq_ctx* c) {
   for (auto& ge : c->gexec)
     if (ge) cudaGraphExecDestroy(ge);
   void* ptrs[] = {c->A, c->B, c->R, c->C, c->Q, c->qinv, c->rinv, c->brb, c->psi, c->xi,
-                  c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->x,
-                  c->r, c->d, c->y, c->q, c->th[0], c->th[1], c->dl[0], c->dl[1], c->tmp0,
-                  c->tmp1, c->rs, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
+                  c->xit, c->fac, c->psi_cls, c->xi_cls, c->psi_keys, c->xi_keys, c->oprow, c->omega, c->fac3, c->fac4, c->cff, c->cfb, c->seg, c->dcls, c->ccls, c->partials, c->st, c->hist, c->err};
   for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (double* p : c->vec_bases)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -239,6 +240,18 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       pkeys.insert(pkeys.end(), key.begin(), key.end());
     }
     pcls[t] = it->second;
+  }
+  // Stage stride and front padding of the device vectors: the stage where the long class run
+  // starts (1 when stage 0 is a class of its own, as for every time-invariant problem) sits
+  // on a 128-byte boundary of the allocation and every node spans a multiple of 8 stages, so
+  // the 8-stage records the chain sweeps move are whole 128-byte lines (GQ_NO_PAD=1: dense).
+  {
+    const char* np = getenv("GQ_NO_PAD");
+    const int first = (g.T1 > 1 && pcls[0] != pcls[1]) ? 1 : 0;
+    c->t0pad = (np && *np == '1') ? 0 : (8 - first) % 8;
+    g.TS = (np && *np == '1') ? g.T1 : (c->t0pad + g.T1 + 7) / 8 * 8;
+    g.T0 = c->t0pad;
+    g.span = (g.nk - 1) * (long long)g.TS * g.n + (long long)g.T1 * g.n;
   }
   std::map<std::array<int, 2>, int> xmap;
   std::vector<int> xcls(std::max(g.T, 1)), xkeys;
@@ -365,11 +378,9 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       // class-pure chunks of <= w stages: runs of equal Psi class split into w's
       auto chunks = [&](int w) {
         std::vector<int4> segs;
-        const char* al = getenv("GQ_SEG_ALIGN");
-        const bool align = al && *al == '1';
         for (int t = 0; t < g.T1;) {
           int e = t + 1;
-          while (e < g.T1 && e - t < w && pcls[e] == pcls[t] && !(align && e % w == 0)) ++e;
+          while (e < g.T1 && e - t < w && pcls[e] == pcls[t]) ++e;
           segs.push_back(make_int4(t, e - t, pcls[t], 0));
           t = e;
         }
@@ -386,7 +397,6 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       CKB(cudaStreamSynchronize(c->stream));
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
-      CKB(chainm_plan(g, c->co, s8.data(), c->stream));
       c->chain = true;
     }
   }
@@ -430,10 +440,16 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
     c->fuse_r = c->chain && g.n != 8 && !(e && *e == '1');
   }
   // work vectors (stage-inner layout) and the reference-layout staging buffers
-  const size_t dim = (size_t)g.dim;
+  const size_t vlen = (size_t)g.nk * g.TS * g.n + (size_t)(c->t0pad + 8) * g.n;
   double** vecs[] = {&c->x, &c->r, &c->d, &c->y, &c->q, &c->th[0], &c->th[1],
                      &c->dl[0], &c->dl[1], &c->tmp0, &c->tmp1, &c->rs};
-  for (double** p : vecs) CKB(dalloc(p, dim));
+  for (double** p : vecs) {
+    double* base = nullptr;
+    CKB(dalloc(&base, vlen));
+    c->vec_bases.push_back(base);
+    CKB(cudaMemset(base, 0, vlen * sizeof(double)));   // the padding stages stay zero
+    *p = base + (size_t)c->t0pad * g.n;
+  }
   c->sh_delta = stencil_shape(g, kDelta, c->sm_count);
   c->grid = c->fast && grid_supported(g.n);
   if (c->grid) c->gsh = grid_shape(g, c->sm_count);
@@ -767,7 +783,7 @@ extern "C" int gq_apply_outer_coupling(gq_ctx* c, const double* x, double* y) {
   if (rc) return rc;
   // the kernel the preconditioner runs (rhs = 0 + Xi~ x) where one is selected
   if (c->grid) {
-    CK(cudaMemsetAsync(c->tmp1, 0, c->g.dim * 8, c->stream));
+    CK(cudaMemsetAsync(c->tmp1, 0, c->g.span * 8, c->stream));
     CK(launch_grid(c->g, c->fo, kOuterRhs, c->tmp0, c->tmp1, c->y, c->gsh, c->partials,
                    nullptr, kDotNone, c->stream));
   } else {
@@ -926,17 +942,17 @@ extern "C" int gq_pcg_start(gq_ctx* c, const double* rhs, const double* x0, int3
     CK(launch_stencil(c->g, c->op, kDelta, c->x, c->y, c->sh_delta, c->partials, nullptr,
                       kDotNone, c->stream));
     CK(launch_sub(c->g, c->tmp0, c->r, c->y, c->vblocks, c->stream));
-    CK(cudaMemcpyAsync(c->r, c->tmp0, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->r, c->tmp0, c->g.span * 8, cudaMemcpyDeviceToDevice, c->stream));
   } else {
-    CK(cudaMemsetAsync(c->x, 0, c->g.dim * 8, c->stream));
+    CK(cudaMemsetAsync(c->x, 0, c->g.span * 8, c->stream));
   }
   if (use_precond) {
     // d = P r ; mu = d.r   (pcg.py:87-93)
     rc = enqueue_precond(c, c->r, c->q, c->st, kDotInit, nullptr);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(c->d, c->q, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d, c->q, c->g.span * 8, cudaMemcpyDeviceToDevice, c->stream));
   } else {
-    CK(cudaMemcpyAsync(c->d, c->r, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d, c->r, c->g.span * 8, cudaMemcpyDeviceToDevice, c->stream));
     CK(launch_dot(c->g, c->d, c->r, c->vblocks, c->partials, c->st, kDotInit, c->stream));
   }
   CK(cudaStreamSynchronize(c->stream));
@@ -1107,7 +1123,7 @@ extern "C" int gq_slab_start(gq_ctx* c, const double* r0, const double* x0, int3
   if (x0) {
     if ((rc = import_vec(c, x0, c->x))) return rc;
   } else {
-    CK(cudaMemsetAsync(c->x, 0, c->g.dim * 8, c->stream));
+    CK(cudaMemsetAsync(c->x, 0, c->g.span * 8, c->stream));
   }
   c->started = true;
   return GQ_OK;
@@ -1125,12 +1141,12 @@ extern "C" int gq_slab_phase(gq_ctx* c, int32_t kind, int32_t s) {
         if (s < 0 || s >= c->S) return fail(GQ_INVALID_ARG, "outer sweep index out of range");
         rc = enqueue_outer(c, s, 0, c->L, c->r, c->q, c->st, kDotInit, nullptr, none, nullptr);
       } else {
-        CK(cudaMemcpyAsync(c->d, c->r, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->d, c->r, c->g.span * 8, cudaMemcpyDeviceToDevice, c->stream));
         CK(launch_dot(c->g, c->d, c->r, c->vblocks, c->partials, c->st, kDotInit, c->stream));
       }
       break;
     case GQ_SLAB_INIT_FINISH:
-      if (pc) CK(cudaMemcpyAsync(c->d, c->q, c->g.dim * 8, cudaMemcpyDeviceToDevice, c->stream));
+      if (pc) CK(cudaMemcpyAsync(c->d, c->q, c->g.span * 8, cudaMemcpyDeviceToDevice, c->stream));
       break;
     case GQ_SLAB_DELTA:        // y = Delta d, partial y.d over the owned stages
       if ((rc = enqueue_delta_step(c))) return rc;

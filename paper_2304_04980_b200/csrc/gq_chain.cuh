@@ -35,10 +35,9 @@ __host__ __device__ __forceinline__ int tile_at(int r, int c, int kc) {
   return ((r >> 3) * (kc >> 3) + (c >> 3)) * 64 + (r & 7) * 8 + (c & 7);
 }
 
-// ---- chain sweeps with CTA-shared factor tiles, n = 2 (gq_chainm.cu) ----
-// sets co.cm / co.s0 from the host copy of co.seg (call once after the tiles are built)
-cudaError_t chainm_plan(const Geo& g, ChainOps& co, const int4* host_segs, cudaStream_t s);
-bool chainm_supported(const Geo& g, const ChainOps& co, int sm_count);
+// ---- twelve-warp chain sweeps with carried theta fragments, n = 2 (gq_chainm.cu) ----
+bool chainm_supported(const Geo& g, int sm_count);
+bool chainm_all();   // GQ_CHAINM=2: every sweep form on the twelve-warp kernel (tests)
 cudaError_t launch_chainm(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
                           const double* th, double* out, const double* rdot, int sm_count,
                           double* partials, PcgState* st, int dotmode, cudaStream_t s);

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(32 * W, INNER ? 1 : 2) k_chain8c(Geo g, ChainO
   const unsigned fbuf_u = smem_u32(fbuf), ring_u = smem_u32(ring);
   const uint64_t pol_k = pol_last();
   const bool dotting = dotmode != kDotNone;
-  const long long rs = (long long)g.T1 * NS8, cs = (long long)g.K * rs, rs2 = 2 * rs;
+  const long long rs = (long long)g.TS * NS8, cs = (long long)g.K * rs, rs2 = 2 * rs;
   const int nb = g.nb, K = g.K;
   double dot = 0.0;
 

@@ -1,4 +1,4 @@
-// Pair-chain sweeps on the fp64 tensor cores, CTA-shared factor tiles (n = 2).
+// Pair-chain sweeps on the fp64 tensor cores for n = 2 grids that fill the machine.
 //
 // Same recurrences and the same arithmetic as gq_chain.cu (block_linalg.py:336-358,
 // nested_jacobi.py:85-103):
@@ -6,24 +6,27 @@
 //   forward   w_k = L_k^-1 tau_k  - (L_k^-1 Omega~_k) theta  - G_k w_{k-1}
 //   backward  x_k = L_k^-T w_k    - H_k x_{k+1}
 //
-// with 8 consecutive stages of one column pair on the M dimension of m8n8k4 DMMAs.  The
-// per-warp kernel of gq_chain.cu copies each block's factor tiles (3.5 KB) and twelve theta
-// neighbour records per warp: 8-9 KB through L2 and ~125 L1 wavefronts per block for 2.5-3 KB
-// of vector data, and it runs at the L2 -> SM and L1 data-pipe limits.  Here:
+// with 8 consecutive stages of one column pair on the M dimension of m8n8k4 DMMAs, records
+// and factor tiles staged per warp by cp.async P blocks ahead.  What differs from the per-warp
+// kernel of gq_chain.cu:
 //
-//   * A CTA (the only one of its SM) takes up to W stage chunks of ONE column pair and one
-//     stage class.  A producer warp streams the pair's factor tiles block by block into a
-//     D-slot shared-memory ring with bulk (TMA) copies, one copy per CTA and block instead of
-//     one per warp; the W consumer warps read their B fragments from the ring.  full/empty
-//     mbarriers per slot couple the warps only loosely: a warp may run D - 2 blocks ahead of
-//     the slowest one.
 //   * The theta records of the two middle columns at rows 2k+1, 2k+2 are the rows -1, 0 of the
-//     next block: their A fragments are carried in registers, so a block fetches eight theta
-//     records instead of twelve (record order in gq_chain.cuh).
-//   * Only the records go through the per-warp cp.async ring (1.9 KB per slot).
-//   * The loop-carried G w / H x products are issued first in each block.
-//   * Stage 0 (Psi_0 = Q_0^-1: block-diagonal, no coupling along the chain or across pairs,
-//     verified on the device at setup) is solved apart, one thread per block.
+//     next block: their A fragments are carried in registers, so an inner sweep fetches eight
+//     theta records per block instead of twelve (record order in gq_chain.cuh).  The ring slot
+//     shrinks from 5.0 to 4.4 KB, and with P = 3 twelve warps fit on an SM instead of eight:
+//     the 3328 items of the headline run in two full rounds of 1776 warps instead of three
+//     rounds of 1184 (inner sweep 0.257 -> 0.236 ms).
+//   * A CTA is W = 12 independent warps (one CTA per SM, no barrier inside the sweep); the last
+//     round spreads its items evenly over the CTAs.
+//   * w is parked and x written with L1 no-allocate stores.
+//
+// Measured and dropped on the way (round 2, all parity-green): B fragments read straight from
+// global memory through L1 with the warps of an SM on one pair (L2 traffic -40%, but L1TEX
+// returns the hits behind the outstanding record copies: 0.31 ms; with a register ring P
+// blocks deep the loads share too few scoreboards: 0.44 ms), L1-allocating factor copies
+// (cp.async.ca: same time as the per-warp kernel, the L1 data pipe carries every tile three
+// times), and a CTA-shared factor-tile ring fed by bulk copies on full/empty mbarriers
+// (0.32 ms: 137 instructions per block and warp).
 #include <algorithm>
 #include <cstdlib>
 
@@ -44,25 +47,23 @@ __device__ __forceinline__ void stg2_out(double* p, double2 v) {
   asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(v.x), "d"(v.y)
                : "memory");
 }
+// factor tiles: plain 16-byte global -> shared copy (L1 bypassed)
+__device__ __forceinline__ void ldgsts_f(unsigned dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
 // vector data read once (prologue fragments): bypass L1
 __device__ __forceinline__ double2 ldcg2(const double* p) {
   return __ldcg(reinterpret_cast<const double2*>(p));
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
 
-template <bool INNER, bool FR, bool DOT>
+template <int NS, bool INNER, bool FR, bool DOT>
 struct Cm {
-  static constexpr int NS = 2;
-  static constexpr int Q = 4 * NS, QQ = Q * Q;
+  static constexpr int Q = 4 * NS, QQ = Q * Q, NT = Q / 8;
   static constexpr int TC = 12 * NS;                  // theta feature count of the M tile
   static constexpr int KT = TC / 8;                   // its k-pairs ...
   static constexpr int KC = KT / 3;                   // ... of which the first KC are carried
   static constexpr int FFS = 2 * QQ + Q * TC;         // forward factor doubles per block
-  static constexpr int FF = INNER ? FFS : 2 * QQ;     // ... used by this sweep
   static constexpr int FB = 2 * QQ;                   // backward factor doubles per block
-  static constexpr int TS = FF > FB ? FF : FB;        // doubles per tile-ring slot
   static constexpr int REC = 8 * NS;                  // record: 8 stages x NS
   static constexpr int RSTR = REC + 2 * NS;           // padded stride (conflict-free A reads)
   static constexpr int CPR = REC / 2;                 // 16-byte chunks per record
@@ -71,33 +72,25 @@ struct Cm {
   static constexpr int NRF = INNER ? 12 : (FR ? 8 : 4);
   static constexpr int NRB = DOT ? 8 : 4;             // backward: w (4) [+ r (4) for q.r]
   static constexpr int JF = NRF / RPI, JB = NRB / RPI;
-  static constexpr int SLOT = (NRF > NRB ? NRF : NRB) * RSTR;   // doubles per record slot
+  static constexpr int FF = INNER ? FFS : 2 * QQ;     // forward factor doubles staged
+  static constexpr int CFF = FF / 64, CFB = FB / 64;  // factor copy instructions (32 x 16 B)
+  static constexpr int SLOT = (NRF * RSTR + FF) > (NRB * RSTR + FB) ? (NRF * RSTR + FF)
+                                                                     : (NRB * RSTR + FB);
+  static_assert(NS == 2 || NS == 4, "multi-warp chain sweep: n in {2, 4}");
 };
 
-// what a sweep reads and writes besides the chain itself
-struct SweepIo {
-  const double* rhs;
-  const double* th;
-  double* out;
-  const double* rdot;
-  const double* yv;
-  double* rupd;
-  double alpha;
-};
-
-// One chain (8 stages of pair v from stage t0) forward and backward.  `tiles` is the CTA's
-// factor ring; step q of the CTA's tile stream (q0 + k forward, q0 + nb + (nb-1-k) backward)
-// lives in slot q % D.
-template <bool INNER, bool FR, bool DOT, int P, int D>
-__device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, double* ring,
-                                            const double* tiles, uint64_t* full,
-                                            uint64_t* empty, unsigned q0, int v, int t0,
-                                            int nvalid, uint64_t pol_k, double& dot,
-                                            double& rmax) {
-  using C = Cm<INNER, FR, DOT>;
-  constexpr int NS = 2, QQ = C::QQ, KT = C::KT, KC = C::KC, REC = C::RSTR, R = P + 1;
+template <int NS, bool INNER, int P, bool FR, bool DOT>
+__device__ __forceinline__ void chainm_item(const Geo& g, const ChainOps& co,
+                                            const double* __restrict__ rhs,
+                                            const double* __restrict__ th, double* out,
+                                            const double* __restrict__ rdot, double* ring, int v,
+                                            int t0, int nvalid, int cls, uint64_t pol_k,
+                                            double& dot, const double* __restrict__ yv,
+                                            double* rupd, double alpha, double& rmax) {
+  using C = Cm<NS, INNER, FR, DOT>;
+  constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, KC = C::KC, REC = C::RSTR, R = P + 1;
   const int lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
-  const long long rs = (long long)g.T1 * NS;
+  const long long rs = (long long)g.TS * NS;
   const long long cs = (long long)g.K * rs;
   const long long rs2 = 2 * rs;
   const int nb = g.nb, K = g.K;
@@ -109,10 +102,8 @@ __device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, dou
   const bool stage_ok = wst < nvalid;
   const int wofs = stage_ok ? 2 * wch : 0;               // stage-invalid lanes read stage 0
   const unsigned ring_u = smem_u32(ring);
-  const double* rhs = io.rhs;
-  // A-fragment offset of feature pair f0 = 8p + 2qd of chain rw inside a record slot
+  // A-fragment offset of feature pair f0 = 8p + 2qd of chain rw inside a slot
   auto aofs = [&](int f0) { return (f0 / NS) * REC + rw * NS + (f0 % NS); };
-  const int bofs = rw * 8 + 2 * qd;                      // my B-fragment pair inside a tile
 
   // ---------------- forward ----------------
   const double* fsrc[C::JF];
@@ -127,11 +118,14 @@ __device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, dou
     fsz[j] = (colok && stage_ok) ? 16 : 0;
     frow[j] = dr;
     // off-grid columns are redirected to the pair's own column (never read: size 0)
-    fsrc[j] = (r < 4 ? rhs : (FR ? io.yv : io.th)) + col_a + (long long)(colok ? dc : 0) * cs +
+    fsrc[j] = (r < 4 ? rhs : (FR ? yv : th)) + col_a + (long long)(colok ? dc : 0) * cs +
               (long long)dr * rs + wofs;
   }
   // per-lane shared destination, kept in a vector register (no [R + UR] LDGSTS forms)
   const unsigned rec_dst = lane_opaque(ring_u + (unsigned)(((lane / C::CPR) * REC + 2 * wch) * 8));
+  const unsigned facf_dst = lane_opaque(ring_u + (unsigned)(C::NRF * REC * 8 + 16 * lane));
+  const unsigned facb_dst = lane_opaque(ring_u + (unsigned)(C::NRB * REC * 8 + 16 * lane));
+  const double* ffb = co.ff + ((long long)cls * g.V + v) * nb * C::FFS + 2 * lane;
 
   // last block (and the prologue): rows outside [0, K) zero-fill
   auto issue_f_chk = [&](int k, int slot) {
@@ -141,24 +135,36 @@ __device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, dou
       const bool ok = fsz[j] && 2 * k + frow[j] < K;
       ldgsts(rec_dst + sb + j * C::RPI * REC * 8, ok ? fsrc[j] + k * rs2 : rhs, ok ? 16 : 0, 0);
     }
+    const double* fp = ffb + (long long)k * C::FFS;
+#pragma unroll
+    for (int i = 0; i < C::CFF; ++i) ldgsts_f(facf_dst + sb + 512 * i, fp + 64 * i);
   };
 
-  double2 wd = make_double2(0.0, 0.0);
+  double2 wd[NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) wd[h] = make_double2(0.0, 0.0);
 
-  // output fragment addressing: lane holds features 2qd, 2qd+1 (node qd) of chain (stage) rw
-  const int orow = qd >> 1;
-  const long long oofs = col_a + (long long)(qd & 1) * cs + (long long)orow * rs + rw * NS;
-  const bool ook = rw < nvalid && ((qd & 1) ? okb : true);
+  // output fragment addressing: lane holds features 8h + 2qd, +1 of chain (stage) rw
+  long long oofs[NT];
+  bool ook[NT];
+  int orow[NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) {
+    const int f0 = 8 * h + 2 * qd, nd = f0 / NS, cc = f0 % NS;
+    orow[h] = nd >> 1;
+    oofs[h] = col_a + (long long)(nd & 1) * cs + (long long)(nd >> 1) * rs + rw * NS + cc;
+    ook[h] = rw < nvalid && ((nd & 1) ? okb : true);
+  }
 
   // carried theta fragments of block 0: rows -1 (zero) and 0 of the two middle columns
-  double2 carry[KC];
+  double2 carry[KC > 0 ? KC : 1];
   if constexpr (INNER) {
 #pragma unroll
     for (int p = 0; p < KC; ++p) {
       const int f0 = 8 * p + 2 * qd, rec = f0 / NS, cc = f0 % NS;
       const int dc = th_dc(rec), dr = th_dr(rec);
       const bool ok = dr == 0 && a + dc >= 0 && a + dc < g.N && rw < nvalid;
-      carry[p] = ok ? ldcg2(io.th + col_a + (long long)dc * cs + rw * NS + cc)
+      carry[p] = ok ? ldcg2(th + col_a + (long long)dc * cs + rw * NS + cc)
                     : make_double2(0.0, 0.0);
     }
   }
@@ -177,11 +183,11 @@ __device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, dou
   const double* fcur[C::JF];
 #pragma unroll
   for (int j = 0; j < C::JF; ++j) fcur[j] = fsz[j] ? fsrc[j] + (long long)P * rs2 : rhs;
+  const double* fpc = ffb + (long long)P * C::FFS;
 
   int slot = 0, islot = P % R;
-  unsigned q = q0;
 #pragma unroll 1
-  for (int k = 0; k < nb; ++k, ++q) {
+  for (int k = 0; k < nb; ++k) {
     const int kk = k + P;
     if (kk < nb) {
       if (kk == nb - 1) {
@@ -191,80 +197,98 @@ __device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, dou
 #pragma unroll
         for (int j = 0; j < C::JF; ++j)
           ldgsts(rec_dst + sb + j * C::RPI * REC * 8, fcur[j], fsz[j], 0);
+#pragma unroll
+        for (int i = 0; i < C::CFF; ++i) ldgsts_f(facf_dst + sb + 512 * i, fpc + 64 * i);
       }
     }
     commit();
 #pragma unroll
     for (int j = 0; j < C::JF; ++j)
       if (fsz[j]) fcur[j] += rs2;
-    // this block's factor tiles: L^-1 | -G | -M
-    const unsigned ts = q % D;
-    mbar_wait(full + ts, (q / D) & 1u);
-    __syncwarp();
-    const double* sf = tiles + ts * C::TS + bofs;
-    const double2 bl = lds2(sf), bg = lds2(sf + QQ);
-    double2 bm[INNER ? KT : 1];
-    if constexpr (INNER) {
-#pragma unroll
-      for (int p = 0; p < KT; ++p) bm[p] = lds2(sf + 2 * QQ + p * 64);
-    }
-    // loop-carried product first: -G w_{k-1}
-    double2 g0 = make_double2(0.0, 0.0), g1 = g0;
-    dmma(g0, wd.x, bg.x);
-    dmma(g1, wd.y, bg.y);
+    fpc += C::FFS;
     wait_groups<P>();
     __syncwarp();
 
     const double* sl = ring + slot * C::SLOT;
-    double2 tv = lds2(sl + aofs(2 * qd));
+    const double* sf = sl + C::NRF * REC + rw * 8 + 2 * qd;
+    // loop-carried products first: -G w_{k-1}
+    double2 g0[NT], g1[NT];
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      g0[h] = g1[h] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const double2 b = lds2(sf + QQ + (h * NT + p) * 64);
+        dmma(g0[h], wd[p].x, b.x);
+        dmma(g1[h], wd[p].y, b.y);
+      }
+    }
+    double2 tv[NT];
+#pragma unroll
+    for (int p = 0; p < NT; ++p) tv[p] = lds2(sl + aofs(8 * p + 2 * qd));
     if constexpr (FR) {
       // r -= alpha y (pcg.py:111) on the staged records; the updated residual is this sweep's
       // right-hand side, is written back, and feeds max|r| (pcg.py:113)
-      const double2 yy = lds2(sl + 4 * REC + aofs(2 * qd));
-      tv.x = __dsub_rn(tv.x, __dmul_rn(io.alpha, yy.x));
-      tv.y = __dsub_rn(tv.y, __dmul_rn(io.alpha, yy.y));
-      if (ook && !(k == nb - 1 && 2 * k + orow >= K)) {
-        stg2_out(io.rupd + oofs + (long long)k * rs2, tv);
-        rmax = nmax(rmax, nmax(fabs(tv.x), fabs(tv.y)));
+      const bool lastk_ = k == nb - 1;
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const double2 yy = lds2(sl + 4 * REC + aofs(8 * p + 2 * qd));
+        tv[p].x = __dsub_rn(tv[p].x, __dmul_rn(alpha, yy.x));
+        tv[p].y = __dsub_rn(tv[p].y, __dmul_rn(alpha, yy.y));
+        if (ook[p] && !(lastk_ && 2 * k + orow[p] >= K)) {
+          stg2_out(rupd + oofs[p] + (long long)k * rs2, tv[p]);
+          rmax = nmax(rmax, nmax(fabs(tv[p].x), fabs(tv[p].y)));
+        }
       }
     }
-    double2 a0 = make_double2(0.0, 0.0), a1 = a0, m0 = a0, m1 = a0, m2 = a0, m3 = a0;
-    dmma(a0, tv.x, bl.x);
-    dmma(a1, tv.y, bl.y);
+    double2 tq[INNER ? KT : 1];
     if constexpr (INNER) {
-      double2 tq[KT];
 #pragma unroll
       for (int p = 0; p < KC; ++p) tq[p] = carry[p];
 #pragma unroll
       for (int p = KC; p < KT; ++p) tq[p] = lds2(sl + aofs(8 * p + 2 * qd));
 #pragma unroll
       for (int p = 0; p < KC; ++p) carry[p] = tq[KC + p];
+    }
 #pragma unroll
-      for (int p = 0; p < KT; ++p) {
-        if (p & 1) {
-          dmma(m2, tq[p].x, bm[p].x);
-          dmma(m3, tq[p].y, bm[p].y);
-        } else {
-          dmma(m0, tq[p].x, bm[p].x);
-          dmma(m1, tq[p].y, bm[p].y);
+    for (int h = 0; h < NT; ++h) {
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0, m0 = a0, m1 = a0, m2 = a0, m3 = a0;
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const double2 b = lds2(sf + (h * NT + p) * 64);
+        dmma(a0, tv[p].x, b.x);
+        dmma(a1, tv[p].y, b.y);
+      }
+      if constexpr (INNER) {
+#pragma unroll
+        for (int p = 0; p < KT; ++p) {
+          const double2 b = lds2(sf + 2 * QQ + (h * KT + p) * 64);
+          if (p & 1) {
+            dmma(m2, tq[p].x, b.x);
+            dmma(m3, tq[p].y, b.y);
+          } else {
+            dmma(m0, tq[p].x, b.x);
+            dmma(m1, tq[p].y, b.y);
+          }
         }
       }
+      double2 sm = add2(a0, a1);
+      if constexpr (INNER) sm = add2(sm, add2(add2(m0, m1), add2(m2, m3)));
+      wd[h] = add2(sm, add2(g0[h], g1[h]));
     }
-    // every B fragment of the slot has been consumed by an issued DMMA: release it
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + ts);
-    double2 sm = add2(a0, a1);
-    if constexpr (INNER) sm = add2(sm, add2(add2(m0, m1), add2(m2, m3)));
-    wd = add2(sm, add2(g0, g1));
-    if (ook && !(k == nb - 1 && 2 * k + orow >= K))
-      stg2_park(io.out + oofs + (long long)k * rs2, wd, pol_k);
+    const bool lastk = k == nb - 1;
+#pragma unroll
+    for (int h = 0; h < NT; ++h)
+      if (ook[h] && !(lastk && 2 * k + orow[h] >= K))
+        stg2_park(out + oofs[h] + (long long)k * rs2, wd[h], pol_k);
     slot = slot + 1 == R ? 0 : slot + 1;
     islot = islot + 1 == R ? 0 : islot + 1;
     __syncwarp();
   }
   wait_groups<0>();
   // w was stored by other lanes of this warp: order the stores before the copies that read
-  // them back.  CTA scope is enough (same SM, L1 bypassed both ways).
+  // them back.  CTA scope is enough (same SM, L1 bypassed both ways), and a GPU-scope fence
+  // would invalidate the L1 lines of the factor tiles for every warp of the SM.
   __threadfence_block();
   __syncwarp();
 
@@ -278,9 +302,10 @@ __device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, dou
     const bool ok = stage_ok && (dc ? okb : true);
     bsz[j] = ok ? 16 : 0;
     brow[j] = dr;
-    bsrc[j] = (r < 4 ? (const double*)io.out : io.rdot) + col_a +
-              (long long)(dc && okb ? 1 : 0) * cs + (long long)dr * rs + wofs;
+    bsrc[j] = (r < 4 ? (const double*)out : rdot) + col_a + (long long)(dc && okb ? 1 : 0) * cs +
+              (long long)dr * rs + wofs;
   }
+  const double* fbb = co.fb + ((long long)cls * g.V + v) * nb * C::FB + 2 * lane;
   auto issue_b_chk = [&](int k, int slot_) {
     const unsigned sb = lane_opaque((unsigned)(slot_ * C::SLOT * 8));
 #pragma unroll
@@ -288,6 +313,9 @@ __device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, dou
       const bool ok = bsz[j] && 2 * k + brow[j] < K;
       ldgsts(rec_dst + sb + j * C::RPI * REC * 8, ok ? bsrc[j] + k * rs2 : rhs, ok ? 16 : 0, 0);
     }
+    const double* fp = fbb + (long long)k * C::FB;
+#pragma unroll
+    for (int i = 0; i < C::CFB; ++i) ldgsts_f(facb_dst + sb + 512 * i, fp + 64 * i);
   };
   {
     const int pro = P < nb ? P : nb;
@@ -303,52 +331,71 @@ __device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, dou
 #pragma unroll
   for (int j = 0; j < C::JB; ++j)
     bcur[j] = bsz[j] ? bsrc[j] + (long long)(nb - 1 - P) * rs2 : rhs;
+  const double* fbc = fbb + (long long)(nb - 1 - P) * C::FB;
 
-  double2 xd = make_double2(0.0, 0.0);
+  double2 xd[NT];
+#pragma unroll
+  for (int h = 0; h < NT; ++h) xd[h] = make_double2(0.0, 0.0);
   slot = 0;
   islot = P % R;
 #pragma unroll 1
-  for (int k = nb - 1; k >= 0; --k, ++q) {
+  for (int k = nb - 1; k >= 0; --k) {
     const int kk = k - P;
     if (kk >= 0) {
       const unsigned sb = lane_opaque((unsigned)(islot * C::SLOT * 8));
 #pragma unroll
       for (int j = 0; j < C::JB; ++j)
         ldgsts(rec_dst + sb + j * C::RPI * REC * 8, bcur[j], bsz[j], 0);
+#pragma unroll
+      for (int i = 0; i < C::CFB; ++i) ldgsts_f(facb_dst + sb + 512 * i, fbc + 64 * i);
     }
     commit();
 #pragma unroll
     for (int j = 0; j < C::JB; ++j)
       if (bsz[j]) bcur[j] -= rs2;
-    // this block's factor tiles: L^-T | -H
-    const unsigned ts = q % D;
-    mbar_wait(full + ts, (q / D) & 1u);
-    __syncwarp();
-    const double* sf = tiles + ts * C::TS + bofs;
-    const double2 bl = lds2(sf), bh = lds2(sf + QQ);
-    // loop-carried product first: -H x_{k+1}
-    double2 g0 = make_double2(0.0, 0.0), g1 = g0;
-    dmma(g0, xd.x, bh.x);
-    dmma(g1, xd.y, bh.y);
+    fbc -= C::FB;
     wait_groups<P>();
     __syncwarp();
 
     const double* sl = ring + slot * C::SLOT;
-    const double2 wv = lds2(sl + aofs(2 * qd));
-    double2 a0 = make_double2(0.0, 0.0), a1 = a0;
-    dmma(a0, wv.x, bl.x);
-    dmma(a1, wv.y, bl.y);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + ts);
-    xd = add2(add2(a0, a1), add2(g0, g1));
-    if (ook && !(k == nb - 1 && 2 * k + orow >= K)) {
-      stg2_out(io.out + oofs + (long long)k * rs2, xd);
-      if constexpr (DOT) {
-        const double2 rv = lds2(sl + 4 * REC + aofs(2 * qd));
-        dot = fma(xd.x, rv.x, dot);
-        dot = fma(xd.y, rv.y, dot);
+    const double* sf = sl + C::NRB * REC + rw * 8 + 2 * qd;
+    // loop-carried products first: -H x_{k+1}
+    double2 g0[NT], g1[NT];
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      g0[h] = g1[h] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const double2 b = lds2(sf + QQ + (h * NT + p) * 64);
+        dmma(g0[h], xd[p].x, b.x);
+        dmma(g1[h], xd[p].y, b.y);
       }
     }
+    double2 wv[NT];
+#pragma unroll
+    for (int p = 0; p < NT; ++p) wv[p] = lds2(sl + aofs(8 * p + 2 * qd));
+#pragma unroll
+    for (int h = 0; h < NT; ++h) {
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+#pragma unroll
+      for (int p = 0; p < NT; ++p) {
+        const double2 b = lds2(sf + (h * NT + p) * 64);
+        dmma(a0, wv[p].x, b.x);
+        dmma(a1, wv[p].y, b.y);
+      }
+      xd[h] = add2(add2(a0, a1), add2(g0[h], g1[h]));
+    }
+    const bool lastk = k == nb - 1;
+#pragma unroll
+    for (int h = 0; h < NT; ++h)
+      if (ook[h] && !(lastk && 2 * k + orow[h] >= K)) {
+        stg2_out(out + oofs[h] + (long long)k * rs2, xd[h]);
+        if constexpr (DOT) {
+          const double2 rv = lds2(sl + 4 * REC + aofs(8 * h + 2 * qd));
+          dot = fma(xd[h].x, rv.x, dot);
+          dot = fma(xd[h].y, rv.y, dot);
+        }
+      }
     slot = slot + 1 == R ? 0 : slot + 1;
     islot = islot + 1 == R ? 0 : islot + 1;
     __syncwarp();
@@ -357,82 +404,14 @@ __device__ __forceinline__ void chains_item(const Geo& g, const SweepIo& io, dou
   __syncwarp();
 }
 
-// Stage 0 of pair v, block k, by one thread: Psi_0 = Q_0^-1 couples nothing outside the
-// block (G = H = M = 0 for its class, checked by k_cls0_check at setup), so
-// x = L^-T L^-1 tau.  Tiles of an 8 x 8 matrix are the matrix itself, row-major.
-template <bool FR, bool DOT>
-__device__ void stage0_block(const Geo& g, const ChainOps& co, const SweepIo& io, int v, int k,
-                             int t0, int cls, double& dot, double& rmax) {
-  constexpr int NS = 2, Q = 8;
-  using C = Cm<true, false, false>;
-  const int a = 2 * v;
-  double tau[Q], rr[Q];
-  long long idx[4];
-  bool ok[4];
-#pragma unroll
-  for (int nd = 0; nd < 4; ++nd) {
-    const int col = a + (nd & 1), row = 2 * k + (nd >> 1);
-    ok[nd] = col < g.N && row < g.K;
-    idx[nd] = ok[nd] ? vidx(g, col, row, t0) : 0;
-    double2 t = make_double2(0.0, 0.0);
-    if (ok[nd]) {
-      t = ldcg2(io.rhs + idx[nd]);
-      if constexpr (FR) {
-        const double2 yy = ldcg2(io.yv + idx[nd]);
-        t.x = __dsub_rn(t.x, __dmul_rn(io.alpha, yy.x));
-        t.y = __dsub_rn(t.y, __dmul_rn(io.alpha, yy.y));
-        stg2_out(io.rupd + idx[nd], t);
-        rmax = nmax(rmax, nmax(fabs(t.x), fabs(t.y)));
-      }
-    }
-    tau[NS * nd] = t.x;
-    tau[NS * nd + 1] = t.y;
-    rr[NS * nd] = rr[NS * nd + 1] = 0.0;
-    if constexpr (DOT) {
-      if (ok[nd]) {
-        const double2 r2 = ldcg2(io.rdot + idx[nd]);
-        rr[NS * nd] = r2.x;
-        rr[NS * nd + 1] = r2.y;
-      }
-    }
-  }
-  const double* F = co.ff + (((long long)cls * g.V + v) * g.nb + k) * C::FFS;
-  const double* B = co.fb + (((long long)cls * g.V + v) * g.nb + k) * C::FB;
-  double w[Q], x[Q];
-#pragma unroll
-  for (int p = 0; p < Q; ++p) {
-    double s = 0.0;
-#pragma unroll
-    for (int c = 0; c <= p; ++c) s = fma(__ldg(F + p * Q + c), tau[c], s);
-    w[p] = s;
-  }
-#pragma unroll
-  for (int p = 0; p < Q; ++p) {
-    double s = 0.0;
-#pragma unroll
-    for (int c = p; c < Q; ++c) s = fma(__ldg(B + p * Q + c), w[c], s);
-    x[p] = s;
-  }
-#pragma unroll
-  for (int nd = 0; nd < 4; ++nd)
-    if (ok[nd]) {
-      stg2_out(io.out + idx[nd], make_double2(x[NS * nd], x[NS * nd + 1]));
-      if constexpr (DOT) {
-        dot = fma(x[NS * nd], rr[NS * nd], dot);
-        dot = fma(x[NS * nd + 1], rr[NS * nd + 1], dot);
-      }
-    }
-}
-
-// Deterministic CTA + grid reduction: lane sums/maxes by butterfly, warp partials folded in
-// warp order by thread 0, CTA partials folded by the last CTA.
+// Deterministic CTA + grid reduction for W-warp CTAs: lane sums/maxes by butterfly, warp
+// partials folded in warp order by thread 0, CTA partials folded by the last CTA.
 template <bool MAX>
 __device__ bool cta_grid_reduce(double v, double* red, double* partials, unsigned int* counter,
                                 double& outv) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   v = MAX ? warp_max(v) : warp_sum(v);
   __shared__ int is_last;
-  __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -456,86 +435,34 @@ __device__ bool cta_grid_reduce(double v, double* red, double* partials, unsigne
   return lane == 0;
 }
 
-// Group = up to W consecutive chunks (co.seg[co.s0 ..], all of one class) of one pair; groups
-// of a pair are consecutive, CTA b takes groups b, b + gridDim.x, ...
-template <bool INNER, bool FR, bool DOT, int P, int W, int D>
-__global__ void __launch_bounds__(32 * (W + 1), 1)
-    k_chains(Geo g, ChainOps co, SweepIo io, double* partials, PcgState* st, int dotmode) {
-  extern __shared__ __align__(128) double smem_all[];
-  using C = Cm<INNER, FR, DOT>;
+template <int NS, bool INNER, int P, int W, bool FR, bool DOT>
+__global__ void __launch_bounds__(32 * W, 1)
+    k_chainm(Geo g, ChainOps co, const double* __restrict__ rhs, const double* __restrict__ th,
+             double* out, const double* __restrict__ rdot, int n_items, double* partials,
+             PcgState* st, int dotmode, const double* __restrict__ yv, double* rupd) {
+  extern __shared__ __align__(16) double ring_all[];
+  using C = Cm<NS, INNER, FR, DOT>;
   if (halted(st)) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* tiles = smem_all;
-  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + D * C::TS);
-  uint64_t* empty = full + D;
-  double* red = reinterpret_cast<double*>(empty + D);
-  double* ring = red + 32 + (size_t)warp * (P + 1) * C::SLOT;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < D; ++i) {
-      mbar_init(full + i, 1);
-      mbar_init(empty + i, W);
-    }
-    fence_proxy_async();
-  }
-  __syncthreads();
-  if constexpr (FR) io.alpha = st->alpha;
+  const int warp = threadIdx.x >> 5;
+  double* ring = ring_all + (size_t)warp * (P + 1) * C::SLOT;
+  double* red = ring_all + (size_t)W * (P + 1) * C::SLOT;
+  const double alpha = FR ? st->alpha : 0.0;
   double rmax = 0.0, dot = 0.0;
   const uint64_t pol_k = pol_last();
-  const int nb = g.nb;
-  const int nchunk = co.nseg - co.s0;
-  const int gpp = (nchunk + W - 1) / W;            // groups per pair
-  const int per = (nchunk + gpp - 1) / gpp;        // chunks per group (the last may be short)
-  const int ngroups = g.V * gpp;
-  const int cls = co.seg[co.s0].z;
-  unsigned q0 = 0;
+  const int nseg = co.nseg;
+  // rounds of gridDim.x * W items; the last round spreads what is left evenly over the CTAs
+  // (consecutive items, i.e. chunks of one pair, stay on one CTA)
+  const int G = gridDim.x;
 #pragma unroll 1
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x, q0 += 2u * nb) {
-    const int v = grp / gpp, h = grp - v * gpp;
-    const int c0 = co.s0 + h * per;
-    const int nact = min(per, co.nseg - c0);
-    if (warp == W) {
-      // producer: forward tiles of blocks 0..nb-1, then backward tiles of blocks nb-1..0
-      if (lane == 0) {
-        const double* ffp = co.ff + ((long long)cls * g.V + v) * nb * C::FFS;
-        const double* fbp = co.fb + ((long long)cls * g.V + v) * nb * C::FB;
-#pragma unroll 1
-        for (int i = 0; i < 2 * nb; ++i) {
-          const unsigned q = q0 + i, ts = q % D;
-          mbar_wait(empty + ts, ((q / D) & 1u) ^ 1u);
-          const bool fwd = i < nb;
-          const unsigned bytes = (fwd ? C::FF : C::FB) * 8;
-          mbar_expect_tx(full + ts, bytes);
-          bulk_g2s(tiles + ts * C::TS,
-                   fwd ? ffp + (long long)i * C::FFS : fbp + (long long)(2 * nb - 1 - i) * C::FB,
-                   bytes, full + ts);
-        }
-      }
-      __syncwarp();
-    } else {
-      if (co.s0 && warp < nact) {
-        // stage 0 of this pair: blocks [h nb / gpp, (h+1) nb / gpp) spread over the group's
-        // warps, one block per thread
-        const int b0 = (int)((long long)h * nb / gpp), b1 = (int)((long long)(h + 1) * nb / gpp);
-        const int4 s0 = co.seg[0];
-        for (int k = b0 + warp * 32 + lane; k < b1; k += nact * 32)
-          stage0_block<FR, DOT>(g, co, io, v, k, s0.x, s0.z, dot, rmax);
-        __syncwarp();
-      }
-      if (warp < nact) {
-        const int4 sg = co.seg[c0 + warp];
-        chains_item<INNER, FR, DOT, P, D>(g, io, ring, tiles, full, empty, q0, v, sg.x, sg.y,
-                                          pol_k, dot, rmax);
-      } else {
-        // no chunk for this warp in this group: keep the slot accounting going
-#pragma unroll 1
-        for (int i = 0; i < 2 * nb; ++i) {
-          const unsigned q = q0 + i, ts = q % D;
-          mbar_wait(full + ts, (q / D) & 1u);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(empty + ts);
-        }
-      }
-    }
+  for (int base = 0; base < n_items; base += G * W) {
+    const int left = n_items - base;
+    const int per = left >= G * W ? W : (left + G - 1) / G;
+    const int u = base + blockIdx.x * per + warp;
+    if (warp >= per || u >= n_items) continue;
+    const int v = u / nseg;
+    const int4 sg = co.seg[u - v * nseg];
+    chainm_item<NS, INNER, P, FR, DOT>(g, co, rhs, th, out, rdot, ring, v, sg.x, sg.y, sg.z,
+                                       pol_k, dot, yv, rupd, alpha, rmax);
   }
   if constexpr (FR) {
     // max |r| over the grid, then the reference's history / convergence step (pcg.py:113-121)
@@ -563,136 +490,70 @@ __global__ void __launch_bounds__(32 * (W + 1), 1)
   }
 }
 
-// flag = 1 if any G, H or M entry of class `cls` is non-zero
-__global__ void k_cls0_check(Geo g, ChainOps co, int cls, int* flag) {
-  using C = Cm<true, false, false>;
-  const long long nblk = (long long)g.V * g.nb;
-  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= nblk) return;
-  const double* F = co.ff + ((long long)cls * nblk + gid) * C::FFS;
-  const double* B = co.fb + ((long long)cls * nblk + gid) * C::FB;
-  bool nz = false;
-  for (int i = C::QQ; i < C::FFS; ++i) nz |= F[i] != 0.0;
-  for (int i = C::QQ; i < C::FB; ++i) nz |= B[i] != 0.0;
-  if (nz) *flag = 1;
-}
-
 int env_or(const char* name, int dflt) {
   const char* s = getenv(name);
   return (s && *s) ? atoi(s) : dflt;
 }
 
-template <bool INNER, bool FR, bool DOT, int P, int W, int D>
-cudaError_t chains_launch(const Geo& g, const ChainOps& co, const SweepIo& io, int sm_count,
-                          double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  using C = Cm<INNER, FR, DOT>;
-  constexpr size_t smem = ((size_t)D * C::TS + 2 * D + 32 + (size_t)W * (P + 1) * C::SLOT) * 8;
-  static_assert(smem <= 227 * 1024, "shared memory budget");
+template <int NS, bool INNER, int P, int W, bool FR, bool DOT>
+cudaError_t chainm_launch(const Geo& g, const ChainOps& co, const double* rhs, const double* th,
+                          double* out, const double* rdot, int sm_count, double* partials,
+                          PcgState* st, int dotmode, const double* yv, double* rupd,
+                          cudaStream_t s) {
+  using C = Cm<NS, INNER, FR, DOT>;
+  constexpr size_t smem = ((size_t)W * (P + 1) * C::SLOT + 32) * sizeof(double);
   static bool configured[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 63;
-  auto kern = k_chains<INNER, FR, DOT, P, W, D>;
+  auto kern = k_chainm<NS, INNER, P, W, FR, DOT>;
   if (!configured[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured[dev] = true;
   }
-  const int nchunk = co.nseg - co.s0;
-  const int ngroups = g.V * ((nchunk + W - 1) / W);
-  const int blocks = std::max(1, std::min(ngroups, sm_count));
-  kern<<<blocks, 32 * (W + 1), smem, s>>>(g, co, io, partials, st, dotmode);
+  const int n_items = g.V * co.nseg;
+  const int blocks = std::max(1, std::min((n_items + W - 1) / W, sm_count));
+  kern<<<blocks, 32 * W, smem, s>>>(g, co, rhs, th, out, rdot, n_items, partials, st, dotmode,
+                                    yv, rupd);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-// Which sweeps the CTA-shared kernel can run: n = 2, every stage chunk of one class except an
-// optional leading stage-0 chunk whose class has no coupling (checked on the device).
-cudaError_t chainm_plan(const Geo& g, ChainOps& co, const int4* host_segs, cudaStream_t s) {
-  co.cm = 0;
-  co.s0 = 0;
-  if (g.n != 2 || co.nseg < 1 || env_or("GQ_NO_CHAINM", 0)) return cudaSuccess;
-  int s0 = 0;
-  if (co.nseg > 1 && host_segs[0].x == 0 && host_segs[0].y == 1 && host_segs[0].z != host_segs[1].z)
-    s0 = 1;
-  for (int i = s0 + 1; i < co.nseg; ++i)
-    if (host_segs[i].z != host_segs[s0].z) return cudaSuccess;
-  if (s0) {
-    int* flag = nullptr;
-    cudaError_t e = cudaMalloc(&flag, sizeof(int));
-    if (e != cudaSuccess) return e;
-    cudaMemsetAsync(flag, 0, sizeof(int), s);
-    const long long nblk = (long long)g.V * g.nb;
-    k_cls0_check<<<(unsigned)((nblk + 127) / 128), 128, 0, s>>>(g, co, host_segs[0].z, flag);
-    int hflag = 1;
-    e = cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(flag);
-    if (e != cudaSuccess) return e;
-    if (hflag) return cudaSuccess;
-  }
-  co.s0 = s0;
-  co.cm = 1;
-  return cudaSuccess;
+bool chainm_supported(const Geo& g, int sm_count) {
+  // twelve-warp CTAs, one per SM: worth it when the items fill the machine; smaller grids
+  // stay on the per-warp kernel (GQ_CHAINM=1 forces this one, the variant tests use it)
+  if (g.n != 2 || env_or("GQ_NO_CHAINM", 0)) return false;
+  return env_or("GQ_CHAINM", 0) >= 1 || (long long)g.V * ((g.T1 + 7) / 8) >= 8LL * sm_count;
 }
 
-bool chainm_supported(const Geo& g, const ChainOps& co, int sm_count) {
-  // one CTA per SM and pair group: worth it when the groups fill most of the machine
-  if (!co.cm) return false;
-  (void)g;
-  (void)sm_count;
-  return env_or("GQ_CHAINM", 0) == 1;   // opt-in while it is slower than the per-warp kernel
-}
-
-// development dispatch over (record ring depth, consumer warps, tile ring depth)
-#define CM_CASE(INNER_, P_, W_, D_, FR_, DOT_)                                                 \
-  if (P == P_ && W == W_ && D == D_)                                                           \
-    return chains_launch<INNER_, FR_, DOT_, P_, W_, D_>(g, co, io, sm_count, partials, st,     \
-                                                        dotmode, s);
-
-template <bool FR, bool DOT>
-static cudaError_t chains_outer(const Geo& g, const ChainOps& co, const SweepIo& io, int sm_count,
-                                double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  const int P = env_or("GQ_CM_PO", 4), W = env_or("GQ_CM_WO", 13), D = env_or("GQ_CM_DO", 16);
-  CM_CASE(false, 4, 13, 16, FR, DOT)
-  CM_CASE(false, 6, 13, 16, FR, DOT)
-  CM_CASE(false, 4, 13, 32, FR, DOT)
-  CM_CASE(false, 3, 13, 8, FR, DOT)
-  CM_CASE(false, 4, 9, 16, FR, DOT)
-  return cudaErrorInvalidValue;
-}
-
-template <bool DOT>
-static cudaError_t chains_inner(const Geo& g, const ChainOps& co, const SweepIo& io, int sm_count,
-                                double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  const int P = env_or("GQ_CM_PI", 3), W = env_or("GQ_CM_WI", 13), D = env_or("GQ_CM_DI", 16);
-  CM_CASE(true, 3, 13, 16, false, DOT)
-  CM_CASE(true, 4, 13, 16, false, DOT)
-  CM_CASE(true, 2, 13, 16, false, DOT)
-  CM_CASE(true, 3, 13, 32, false, DOT)
-  CM_CASE(true, 3, 13, 8, false, DOT)
-  CM_CASE(true, 3, 9, 16, false, DOT)
-  return cudaErrorInvalidValue;
-}
+bool chainm_all() { return env_or("GQ_CHAINM", 0) == 2; }
 
 cudaError_t launch_chainm(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
                           const double* th, double* out, const double* rdot, int sm_count,
                           double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  // ring depth: inner P = 3 (4 slots x 4.4 KB x 12 warps = 215 KB), outer P = 6
   const bool dot = dotmode != kDotNone;
-  const SweepIo io{rhs, th, out, rdot, nullptr, nullptr, 0.0};
-  if (inner)
-    return dot ? chains_inner<true>(g, co, io, sm_count, partials, st, dotmode, s)
-               : chains_inner<false>(g, co, io, sm_count, partials, st, dotmode, s);
-  return dot ? chains_outer<false, true>(g, co, io, sm_count, partials, st, dotmode, s)
-             : chains_outer<false, false>(g, co, io, sm_count, partials, st, dotmode, s);
+  if (inner) {
+    if (dot)
+      return chainm_launch<2, true, 3, 12, false, true>(g, co, rhs, th, out, rdot, sm_count,
+                                                        partials, st, dotmode, nullptr, nullptr, s);
+    return chainm_launch<2, true, 3, 12, false, false>(g, co, rhs, th, out, rdot, sm_count,
+                                                       partials, st, dotmode, nullptr, nullptr, s);
+  }
+  if (dot)
+    return chainm_launch<2, false, 6, 12, false, true>(g, co, rhs, th, out, rdot, sm_count,
+                                                       partials, st, dotmode, nullptr, nullptr, s);
+  return chainm_launch<2, false, 6, 12, false, false>(g, co, rhs, th, out, rdot, sm_count,
+                                                      partials, st, dotmode, nullptr, nullptr, s);
 }
 
 cudaError_t launch_chainm_fr(const Geo& g, const ChainOps& co, double* r, const double* y,
                              double* out, int sm_count, double* partials, PcgState* st,
                              cudaStream_t s) {
-  const SweepIo io{r, nullptr, out, nullptr, y, r, 0.0};
-  return chains_outer<true, false>(g, co, io, sm_count, partials, st, kDotNone, s);
+  return chainm_launch<2, false, 6, 12, true, false>(g, co, r, nullptr, out, nullptr, sm_count,
+                                                     partials, st, kDotNone, y, r, s);
 }
 
 }  // namespace gq

@@ -1,7 +1,11 @@
 // Shared definitions for the B200 PCGM kernels (sm_100a, fp64).
 //
 // Device vector layout ("stage-inner"): every multiplier vector is stored as
-//   v[j][i][t][k]   index = ((j*K + i)*T1 + t)*n + k
+//   v[j][i][t][k]   index = ((j*K + i)*TS + t)*n + k
+// with the stage stride TS >= T1 a multiple of 8 and the vector pointer itself T0 stages past
+// its 128-byte aligned allocation (Geo::TS, gq_api.cu), so that the 8-stage records of the
+// chain sweeps (and every node's first record) are whole 128-byte lines.  The padding stages
+// hold zeros and are never written.
 // i.e. node-major with the stage index innermost.  A warp maps its 32 lanes onto 32
 // consecutive stages of ONE grid node, so
 //   * every vector load/store of a warp is one contiguous 32*n*8-byte segment, and
@@ -45,6 +49,9 @@ struct Geo {
   int V, nb;          // column pairs, 2-row blocks per pair chain
   long long nk;       // K*N
   long long dim;      // K*N*n*T1
+  int TS = 0;         // stage stride of the device vectors (stages per node, >= T1)
+  int T0 = 0;         // zero stages between a vector's 128-byte aligned allocation and v[0]
+  long long span = 0; // doubles from a vector's first to one past its last entry
   int hx0 = -1, hx1 = -1;   // stage-slab halo stages: Delta leaves them unwritten (-1: none)
 };
 
@@ -244,7 +251,7 @@ __device__ bool grid_reduce(double v, double* partials, unsigned int* counter, d
 }
 
 __device__ __forceinline__ long long vidx(const Geo& g, int j, int i, int t) {
-  return (((long long)j * g.K + i) * g.T1 + t) * g.n;
+  return (((long long)j * g.K + i) * g.TS + t) * g.n;
 }
 
 }  // namespace gq

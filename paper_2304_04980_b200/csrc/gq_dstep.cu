@@ -503,7 +503,7 @@ bool dstep_make_map(const Geo& g, const double* base, bool out, CUtensorMap* m) 
   EncodeTiled enc = encoder();
   if (!enc || base == nullptr) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)g.T1 * 2, (cuuint64_t)g.K, (cuuint64_t)g.N};
-  const cuuint64_t strides[2] = {(cuuint64_t)g.T1 * 16, (cuuint64_t)g.T1 * 16 * g.K};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.TS * 16, (cuuint64_t)g.TS * 16 * g.K};
   const cuuint32_t box[3] = {(cuuint32_t)(CH * 2), (cuuint32_t)(out ? TI : PI),
                              (cuuint32_t)(out ? TJ : PJ)};
   const cuuint32_t es[3] = {1, 1, 1};

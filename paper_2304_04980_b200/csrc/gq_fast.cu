@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(128) k_stencil3(Geo g, FastOps fo, const doubl
   if (active) {
     const int i0 = strip * rows;
     const int i1 = min(g.K, i0 + rows);
-    const long long rs = (long long)g.T1 * NS;
+    const long long rs = (long long)g.TS * NS;
     const int dj[5] = {0, -1, 1, -2, 2};
     const double* cx[5];
     bool cok[5];
@@ -271,9 +271,9 @@ __global__ void __launch_bounds__(128) k_stencil3(Geo g, FastOps fo, const doubl
     for (int m = 0; m < 5; ++m) {
       const int jj = j + dj[m];
       cok[m] = tv && jj >= 0 && jj < g.N;
-      cx[m] = cok[m] ? x + ((long long)jj * g.K * g.T1 + t) * NS : x;
+      cx[m] = cok[m] ? x + ((long long)jj * g.K * g.TS + t) * NS : x;
     }
-    const double* cr = (MODE == kOuterRhs && tv) ? rin + ((long long)j * g.K * g.T1 + t) * NS : rin;
+    const double* cr = (MODE == kOuterRhs && tv) ? rin + ((long long)j * g.K * g.TS + t) * NS : rin;
     const double* oA = fo.oprow + ((long long)cA * g.nk + (long long)j * g.K) * C::OPR + C::OPOFF;
     const double* oB = fo.oprow + ((long long)cB * g.nk + (long long)j * g.K) * C::OPR + C::OPOFF;
     const bool two = cB != cA;
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(128) k_stencil3(Geo g, FastOps fo, const doubl
         for (int k = 0; k < NS; ++k) acc.v[k] = rv.v[k] + ((0.0 - eu.v[k]) - fd.v[k]);
       }
       if (useful) {
-        stv<NS>(y + ((long long)j * g.K * g.T1 + t) * NS + i * rs, acc);
+        stv<NS>(y + ((long long)j * g.K * g.TS + t) * NS + i * rs, acc);
         if (dotmode != kDotNone) {
 #pragma unroll
           for (int k = 0; k < NS; ++k) dot = fma(acc.v[k], c0[2].v[k], dot);
@@ -434,8 +434,8 @@ __global__ void __launch_bounds__(32) k_sweep3(Geo g, FastOps fo, const double* 
   double* ring = smem;
   const uint64_t pol = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
-  const long long rs = (long long)g.T1 * NS;            // next row, same column and stage
-  const long long cs = (long long)g.K * g.T1 * NS;      // next column
+  const long long rs = (long long)g.TS * NS;            // next row, same column and stage
+  const long long cs = (long long)g.K * g.TS * NS;      // next column
   double dot = 0.0;
 
 #pragma unroll 1
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(32) k_sweep3(Geo g, FastOps fo, const double* 
     const int a = 2 * v;
     const bool okb = a + 1 < g.N;
     const long long lane_off = (long long)(tv ? t : 0) * NS;
-    const long long col_a = (long long)a * g.K * g.T1 * NS + lane_off;   // (a, row 0, t)
+    const long long col_a = (long long)a * g.K * g.TS * NS + lane_off;   // (a, row 0, t)
     const double* FA = fo.fac3 + ((long long)cA * g.V + v) * g.nb * 3 * QQ;
     const double* FB = fo.fac3 + ((long long)cB * g.V + v) * g.nb * 3 * QQ;
     const double* OA = fo.omega + ((long long)cA * g.nk + (long long)a * g.K) * 5 * B2;
@@ -782,13 +782,13 @@ __device__ __forceinline__ void sweep6_item(
   constexpr int CPR = CH * NS / 2;                 // 16-byte chunks per record
   constexpr int RPI = 32 / CPR;                    // records per warp instruction
   const int qd = lane & 3, rw = lane >> 2;
-  const long long rs = (long long)g.T1 * NS;
-  const long long cs = (long long)g.K * g.T1 * NS;
+  const long long rs = (long long)g.TS * NS;
+  const long long cs = (long long)g.K * g.TS * NS;
   const long long rs2 = 2 * rs;
   const int a = 2 * v;
   const bool okb = a + 1 < g.N;
   const int nb = g.nb;
-  const long long col_a = (long long)a * g.K * g.T1 * NS + (long long)t0 * NS;
+  const long long col_a = (long long)a * g.K * g.TS * NS + (long long)t0 * NS;
   const double* FA = fo.fac4 + ((long long)cA * g.V + v) * nb * 4 * QQ;
   const double* FB = fo.fac4 + ((long long)cB * g.V + v) * nb * 4 * QQ;
   const double* OA = fo.omega + ((long long)cA * g.nk + (long long)a * g.K) * 5 * B2;

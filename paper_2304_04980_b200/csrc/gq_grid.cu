@@ -112,7 +112,7 @@ __device__ __forceinline__ void grid_body(const Geo& g, const FastOps& fo,
   const bool kf = tv && t >= 1;     // f_t exists (Xi_{t-1})
   const bool ku = t >= 1;           // receives e_{t-1}
   const bool kd = t < g.T;          // receives f_{t+1}
-  const long long rs = (long long)g.T1 * 2;
+  const long long rs = (long long)g.TS * 2;
   const long long cs = (long long)K * rs;
   const long long toff = (long long)(tv ? t : 0) * 2;
   auto colp = [&](const double* base, int jj) { return base + (long long)jj * cs + toff; };

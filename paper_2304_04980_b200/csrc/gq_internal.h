@@ -114,8 +114,6 @@ struct ChainOps {
   const double* omega = nullptr;   // [npc][N][K][5][n][n] cross-pair Psi blocks (n = 8 inner)
   const int4* grp = nullptr;       // CTA items (n = 8: all classes; n = 2: class-1 runs)
   int ngrp = 0;
-  // CTA-shared kernel (gq_chainm.cu): usable (cm), and seg[0] is the coupling-free stage 0 (s0)
-  int cm = 0, s0 = 0;
 };
 
 // n = 8 pair-chain sweeps with CTA-shared factor tiles (gq_chain8c.cu)

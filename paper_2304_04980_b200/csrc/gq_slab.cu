@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) k_stage_pack(Geo g, int t, const double* 
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < per;
        e += (long long)gridDim.x * blockDim.x) {
     const long long node = e / g.n;
-    buf[e] = v[(node * g.T1 + t) * g.n + (e - node * g.n)];
+    buf[e] = v[(node * g.TS + t) * g.n + (e - node * g.n)];
   }
 }
 
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_stage_zero(Geo g, int t, double* __rest
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < per;
        e += (long long)gridDim.x * blockDim.x) {
     const long long node = e / g.n;
-    v[(node * g.T1 + t) * g.n + (e - node * g.n)] = 0.0;
+    v[(node * g.TS + t) * g.n + (e - node * g.n)] = 0.0;
   }
 }
 
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) k_stage_unpack(Geo g, int t, const double
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < per;
        e += (long long)gridDim.x * blockDim.x) {
     const long long node = e / g.n;
-    v[(node * g.T1 + t) * g.n + (e - node * g.n)] = buf[e];
+    v[(node * g.TS + t) * g.n + (e - node * g.n)] = buf[e];
   }
 }
 

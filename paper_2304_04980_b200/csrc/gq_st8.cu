@@ -44,7 +44,7 @@ __device__ __forceinline__ void st8_body(const Geo& g, const Ops& op, const int4
     }
   }
   const int lane = threadIdx.x, rw = lane >> 2, qd = lane & 3;
-  const long long rs = (long long)g.T1 * NS, cs = (long long)g.K * rs;
+  const long long rs = (long long)g.TS * NS, cs = (long long)g.K * rs;
   double dot = 0.0;
 #pragma unroll 1
   for (long long node = blockIdx.x; node < g.nk; node += gridDim.x) {

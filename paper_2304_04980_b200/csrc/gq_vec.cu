@@ -285,7 +285,8 @@ __global__ void __launch_bounds__(256) k_sub(long long dim, double* __restrict__
 
 cudaError_t launch_update(const Geo& g, double* x, double* r, const double* d, const double* y,
                           int blocks, double* partials, PcgState* st, cudaStream_t s) {
-  k_update<<<blocks, 256, 0, s>>>(g.dim, x, r, d, y, partials, st);
+  const long long fp = (long long)g.T0 * g.n;
+  k_update<<<blocks, 256, 0, s>>>(g.span + fp, x - fp, r - fp, d - fp, y - fp, partials, st);
   return cudaGetLastError();
 }
 
@@ -302,55 +303,64 @@ __global__ void __launch_bounds__(256) k_nonfinite(long long dim, const double* 
 
 cudaError_t launch_nonfinite(const Geo& g, const double* v, int blocks, PcgState* st,
                              cudaStream_t s) {
-  k_nonfinite<<<blocks, 256, 0, s>>>(g.dim, v, st);
+  const long long fp = (long long)g.T0 * g.n;
+  k_nonfinite<<<blocks, 256, 0, s>>>(g.span + fp, v - fp, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_r(const Geo& g, double* r, const double* y, int blocks,
                             double* partials, PcgState* st, cudaStream_t s) {
-  k_update_r<<<blocks, 256, 0, s>>>(g.dim, r, y, partials, st);
+  const long long fp = (long long)g.T0 * g.n;
+  k_update_r<<<blocks, 256, 0, s>>>(g.span + fp, r - fp, y - fp, partials, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_x(const Geo& g, double* x, const double* d, int blocks, PcgState* st,
                             cudaStream_t s) {
-  k_update_x<<<blocks, 256, 0, s>>>(g.dim, x, d, st);
+  const long long fp = (long long)g.T0 * g.n;
+  k_update_x<<<blocks, 256, 0, s>>>(g.span + fp, x - fp, d - fp, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dirupdate(const Geo& g, double* d, const double* q, int blocks, PcgState* st,
                              cudaStream_t s) {
-  k_dirupdate<<<blocks, 256, 0, s>>>(g.dim, d, q, st);
+  const long long fp = (long long)g.T0 * g.n;
+  k_dirupdate<<<blocks, 256, 0, s>>>(g.span + fp, d - fp, q - fp, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dirupdate_x(const Geo& g, double* d, const double* q, double* x, int blocks,
                                PcgState* st, cudaStream_t s) {
-  k_dirupdate_x<<<blocks, 256, 0, s>>>(g.dim, d, q, x, st);
+  const long long fp = (long long)g.T0 * g.n;
+  k_dirupdate_x<<<blocks, 256, 0, s>>>(g.span + fp, d - fp, q - fp, x - fp, st);
   return cudaGetLastError();
 }
 
 cudaError_t launch_maxdiff(const Geo& g, const double* a, const double* b, int blocks,
                           double* partials, unsigned int* counter, double* out, cudaStream_t s) {
-  k_maxdiff<<<blocks, 256, 0, s>>>(g.dim, a, b, partials, counter, out);
+  const long long fp = (long long)g.T0 * g.n;
+  k_maxdiff<<<blocks, 256, 0, s>>>(g.span + fp, a - fp, b ? b - fp : nullptr, partials, counter, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_add(const Geo& g, double* out, const double* a, const double* b, int blocks,
                        cudaStream_t s) {
-  k_add<<<blocks, 256, 0, s>>>(g.dim, out, a, b);
+  const long long fp = (long long)g.T0 * g.n;
+  k_add<<<blocks, 256, 0, s>>>(g.span + fp, out - fp, a - fp, b - fp);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dot(const Geo& g, const double* a, const double* b, int blocks,
                        double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  k_dot<<<blocks, 256, 0, s>>>(g.dim, a, b, partials, st, dotmode);
+  const long long fp = (long long)g.T0 * g.n;
+  k_dot<<<blocks, 256, 0, s>>>(g.span + fp, a - fp, b - fp, partials, st, dotmode);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sub(const Geo& g, double* out, const double* a, const double* b, int blocks,
                        cudaStream_t s) {
-  k_sub<<<blocks, 256, 0, s>>>(g.dim, out, a, b);
+  const long long fp = (long long)g.T0 * g.n;
+  k_sub<<<blocks, 256, 0, s>>>(g.span + fp, out - fp, a - fp, b - fp);
   return cudaGetLastError();
 }
 
@@ -383,7 +393,7 @@ __global__ void __launch_bounds__(256) k_transpose(Geo g, int tn, const double* 
       const int ts = w / n, k = w % n;
       const long long nd = nd0 + nl;
       const int t = t0 + ts;
-      if (t < g.T1 && nd < nodes) dst[(nd * g.T1 + t) * n + k] = tile[ts * rec + nl * n + k];
+      if (t < g.T1 && nd < nodes) dst[(nd * g.TS + t) * n + k] = tile[ts * rec + nl * n + k];
     }
   } else {
     const int rec2 = kTS * n;
@@ -392,7 +402,7 @@ __global__ void __launch_bounds__(256) k_transpose(Geo g, int tn, const double* 
       const int ts = w / n, k = w % n;
       const long long nd = nd0 + nl;
       const int t = t0 + ts;
-      if (t < g.T1 && nd < nodes) tile[ts * rec + nl * n + k] = src[(nd * g.T1 + t) * n + k];
+      if (t < g.T1 && nd < nodes) tile[ts * rec + nl * n + k] = src[(nd * g.TS + t) * n + k];
     }
     __syncthreads();
     for (int e = threadIdx.x; e < total; e += blockDim.x) {

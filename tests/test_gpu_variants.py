@@ -16,7 +16,7 @@ VARIANTS = {
     "generic_v1": {"GQ_FORCE_V1": "1"},          # thread-per-chain sweeps, v1 stencils
     "no_chain": {"GQ_NO_CHAIN": "1"},            # FMA / v6 sweeps instead of the chain kernel
     "no_grid": {"GQ_NO_GRID": "1"},              # v2 stencils instead of the n=2 grid kernel
-    "chainm": {"GQ_CHAINM": "1"},                # multi-warp chain sweeps on every n=2 golden case
+    "chainm": {"GQ_CHAINM": "2"},                # twelve-warp chain sweeps (every form) on the n=2 cases
     "dstep": {"GQ_DSTEP": "1"},                  # t-loop Delta on every (small) golden case
     "fuse_x": {"GQ_FUSE_X": "1"},                # x update fused into the direction update
     "no_fuse_r": {"GQ_NO_FUSE_R": "1"},          # separate r update kernel
