@@ -30,6 +30,12 @@ def step_name(fn, seen):
         return "dirupdate"
     if "k_grid<3" in fn:
         return "outer_rhs_s1"
+    if "k_chainm<2, 0, 6, 12, 1" in fn:
+        return "sweep_s0_l0_r"
+    if "k_chainm<2, 1" in fn:
+        return "sweep_s0_l1" if "sweep_s0_l1" not in seen else "sweep_s1_l1"
+    if "k_chainm<2, 0" in fn:
+        return "sweep_s1_l0"
     if "k_chain<2, 0, 7, 1, 0, 1" in fn:
         return "sweep_s0_l0_r"
     if "k_chain<2, 1" in fn:

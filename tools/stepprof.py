@@ -5,7 +5,7 @@ import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2304_04980_b200 import GpuSchurOperator, GpuNestedJacobiPreconditioner, _lib, generators
-ga = generators.config4(0)
+ga = generators.config4(0, N=int(os.environ.get("SP_N", "256")))
 op = GpuSchurOperator(ga, 2, 2); pc = GpuNestedJacobiPreconditioner(op, 2, 2)
 ctx = op._ctx; lib = ctx.lib
 rhs = torch.tensor(ga.offset, device="cuda", dtype=torch.float64)
