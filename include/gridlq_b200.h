@@ -147,6 +147,22 @@ int gq_recover(gq_ctx* ctx, const double* lam, double* x_out, double* u_out, dou
 int gq_kkt_residual(gq_ctx* ctx, const double* lam, const double* x, const double* u,
                     const double* offset, double* res3);
 
+/* Reduced right-hand side omega~ built on the device (replaces the offset loop of
+ * build_stacked, kkt_assembly.py:275-301): out[stage 0] = init, out[stage t+1] (edge nodes) =
+ * sum over the off-grid directions d with a declared trajectory of C_d(t) sigma_d(t), added in
+ * the reference's order north, south, west, east.  All pointers are device pointers:
+ *   init   [N][K][n]                initial states, node order (j, i) as in the vectors
+ *   blocks [4][L][ncls][n][n]       coupling blocks of edge node e of direction d (west,
+ *                                   east, north, south; L = max(K, N); e = row i for
+ *                                   west/east, column j for north/south), row-major
+ *   cls    [4][L][T]  int32         block class of (d, e, t), or -1: no term
+ *   traj   [4][L][T][n]             boundary trajectories sigma_d(e, t)
+ *   out    [gq_dim]                 omega~ in the reference order (t, j, i, k)
+ * No context is needed; `stream` is a cudaStream_t (or null). */
+int gq_build_offset(int32_t K, int32_t N, int32_t T, int32_t n, int32_t ncls,
+                    const double* init, const double* blocks, const int32_t* cls,
+                    const double* traj, double* out, void* stream);
+
 /* Measurement helpers (bench.py): run `steps` PCG steps as individual launches with CUDA
  * events around every kernel; per-kernel total milliseconds go to ms_out[0..count) in the
  * order gq_kernel_name(ctx, i) reports.  Returns the number of kernels per step. */

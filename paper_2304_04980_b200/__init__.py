@@ -8,8 +8,9 @@ preconditioner duck types, executed by hand-written sm_100a CUDA in libgridlq_b2
 from .errors import (BreakdownError, DimensionGuardError, DimensionMismatchError, GridLQError,
                      MaxIterationsExceeded, NotPositiveDefiniteError)
 from .problem import (BoundaryData, ConstSeq, GridArrays, GridLayout, GridLQProblem,
-                      SubsystemData, arrays_from_problem, arrays_to_problem, load_problem,
-                      problem_from_dict, problem_to_dict, save_problem, validate_arrays)
+                      SubsystemData, arrays_from_problem, arrays_to_problem, boundary_arrays,
+                      load_problem, problem_from_dict, problem_to_dict, rhs_offset_device,
+                      save_problem, validate_arrays)
 from .recovery import TrajectorySolution, kkt_residual, recover_solution
 from .slab import SlabComm, SlabPcg, pcg_solve_slabs
 from .solver import (COUNT_KEYS, GpuNestedJacobiPreconditioner, GpuSchurOperator, SolveReport,

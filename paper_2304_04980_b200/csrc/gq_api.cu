@@ -29,6 +29,11 @@ static int fail(int code, const std::string& msg) {
   return code;
 }
 
+namespace gq {
+// for the entry points that live in other translation units (gq_rhs.cu)
+int api_fail(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace gq
+
 #define CK(call)                                                                     \
   do {                                                                               \
     cudaError_t e_ = (call);                                                         \

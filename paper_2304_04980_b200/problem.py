@@ -514,6 +514,75 @@ def rhs_offset(problem, n):
     return offset
 
 
+def boundary_arrays(problem, n):
+    """The inputs of ``gq_build_offset`` as dense host arrays: ``init`` [N][K][n], the edge
+    coupling ``blocks`` [4][L][ncls][n][n] (L = max(K, N); direction order DIRECTIONS), their
+    stage ``cls`` map [4][L][T] (-1: no coupling list or no trajectory -> no term) and the
+    boundary trajectories ``traj`` [4][L][T][n].  A coupling list that repeats one block
+    (``ConstSeq``) is one class; any other list keeps its T blocks."""
+    K, N, T = problem.K, problem.N, problem.T
+    L = max(K, N)
+    bnd = problem.boundary
+    init = np.ascontiguousarray(
+        np.transpose(np.asarray(bnd.init, dtype=float).reshape(K, N, n), (1, 0, 2)))
+    edges = {}
+    varying = False
+    for d, direction in enumerate(DIRECTIONS):
+        traj = getattr(bnd, direction)
+        if traj is None:
+            continue
+        if direction in ("north", "south"):
+            i = 0 if direction == "north" else K - 1
+            nodes = [(i, j, j) for j in range(N)]
+        else:
+            j = 0 if direction == "west" else N - 1
+            nodes = [(i, j, i) for i in range(K)]
+        for i, j, e in nodes:
+            blocks = problem.sub(i, j).coupling(direction)
+            if blocks is None:
+                continue
+            const = isinstance(blocks, ConstSeq)
+            varying = varying or not const
+            edges[(d, e)] = (blocks, const, traj[e])
+    ncls = T if varying else 1
+    blk = np.zeros((4, L, ncls, n, n))
+    cls = np.full((4, L, T), -1, dtype=np.int32)
+    tr = np.zeros((4, L, T, n))
+    for (d, e), (blocks, const, sig) in edges.items():
+        if const:
+            blk[d, e, 0] = np.asarray(blocks[0], dtype=float)
+            cls[d, e] = 0
+        else:
+            blk[d, e] = np.asarray(blocks, dtype=float).reshape(T, n, n)
+            cls[d, e] = np.arange(T)
+        tr[d, e] = np.asarray(sig, dtype=float).reshape(T, n)
+    return init, blk, cls, tr
+
+
+def rhs_offset_device(problem, n=None, device="cuda"):
+    """omega~ (``kkt_assembly.py:275-301``) as a CUDA tensor in the reference vector order,
+    built by the ``gq_build_offset`` kernel from the boundary data: the device-side
+    counterpart of ``rhs_offset`` for right-hand sides that never need to exist on the host."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+
+    if n is None:
+        n = problem.sub(0, 0).n
+    K, N, T = problem.K, problem.N, problem.T
+    init, blk, cls, tr = boundary_arrays(problem, n)
+    dev = [torch.as_tensor(a, device=device) for a in (init, blk, cls, tr)]
+    out = torch.empty((T + 1) * K * N * n, dtype=torch.float64, device=device)
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    with torch.cuda.device(out.device):
+        _lib.check(_lib.load().gq_build_offset(
+            K, N, T, n, blk.shape[2], *(ctypes.c_void_p(t.data_ptr()) for t in dev),
+            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream)), "gq_build_offset")
+    return out
+
+
 def as_arrays(problem_or_arrays) -> GridArrays:
     if isinstance(problem_or_arrays, GridArrays):
         msgs = validate_arrays(problem_or_arrays)

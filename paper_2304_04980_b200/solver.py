@@ -28,7 +28,7 @@ import numpy as np
 from . import _lib
 from .counts import counters
 from .errors import BreakdownError, DimensionMismatchError, MaxIterationsExceeded
-from .problem import GridArrays, as_arrays
+from .problem import GridArrays, as_arrays, rhs_offset_device
 
 COUNT_KEYS = (
     "operator_apply",
@@ -169,12 +169,22 @@ class GpuSchurOperator:
 
     def __init__(self, problem, inner_sweeps=2, outer_sweeps=2):
         self.arrays = as_arrays(problem)
+        self._problem = None if isinstance(problem, GridArrays) else problem
         self._ctx = _Context(self.arrays, inner_sweeps, outer_sweeps)
         self.dim = self._ctx.dim
         self.layout = self.arrays.layout
         self.pairs = self.layout.pairs
         self.offset = self.arrays.offset
         self._counts = {}
+
+    def offset_device(self):
+        """omega~ as a CUDA tensor: built by the ``gq_build_offset`` kernel when the operator
+        was made from a GridLQProblem (``kkt_assembly.py:275-301``), uploaded otherwise."""
+        import torch
+
+        if self._problem is not None:
+            return rhs_offset_device(self._problem, self.arrays.n)
+        return torch.as_tensor(self.arrays.offset, device="cuda")
 
     def counts(self, inner_sweeps=2, outer_sweeps=2):
         key = (inner_sweeps, outer_sweeps)

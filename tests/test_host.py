@@ -139,3 +139,33 @@ def test_time_varying_ingestion_is_vectorised():
     assert len(ga.A) == T - 1 and ga.dyn_class[7] == ga.dyn_class[3]
     assert len(ga.Q) == T + 1
     assert np.array_equal(ga.A[ga.dyn_class[5], 10, 20], A[5])
+
+
+def _offset_from_boundary_arrays(problem, n):
+    """numpy restatement of k_offset (csrc/gq_rhs.cu) on the arrays gq_build_offset receives."""
+    from paper_2304_04980_b200.problem import boundary_arrays
+    K, N, T = problem.K, problem.N, problem.T
+    init, blk, cls, tr = boundary_arrays(problem, n)
+    out = np.zeros((T + 1, N, K, n))
+    out[0] = init
+    for t in range(T):
+        for j in range(N):
+            for i in range(K):
+                for d, edge, e in ((2, i == 0, j), (3, i == K - 1, j), (0, j == 0, i),
+                                   (1, j == N - 1, i)):
+                    if edge and cls[d, e, t] >= 0:
+                        out[t + 1, j, i] += blk[d, e, cls[d, e, t]] @ tr[d, e, t]
+    return out.reshape(-1)
+
+
+def test_boundary_arrays_reproduce_reference_offset():
+    """The dense inputs of the device omega~ kernel carry everything the reference's offset
+    loop uses (kkt_assembly.py:275-301): all four edges, corners, missing trajectories."""
+    p = cases.boundary_problem()
+    _, rec = load_golden("boundary")
+    assert np.allclose(_offset_from_boundary_arrays(p, 2), rec["ref_offset"], rtol=1e-15, atol=1e-16)
+    p.boundary.south = None           # a direction without a trajectory contributes nothing
+    from paper_2304_04980_b200.problem import rhs_offset
+    assert np.allclose(_offset_from_boundary_arrays(p, 2), rhs_offset(p, 2), rtol=1e-15, atol=1e-16)
+    tv = cases.time_varying()
+    assert np.allclose(_offset_from_boundary_arrays(tv, 2), rhs_offset(tv, 2), rtol=1e-15, atol=1e-16)
