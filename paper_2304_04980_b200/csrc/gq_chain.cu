@@ -776,11 +776,11 @@ static cudaError_t chain_p(const Geo& g, const ChainOps& co, const double* rhs, 
 cudaError_t launch_chain(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
                          const double* th, double* out, const double* rdot, int sm_count,
                          double* partials, PcgState* st, int dotmode, cudaStream_t s) {
-  // large n = 2 grids: inner sweeps without the fused dot run on the twelve-warp kernel (0.240
-  // against 0.262 ms at the headline); its outer, fused-residual and fused-dot forms measured
-  // slower than this file's (0.167 / 0.308 / 0.347 against 0.160 / 0.277 / 0.273 ms) and are
-  // only reached with GQ_CHAINM=2
-  if (chainm_supported(g, sm_count) && ((inner && dotmode == kDotNone) || chainm_all()))
+  // large n = 2 grids: the inner sweeps (with or without the fused dot) run on the twelve-warp
+  // kernel (0.236 / 0.255 against 0.262 / 0.273 ms at the headline); its plain outer form
+  // measured slower than this file's (0.166 against 0.161 ms) and is only reached with
+  // GQ_CHAINM=2
+  if (chainm_supported(g, sm_count) && (inner || chainm_all()))
     return launch_chainm(g, co, inner, rhs, th, out, rdot, sm_count, partials, st, dotmode, s);
   if (g.n == 2)
     return inner ? chain_p<2, true>(g, co, rhs, th, out, rdot, sm_count, partials, st, dotmode, s)
@@ -821,7 +821,7 @@ static cudaError_t chain_fr_launch(const Geo& g, const ChainOps& co, double* r, 
 cudaError_t launch_chain_fr(const Geo& g, const ChainOps& co, double* r, const double* y,
                             double* out, int sm_count, double* partials, PcgState* st,
                             cudaStream_t s) {
-  if (chainm_supported(g, sm_count) && chainm_all())
+  if (chainm_supported(g, sm_count))   // 0.256 against 0.277 ms at the headline
     return launch_chainm_fr(g, co, r, y, out, sm_count, partials, st, s);
   if (g.n == 2)
     return chain_fr_launch<2, 7>(g, co, r, y, out, sm_count, partials, st, s);

@@ -65,7 +65,10 @@ struct Cm {
   static constexpr int FFS = 2 * QQ + Q * TC;         // forward factor doubles per block
   static constexpr int FB = 2 * QQ;                   // backward factor doubles per block
   static constexpr int REC = 8 * NS;                  // record: 8 stages x NS
-  static constexpr int RSTR = REC + 2 * NS;           // padded stride (conflict-free A reads)
+  // records are whole 128-byte rows of the ring (a padded stride would split every 128-byte
+  // cp.async row write in two); the 16-byte stage chunks of record r sit at chunk ^ 2 (r & 3),
+  // which keeps the A-fragment reads of a quarter warp (4 records x 2 stages) conflict-free
+  static constexpr int RSTR = REC;
   static constexpr int CPR = REC / 2;                 // 16-byte chunks per record
   static constexpr int RPI = 32 / CPR;                // records per warp copy instruction
   // forward records: tau (4), then theta records 4..11 (inner) or y (4, fused r update)
@@ -76,7 +79,7 @@ struct Cm {
   static constexpr int CFF = FF / 64, CFB = FB / 64;  // factor copy instructions (32 x 16 B)
   static constexpr int SLOT = (NRF * RSTR + FF) > (NRB * RSTR + FB) ? (NRF * RSTR + FF)
                                                                      : (NRB * RSTR + FB);
-  static_assert(NS == 2 || NS == 4, "multi-warp chain sweep: n in {2, 4}");
+  static_assert(NS == 2, "record swizzle: one 16-byte chunk per stage");
 };
 
 template <int NS, bool INNER, int P, bool FR, bool DOT>
@@ -103,7 +106,9 @@ __device__ __forceinline__ void chainm_item(const Geo& g, const ChainOps& co,
   const int wofs = stage_ok ? 2 * wch : 0;               // stage-invalid lanes read stage 0
   const unsigned ring_u = smem_u32(ring);
   // A-fragment offset of feature pair f0 = 8p + 2qd of chain rw inside a slot
-  auto aofs = [&](int f0) { return (f0 / NS) * REC + rw * NS + (f0 % NS); };
+  auto aofs = [&](int f0) {
+    return (f0 / NS) * REC + ((rw ^ (2 * ((f0 / NS) & 3))) * NS) + (f0 % NS);
+  };
 
   // ---------------- forward ----------------
   const double* fsrc[C::JF];
@@ -122,7 +127,8 @@ __device__ __forceinline__ void chainm_item(const Geo& g, const ChainOps& co,
               (long long)dr * rs + wofs;
   }
   // per-lane shared destination, kept in a vector register (no [R + UR] LDGSTS forms)
-  const unsigned rec_dst = lane_opaque(ring_u + (unsigned)(((lane / C::CPR) * REC + 2 * wch) * 8));
+  const unsigned rec_dst = lane_opaque(
+      ring_u + (unsigned)(((lane / C::CPR) * REC + 2 * (wch ^ (2 * ((lane / C::CPR) & 3)))) * 8));
   const unsigned facf_dst = lane_opaque(ring_u + (unsigned)(C::NRF * REC * 8 + 16 * lane));
   const unsigned facb_dst = lane_opaque(ring_u + (unsigned)(C::NRB * REC * 8 + 16 * lane));
   const double* ffb = co.ff + ((long long)cls * g.V + v) * nb * C::FFS + 2 * lane;
@@ -411,7 +417,9 @@ __device__ bool cta_grid_reduce(double v, double* red, double* partials, unsigne
                                 double& outv) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   v = MAX ? warp_max(v) : warp_sum(v);
-  __shared__ int is_last;
+  // the flag lives in the dynamic array: a static __shared__ variable would move the rings
+  // off their 128-byte alignment, and every cp.async into them would split in two
+  int& is_last = *reinterpret_cast<int*>(red + 24);
   if (lane == 0) red[w] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -440,7 +448,7 @@ __global__ void __launch_bounds__(32 * W, 1)
     k_chainm(Geo g, ChainOps co, const double* __restrict__ rhs, const double* __restrict__ th,
              double* out, const double* __restrict__ rdot, int n_items, double* partials,
              PcgState* st, int dotmode, const double* __restrict__ yv, double* rupd) {
-  extern __shared__ __align__(16) double ring_all[];
+  extern __shared__ __align__(128) double ring_all[];
   using C = Cm<NS, INNER, FR, DOT>;
   if (halted(st)) return;
   const int warp = threadIdx.x >> 5;
@@ -543,16 +551,16 @@ cudaError_t launch_chainm(const Geo& g, const ChainOps& co, bool inner, const do
                                                        partials, st, dotmode, nullptr, nullptr, s);
   }
   if (dot)
-    return chainm_launch<2, false, 6, 12, false, true>(g, co, rhs, th, out, rdot, sm_count,
+    return chainm_launch<2, false, 7, 12, false, true>(g, co, rhs, th, out, rdot, sm_count,
                                                        partials, st, dotmode, nullptr, nullptr, s);
-  return chainm_launch<2, false, 6, 12, false, false>(g, co, rhs, th, out, rdot, sm_count,
+  return chainm_launch<2, false, 7, 12, false, false>(g, co, rhs, th, out, rdot, sm_count,
                                                       partials, st, dotmode, nullptr, nullptr, s);
 }
 
 cudaError_t launch_chainm_fr(const Geo& g, const ChainOps& co, double* r, const double* y,
                              double* out, int sm_count, double* partials, PcgState* st,
                              cudaStream_t s) {
-  return chainm_launch<2, false, 6, 12, true, false>(g, co, r, nullptr, out, nullptr, sm_count,
+  return chainm_launch<2, false, 7, 12, true, false>(g, co, r, nullptr, out, nullptr, sm_count,
                                                      partials, st, kDotNone, y, r, s);
 }
 
