@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(32) k_chain(Geo g, ChainOps co, const double* 
                                               double* partials, PcgState* st, int dotmode,
                                               const double* __restrict__ yv = nullptr,
                                               double* rupd = nullptr, int smc = 0) {
-  extern __shared__ __align__(16) double ring[];
+  extern __shared__ __align__(128) double ring[];
   if (halted(st)) return;
   const double alpha = FR ? st->alpha : 0.0;
   double rmax = 0.0;

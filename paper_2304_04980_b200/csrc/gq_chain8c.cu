@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(32 * W, INNER ? 1 : 2) k_chain8c(Geo g, ChainO
                                                        int n_items, double* partials,
                                                        PcgState* st, int dotmode) {
   using C = C8<INNER>;
-  extern __shared__ __align__(16) double sm8[];
+  extern __shared__ __align__(128) double sm8[];
   if (halted(st)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, rw = lane >> 2, qd = lane & 3;
   const int tid = threadIdx.x;

@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(128) k_stencil3(Geo g, FastOps fo, const doubl
                                                   int dotmode) {
   using C = St3<NS, MODE>;
   constexpr int B2 = C::B2, REC = C::REC;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   if (st != nullptr) {
     if (dotmode == kDotStep) {
       const bool stop = st->done || st->step >= st->max_steps;
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(32) k_sweep3(Geo g, FastOps fo, const double* 
                                                int dotmode) {
   using C = Sw3<NS, INNER>;
   constexpr int Q = C::Q, QQ = C::QQ, B2 = C::B2, REC = C::REC;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   if (halted(st)) return;
   const int lane = threadIdx.x & 31;
   double* ring = smem;
@@ -1239,7 +1239,7 @@ __global__ void __launch_bounds__(32) k_sweep6(Geo g, FastOps fo, const double* 
                                                const double* __restrict__ rdot, int n_items,
                                                int nchunk, double* partials, PcgState* st,
                                                int dotmode) {
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   if (halted(st)) return;
   const int lane = threadIdx.x & 31;
   const int rw = lane >> 2;

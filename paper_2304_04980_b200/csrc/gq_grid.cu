@@ -77,7 +77,7 @@ __device__ __forceinline__ void grid_body(const Geo& g, const FastOps& fo,
                                           PcgState* st, int dotmode) {
   using C = Gd<MODE>;
   constexpr int R = P + 1, REC = C::REC, OPS = C::OPS;
-  extern __shared__ __align__(16) double ring[];
+  extern __shared__ __align__(128) double ring[];
   if (st != nullptr) {
     if (dotmode == kDotStep) {
       const bool stop = st->done || st->step >= st->max_steps;
