@@ -30,11 +30,12 @@ def step_name(fn, seen):
         return "dirupdate"
     if "k_grid<3" in fn:
         return "outer_rhs_s1"
-    if "k_chainm<2, 0, 6, 12, 1" in fn:
-        return "sweep_s0_l0_r"
-    if "k_chainm<2, 1" in fn:
-        return "sweep_s0_l1" if "sweep_s0_l1" not in seen else "sweep_s1_l1"
-    if "k_chainm<2, 0" in fn:
+    if "k_chainm<" in fn:   # k_chainm<NS, INNER, P, W, FR, DOT>
+        targs = [x.strip() for x in fn.split("k_chainm<")[1].split(">")[0].split(",")]
+        if targs[4] == "1":
+            return "sweep_s0_l0_r"
+        if targs[1] == "1":
+            return "sweep_s0_l1" if "sweep_s0_l1" not in seen else "sweep_s1_l1"
         return "sweep_s1_l0"
     if "k_chain<2, 0, 7, 1, 0, 1" in fn:
         return "sweep_s0_l0_r"
