@@ -511,15 +511,62 @@ def _oracle_steps(ga, S, L, steps, threads, budget_s=None):
     return per_step, setup, k - 1, orc.threads
 
 
+def reference_python_leg(steps=8):
+    """The unmodified reference package (baseline/_ref, pure Python + NumPy) timed on this
+    host at a size it can hold: BASELINE config 2 (MSD 16x16, T=50, S=L=2), its own pcg_solve
+    with pool=None and with its --threads executor (cli.py:285).  The headline size is out of
+    its reach (>100 GB, hours of setup: SURVEY.md 6).  None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "gridlq")):
+        return None
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2304_04980_b200 import generators
+    from paper_2304_04980_b200.problem import arrays_to_problem
+
+    sys.path.insert(0, ref)
+    try:
+        import gridlq
+    finally:
+        sys.path.remove(ref)
+    ga = generators.config2(0)
+    t0 = time.perf_counter()
+    st = gridlq.build_stacked(arrays_to_problem(ga))
+    sc = gridlq.build_schur(st)
+    pc = gridlq.NestedJacobiPreconditioner(sc, inner_sweeps=2, outer_sweeps=2)
+    setup = time.perf_counter() - t0
+    out = {"workload": "config2 msd 16x16 T=50 n=2, S=L=2", "dim": int(sc.dim),
+           "setup_s": round(setup, 2), "steps": steps, "unit": UNIT}
+    threads = os.cpu_count() or 1
+    for key, pool in (("pool_none", None), (f"threads_{threads}", ThreadPoolExecutor(threads))):
+        stamps = []
+        try:
+            gridlq.pcg_solve(sc, pc, st.offset, tol=1e-300, max_steps=steps, pool=pool,
+                             callback=lambda k, x, r: stamps.append(time.perf_counter()))
+        except gridlq.MaxIterationsExceeded:
+            pass
+        if pool is not None:
+            pool.shutdown()
+        out[key] = (len(stamps) - 1) / (stamps[-1] - stamps[0])
+    return out
+
+
 def cpu_baseline(args, ga):
     per_step, setup, k, th = _oracle_steps(ga, args.S, args.L, args.cpu_steps + 1, 1)
-    return {
+    line = {
         "value": 1.0 / per_step, "unit": UNIT, "cores": th, "kind": "port",
         "sample": f"{k} PCGM step(s) of the same workload with the C restatement of the "
                   f"reference loop (oracle/gridlq_oracle.c), 1 thread; setup {setup:.1f}s "
                   "and the initial preconditioner apply excluded",
         "host_cpus": os.cpu_count(),
     }
+    try:
+        ref = reference_python_leg()
+    except Exception as exc:   # the reference leg is informational; never fail the bench on it
+        ref = {"error": str(exc)[:200]}
+    if ref is not None:
+        line["reference_python"] = ref
+    return line
 
 
 def workload_config(args, ga, S, L, parallelism):
