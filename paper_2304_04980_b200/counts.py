@@ -75,10 +75,18 @@ def _cross_pair(N, dj):
     return (jj + dj) // 2 != jj // 2
 
 
-def counters(ga: GridArrays, inner_sweeps: int, outer_sweeps: int) -> dict:
+def counters(ga: GridArrays, inner_sweeps: int, outer_sweeps: int, nd=None) -> dict:
+    """``nd`` [N][K]: the true state dimensions when ``ga`` is the padded embedding of a
+    problem with mixed dimensions (embed.py); a stored block (a, b) then costs n_a n_b."""
     n = ga.n
-    n2 = n * n
     T = ga.T
+    dims = np.full((ga.N, ga.K), n, dtype=np.int64) if nd is None else np.asarray(nd, dtype=np.int64)
+
+    def weight(mask, off):
+        """sum over stored blocks (a, a+off) of n_a * n_{a+off}"""
+        di, dj = off
+        return int(np.sum(mask * dims * _shift(dims, di, dj)))
+
     per_dc = {}
     for dc in np.unique(ga.dyn_class):
         ex = ahat_exists(ga, int(dc))
@@ -89,25 +97,24 @@ def counters(ga: GridArrays, inner_sweeps: int, outer_sweeps: int) -> dict:
             dj = OFF13[o][1]
             if dj == 0:
                 continue
-            cross += int(np.sum(ps[o] & _cross_pair(ga.N, dj)[:, None]))
-        per_dc[int(dc)] = dict(ahat=int(ex.sum()), psi=int(ps.sum()), cross=cross)
-    diag = ga.K * ga.N
-    matvec = diag * n2                       # Psi_0 = Qinv_0: diagonal blocks only
+            cross += weight(ps[o] & _cross_pair(ga.N, dj)[:, None], OFF13[o])
+        per_dc[int(dc)] = dict(ahat=sum(weight(ex[u], OFF5[u]) for u in range(5)),
+                               psi=sum(weight(ps[o], OFF13[o]) for o in range(13)),
+                               cross=cross)
+    matvec = int(np.sum(dims * dims))        # Psi_0 = Qinv_0: diagonal blocks only
     outer = 0
     inner = 0
     for t in range(T):
         st = per_dc[int(ga.dyn_class[t])]
-        matvec += st["psi"] * n2 + 2 * st["ahat"] * n2     # Psi_{t+1} and Xi_t (both ways)
-        outer += 2 * st["ahat"] * n2
-        inner += st["cross"] * n2
-    # pair solves: every (v, t) chain, blocks q_k = rows_k * cols_v * n
+        matvec += st["psi"] + 2 * st["ahat"]               # Psi_{t+1} and Xi_t (both ways)
+        outer += 2 * st["ahat"]
+        inner += st["cross"]
+    # pair solves: every (v, t) chain, block k holds the states of rows 2k, 2k+1 of the pair
     pair = 0
     for v in range((ga.N + 1) // 2):
-        cols = min(2, ga.N - 2 * v)
         prev = None
         for k in range((ga.K + 1) // 2):
-            rows = min(2, ga.K - 2 * k)
-            q = rows * cols * n
+            q = int(dims[2 * v:2 * v + 2, 2 * k:2 * k + 2].sum())
             pair += 2 * q * q + (2 * q * prev if prev is not None else 0)
             prev = q
     pair *= T + 1

@@ -435,7 +435,8 @@ def arrays_from_problem(problem) -> GridArrays:
             s = problem.sub(i, j)
             if s.n != n or s.m != m:
                 raise DimensionMismatchError(
-                    "the B200 path needs uniform state/input dimensions across subsystems "
+                    "GridArrays hold one block size: mixed dimensions go through "
+                    "GpuSchurOperator(problem), which embeds them (embed.py) "
                     f"(got n={s.n}, m={s.m} at ({i}, {j}) vs n={n}, m={m})")
     ids = {}
     stacks = {}
@@ -581,6 +582,11 @@ def rhs_offset_device(problem, n=None, device="cuda"):
             K, N, T, n, blk.shape[2], *(ctypes.c_void_p(t.data_ptr()) for t in dev),
             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream)), "gq_build_offset")
     return out
+
+
+def problem_messages(problem):
+    """The reference's ``validate`` messages for a problem (``grid_problem.py:195-288``)."""
+    return _problem_messages(problem)
 
 
 def as_arrays(problem_or_arrays) -> GridArrays:

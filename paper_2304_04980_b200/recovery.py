@@ -61,13 +61,22 @@ def recover_solution(schur, multipliers) -> TrajectorySolution:
     """x = -Qinv (A' lam), u = -Rinv (B' lam) on the device (``recovery.py:50-65``)."""
     _check_schur(schur)
     ctx = schur._ctx
-    lam = _Vec(multipliers, schur.dim, "multipliers")
+    emb = ctx.embed
+    given = multipliers
+    if emb is not None:      # mixed dimensions: padded vectors on the device (embed.py)
+        multipliers = emb.expand_x(multipliers, "multipliers")
+    lam = _Vec(multipliers, ctx.dim, "multipliers")
     nu = int(ctx.lib.gq_input_dim(ctx.h))
     x = lam.like()
     u = _input_like(lam, nu)
     obj = ctypes.c_double()
     _lib.check(ctx.lib.gq_recover(ctx.h, lam.ptr, _ptr(x), _ptr(u), ctypes.byref(obj)),
                "recover_solution")
+    if emb is not None:
+        return TrajectorySolution(layout=emb.layout(), x_flat=emb.restrict_x(x),
+                                  u_flat=emb.restrict_u(u),
+                                  multipliers=_Vec(given, schur.dim, "multipliers").obj,
+                                  objective_value=float(obj.value))
     return TrajectorySolution(layout=schur.layout, x_flat=x, u_flat=u, multipliers=lam.obj,
                               objective_value=float(obj.value))
 
@@ -77,13 +86,19 @@ def kkt_residual(schur, sol: TrajectorySolution):
     _check_schur(schur)
     ctx = schur._ctx
     nu = int(ctx.lib.gq_input_dim(ctx.h))
-    lam = _Vec(sol.multipliers, schur.dim, "multipliers")
-    x = _Vec(sol.x_flat, schur.dim, "x")
-    if _torch_cuda(sol.u_flat):
-        u = _Vec(sol.u_flat, nu, "u") if nu else None
+    emb = ctx.embed
+    mult, xf, uf, offv = sol.multipliers, sol.x_flat, sol.u_flat, schur.offset
+    if emb is not None:
+        mult, xf = emb.expand_x(mult, "multipliers"), emb.expand_x(xf, "x")
+        uf = emb.expand_u(uf if _torch_cuda(uf) else np.asarray(uf, dtype=float).reshape(-1), "u")
+        offv = schur.arrays.offset
+    lam = _Vec(mult, ctx.dim, "multipliers")
+    x = _Vec(xf, ctx.dim, "x")
+    if _torch_cuda(uf):
+        u = _Vec(uf, nu, "u") if nu else None
     else:
-        u = _Vec(np.asarray(sol.u_flat, dtype=float).reshape(-1), nu, "u") if nu else None
-    off = _Vec(schur.offset, schur.dim, "offset")
+        u = _Vec(np.asarray(uf, dtype=float).reshape(-1), nu, "u") if nu else None
+    off = _Vec(offv, ctx.dim, "offset")
     if nu == 0:
         raise DimensionMismatchError("problem has no inputs")
     out = (ctypes.c_double * 3)()

@@ -138,6 +138,7 @@ class _Context:
         self.h = handle
         self.dim = int(lib.gq_dim(handle))
         self.L, self.S = int(inner_sweeps), int(outer_sweeps)
+        self.embed = None   # embed.Embedding when the problem has mixed dimensions
 
     def set_sweeps(self, inner, outer):
         if (inner, outer) != (self.L, self.S):
@@ -145,10 +146,12 @@ class _Context:
             self.L, self.S = int(inner), int(outer)
 
     def unary(self, fn, x, name="x"):
+        if self.embed is not None:
+            x = self.embed.expand_x(x, name)
         v = _Vec(x, self.dim, name)
         out = v.like()
         _lib.check(getattr(self.lib, fn)(self.h, v.ptr, _ptr(out)), fn)
-        return out
+        return out if self.embed is None else self.embed.restrict_x(out)
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -168,13 +171,28 @@ class GpuSchurOperator:
     """
 
     def __init__(self, problem, inner_sweeps=2, outer_sweeps=2):
+        self._embed = None
+        if not isinstance(problem, GridArrays):
+            from .embed import Embedding, is_heterogeneous
+            from .problem import problem_messages
+            if is_heterogeneous(problem):
+                # mixed state/input dimensions (grid_problem.py:103-141): solve the padded
+                # uniform problem, map vectors at the interface (embed.py)
+                msgs = problem_messages(problem)
+                if msgs:
+                    raise ValueError("invalid problem: " + "; ".join(msgs))
+                self._embed = Embedding(problem)
+                self._hetero_problem = problem
+                problem = self._embed.padded_problem(problem)
         self.arrays = as_arrays(problem)
         self._problem = None if isinstance(problem, GridArrays) else problem
         self._ctx = _Context(self.arrays, inner_sweeps, outer_sweeps)
-        self.dim = self._ctx.dim
-        self.layout = self.arrays.layout
+        self._ctx.embed = self._embed
+        self.dim = self._ctx.dim if self._embed is None else self._embed.dim
+        self.layout = self.arrays.layout if self._embed is None else self._embed.layout()
         self.pairs = self.layout.pairs
-        self.offset = self.arrays.offset
+        self.offset = (self.arrays.offset if self._embed is None
+                       else self._embed.restrict_x(self.arrays.offset))
         self._counts = {}
 
     def offset_device(self):
@@ -183,13 +201,16 @@ class GpuSchurOperator:
         import torch
 
         if self._problem is not None:
-            return rhs_offset_device(self._problem, self.arrays.n)
+            off = rhs_offset_device(self._problem, self.arrays.n)
+            return off if self._embed is None else self._embed.restrict_x(off)
         return torch.as_tensor(self.arrays.offset, device="cuda")
 
     def counts(self, inner_sweeps=2, outer_sweeps=2):
         key = (inner_sweeps, outer_sweeps)
         if key not in self._counts:
-            self._counts[key] = counters(self.arrays, inner_sweeps, outer_sweeps)
+            emb = self._embed
+            self._counts[key] = counters(self.arrays, inner_sweeps, outer_sweeps,
+                                         nd=None if emb is None else emb.nd)
         return self._counts[key]
 
     @property
@@ -274,7 +295,10 @@ class GpuNestedJacobiPreconditioner:
         ctx = self.schur._ctx
         max_outer = int(max_outer)
         msg = f"nested Jacobi did not converge within {max_outer} outer sweeps"
-        v = _Vec(rhs, self.dim, "rhs")
+        emb = ctx.embed
+        if emb is not None:
+            rhs = emb.expand_x(rhs, "rhs")
+        v = _Vec(rhs, ctx.dim, "rhs")
         if max_outer < 1:            # the reference loop never runs
             raise MaxIterationsExceeded(msg, iterate=None, iterations=max_outer)
         self._select()
@@ -282,6 +306,8 @@ class GpuNestedJacobiPreconditioner:
         outers = ctypes.c_int64()
         rc = ctx.lib.gq_nbjm_solve(ctx.h, v.ptr, float(tol), max_outer, _ptr(out),
                                    ctypes.byref(outers))
+        if emb is not None:
+            out = emb.restrict_x(out)
         if rc == _lib.GQ_MAX_ITER:
             raise MaxIterationsExceeded(msg, iterate=out, iterations=max_outer)
         _lib.check(rc, "nbjm_solve")
@@ -360,8 +386,12 @@ def pcg_solve(schur, preconditioner, rhs, tol=1e-9, max_steps=None, x0=None, poo
                 f"(got {preconditioner.inner_sweeps}); odd budgets are standalone-only")
         preconditioner._select()
     start = time.perf_counter()
-    rv = _Vec(rhs, dim, "rhs")
-    x0v = _Vec(x0, dim, "x0") if x0 is not None else None
+    emb = ctx.embed
+    if emb is not None:      # mixed dimensions: the device works on the padded vectors
+        rhs = emb.expand_x(rhs, "rhs")
+        x0 = emb.expand_x(x0, "x0") if x0 is not None else None
+    rv = _Vec(rhs, ctx.dim, "rhs")
+    x0v = _Vec(x0, ctx.dim, "x0") if x0 is not None else None
     lib = ctx.lib
     _lib.check(lib.gq_pcg_start(ctx.h, rv.ptr, x0v.ptr if x0v else None, int(use_pc)), "pcg")
     steps = ctypes.c_int64()
@@ -386,6 +416,8 @@ def pcg_solve(schur, preconditioner, rhs, tol=1e-9, max_steps=None, x0=None, poo
             xk, rk = rv.like(), rv.like()
             _lib.check(lib.gq_pcg_read(ctx.h, _lib.GQ_VEC_X, _ptr(xk)))
             _lib.check(lib.gq_pcg_read(ctx.h, _lib.GQ_VEC_R, _ptr(rk)))
+            if emb is not None:
+                xk, rk = emb.restrict_x(xk), emb.restrict_x(rk)
             callback(steps.value, xk, rk)
             if conv.value:
                 break
@@ -395,6 +427,8 @@ def pcg_solve(schur, preconditioner, rhs, tol=1e-9, max_steps=None, x0=None, poo
         raise BreakdownError(_lib.last_error())
     nsteps = int(steps.value)
     _lib.check(lib.gq_pcg_read(ctx.h, _lib.GQ_VEC_X, _ptr(x)))
+    if emb is not None:
+        x = emb.restrict_x(x)
     hist = np.empty(nsteps)
     if nsteps:
         _lib.check(lib.gq_pcg_history(ctx.h, hist.ctypes.data, nsteps))

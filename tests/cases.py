@@ -113,3 +113,36 @@ def sparse_couplings(K=5, N=5, T=4, n=2, m=1, seed=11):
         subs.append(row)
         init.append(irow)
     return GridLQProblem(K, N, T, subs, BoundaryData(init=init))
+
+
+def hetero_problem(K=3, N=4, T=4, seed=21):
+    """Mixed state (1..3) and input (1..2) dimensions (grid_problem.py:103-141): couplings
+    map the neighbour's state into the node's, every block stage-invariant, a boundary
+    trajectory on the north edge."""
+    rng = np.random.default_rng(seed)
+    nd = [[1 + (i + 2 * j) % 3 for j in range(N)] for i in range(K)]
+    md = [[1 + (i + j) % 2 for j in range(N)] for i in range(K)]
+    nbr = {"west": (0, -1), "east": (0, 1), "north": (-1, 0), "south": (1, 0)}
+    subs, init = [], []
+    for i in range(K):
+        row, irow = [], []
+        for j in range(N):
+            n, m = nd[i][j], md[i][j]
+            a = 0.6 * np.eye(n) + 0.15 * rng.uniform(-1, 1, (n, n))
+            q = np.eye(n) * rng.uniform(1.0, 3.0) + 0.1 * np.ones((n, n))
+            r = np.eye(m) * rng.uniform(0.5, 2.0)
+            kw = {}
+            for d, (di, dj) in nbr.items():
+                ii, jj = i + di, j + dj
+                inside = 0 <= ii < K and 0 <= jj < N
+                if not inside and d != "north":
+                    continue                            # only the north edge has a trajectory
+                cols = nd[ii][jj] if inside else n      # off-grid: boundary signal of size n
+                kw[d] = [0.08 * rng.uniform(-1, 1, (n, cols))] * T
+            row.append(SubsystemData(n=n, m=m, A=[a] * T, B=[rng.uniform(-1, 1, (n, m))] * T,
+                                     Q=[q] * (T + 1), R=[r] * T, **kw))
+            irow.append(rng.uniform(-1, 1, n))
+        subs.append(row)
+        init.append(irow)
+    north = [[rng.uniform(-1, 1, nd[0][j]) for _ in range(T)] for j in range(N)]
+    return GridLQProblem(K, N, T, subs, BoundaryData(init=init, north=north))
