@@ -34,6 +34,11 @@ def is_heterogeneous(problem) -> bool:
                for i in range(problem.K) for j in range(problem.N))
 
 
+def needs_embedding(problem) -> bool:
+    """Mixed dimensions, or a uniform state dimension the kernels are not compiled for."""
+    return is_heterogeneous(problem) or problem.sub(0, 0).n not in SUPPORTED_N
+
+
 def _pad_block(block, rows, cols, unit_diag):
     a = np.asarray(block, dtype=float)
     out = np.zeros((rows, cols))

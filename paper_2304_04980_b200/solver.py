@@ -173,11 +173,12 @@ class GpuSchurOperator:
     def __init__(self, problem, inner_sweeps=2, outer_sweeps=2):
         self._embed = None
         if not isinstance(problem, GridArrays):
-            from .embed import Embedding, is_heterogeneous
+            from .embed import Embedding, needs_embedding
             from .problem import problem_messages
-            if is_heterogeneous(problem):
-                # mixed state/input dimensions (grid_problem.py:103-141): solve the padded
-                # uniform problem, map vectors at the interface (embed.py)
+            if needs_embedding(problem):
+                # mixed state/input dimensions (grid_problem.py:103-141), or a uniform state
+                # dimension without compiled kernels (5, 6, 7): solve the padded uniform
+                # problem, map vectors at the interface (embed.py)
                 msgs = problem_messages(problem)
                 if msgs:
                     raise ValueError("invalid problem: " + "; ".join(msgs))

@@ -99,3 +99,30 @@ def test_hetero_operator_preconditioner_and_pcg(gpu):
     assert sol.state(1, 2).shape == (p.T + 1, p.sub(1, 2).n)
     rx, ru, rdyn = kkt_residual(op, sol)
     assert rx <= 1e-12 and ru <= 1e-12 and rdyn <= 10 * float(g["kkt"][2]) + 1e-12
+
+
+@pytest.mark.gpu
+def test_uniform_dimension_without_compiled_kernels(gpu):
+    """n = 5 has no compiled kernels; as a GridLQProblem it runs embedded in n = 8 and matches
+    the numpy oracle (which restates the reference for any n) step for step."""
+    from oracle.gridlq_oracle import Oracle, pcg
+    from paper_2304_04980_b200 import (GpuNestedJacobiPreconditioner, GpuSchurOperator,
+                                       MaxIterationsExceeded, generators, pcg_solve)
+    from paper_2304_04980_b200.problem import arrays_to_problem
+    ga = generators.random_case(4, 5, 3, 5, 2, seed=0)
+    op = GpuSchurOperator(arrays_to_problem(ga), 2, 2)
+    assert op.dim == ga.dim and op._embed.n == 8
+    pc = GpuNestedJacobiPreconditioner(op, 2, 2)
+    orc = Oracle(ga, 2, 2)
+    v = np.random.default_rng(1).standard_normal(ga.dim)
+    ref = orc.apply_delta(v)
+    assert np.max(np.abs(op.apply(v) - ref)) <= 1e-12 * np.max(np.abs(ref))
+    xo, ho, so, _, _ = pcg(orc, ga.offset, tol=1e-30, max_steps=12)
+    try:
+        x, rep = pcg_solve(op, pc, ga.offset, tol=1e-30, max_steps=12)
+    except MaxIterationsExceeded as exc:
+        x, rep = exc.iterate, exc.report
+    h, ho = np.array(rep.residual_inf_history), np.array(ho)
+    assert rep.steps == so == 12
+    assert np.all(np.abs(h - ho) <= 1e-9 * ho + 1e-14 * ho[0])
+    assert np.max(np.abs(x - xo)) <= 1e-9 * np.max(np.abs(xo))
