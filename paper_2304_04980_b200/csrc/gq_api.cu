@@ -403,6 +403,7 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
       c->chain = true;
+      c->st8 = st8_supported(g, c->nxc);   // n = 4: DMMA block stencils (two nodes per warp)
     }
   }
 
@@ -610,12 +611,12 @@ static int enqueue_outer(gq_ctx* c, int s, int l0, int l1, const double* rin, do
       if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->gsh,
                        c->partials, st, kDotNone, c->stream));
-      } else if (c->fast) {
-        CK(launch_stencil3(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->sh_outer,
-                           c->partials, st, kDotNone, c->stream));
       } else if (c->st8) {
         CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kOuterRhs, c->dl[(s - 1) % 2], rin,
                       c->rs, c->sm_count, c->partials, st, kDotNone, c->stream));
+      } else if (c->fast) {
+        CK(launch_stencil3(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->sh_outer,
+                           c->partials, st, kDotNone, c->stream));
       } else {   // chain sweeps without the fast stencils: generic Xi~ apply + add
         CK(launch_stencil(c->g, c->op, kOuter, c->dl[(s - 1) % 2], c->rs, c->sh_outer,
                           c->partials, st, kDotNone, c->stream));
@@ -718,13 +719,13 @@ extern "C" int gq_nbjm_solve(gq_ctx* c, const double* rhs, double tol, int64_t m
         CK(launch_grid(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->gsh, c->partials,
                        nullptr, kDotNone, c->stream));
         rhs_s = c->rs;
-      } else if (c->fast) {
-        CK(launch_stencil3(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->sh_outer,
-                           c->partials, nullptr, kDotNone, c->stream));
-        rhs_s = c->rs;
       } else if (c->st8) {
         CK(launch_st8(c->g, c->op, c->co.seg, c->co.nseg, kOuterRhs, delta, c->r, c->rs,
                       c->sm_count, c->partials, nullptr, kDotNone, c->stream));
+        rhs_s = c->rs;
+      } else if (c->fast) {
+        CK(launch_stencil3(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->sh_outer,
+                           c->partials, nullptr, kDotNone, c->stream));
         rhs_s = c->rs;
       } else if (c->chain) {
         CK(launch_stencil(c->g, c->op, kOuter, delta, c->rs, c->sh_outer, c->partials, nullptr,

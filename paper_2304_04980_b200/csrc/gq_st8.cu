@@ -150,6 +150,159 @@ __device__ __forceinline__ void st8_body(const Geo& g, const Ops& op, const int4
   }
 }
 
+// ---- n = 4: two vertically adjacent nodes per warp ------------------------------------------
+// A 4 x 4 block is one k-step (K = 4 = the input node's features); the N = 8 outputs are the
+// 4 features of node a1 = (i, j) and the 4 of a2 = (i + 1, j).  For every input node z of the
+// union of the two stencils one DMMA computes both contributions:
+//   D[stage][out] += x_z[stage][k] * B[k][out],  B[k][out] = Blk(a1, z)[out][k]  (out < 4)
+//                                                           Blk(a2, z)[out-4][k] (out >= 4)
+// A fragment: lane (rw, qd) holds x_z[t0 + rw][qd]; B fragment: lane (qd, rw) holds the entry
+// above (zero where z is outside that node's stencil); D fragment: lane (rw, qd) holds two
+// consecutive outputs of node a1 (qd < 2) or a2 (qd >= 2) at stage t0 + rw.  Union of the two
+// 13-point diamonds: 18 input nodes; of the two 5-point stencils: 8 (times two stages).
+namespace {
+// input node z = a1 + (di, dj); o1 / o2 = its 13-point index as seen from a1 / a2, or -1
+__device__ constexpr int U13_DI[18] = {-2, -1, 0, 1, 2, 3, -1, 0, 1, 2, -1, 0, 1, 2, 0, 1, 0, 1};
+__device__ constexpr int U13_DJ[18] = {0, 0, 0, 0, 0, 0, -1, -1, -1, -1, 1, 1, 1, 1, -2, -2, 2, 2};
+__device__ constexpr int U13_O1[18] = {5, 1, 0, 2, 6, -1, 9, 3, 11, -1, 10, 4, 12, -1, 7, -1, 8, -1};
+__device__ constexpr int U13_O2[18] = {-1, 5, 1, 0, 2, 6, -1, 9, 3, 11, -1, 10, 4, 12, -1, 7, -1, 8};
+// the same for the 5-point stencil (self, north, south, west, east)
+__device__ constexpr int U5_DI[8] = {-1, 0, 1, 2, 0, 1, 0, 1};
+__device__ constexpr int U5_DJ[8] = {0, 0, 0, 0, -1, -1, 1, 1};
+__device__ constexpr int U5_U1[8] = {1, 0, 2, -1, 3, -1, 4, -1};
+__device__ constexpr int U5_U2[8] = {-1, 1, 0, 2, -1, 3, -1, 4};
+}  // namespace
+
+template <int MODE>
+__global__ void __launch_bounds__(32, MODE == kDelta ? 32 : 16) k_st4(Geo g, Ops op, const int4* __restrict__ seg, int nseg,
+                                            const double* __restrict__ x,
+                                            const double* __restrict__ rin,
+                                            double* __restrict__ y, double* partials,
+                                            PcgState* st, int dotmode) {
+  constexpr int NS = 4, B2 = 16;
+  if (st != nullptr) {
+    if (dotmode == kDotStep) {
+      const bool stop = st->done || st->step >= st->max_steps;
+      if (blockIdx.x == 0 && threadIdx.x == 0) st->skip = stop ? 1 : 0;
+      if (stop) return;
+    } else if (halted(st)) {
+      return;
+    }
+  }
+  const int lane = threadIdx.x, rw = lane >> 2, qd = lane & 3;
+  const long long rs = (long long)g.TS * NS, cs = (long long)g.K * rs;
+  const int kp = (g.K + 1) / 2;                       // node pairs per column
+  const long long npairs = (long long)kp * g.N;
+  const int which = rw >> 2, orow = rw & 3;           // my B entry: node a1 / a2, output row
+  double dot = 0.0;
+  // items = (node pair, stage chunk): the chunks of a pair go to consecutive warps
+#pragma unroll 1
+  for (long long item = blockIdx.x; item < npairs * nseg; item += gridDim.x) {
+    const long long pr = item / nseg;
+    const int sgi = (int)(item - pr * nseg);
+    const int j = (int)(pr / kp), i1 = 2 * (int)(pr % kp);
+    const bool has2 = i1 + 1 < g.K;
+    const long long node1 = (long long)j * g.K + i1;
+    const long long mynode = node1 + which;           // the node my B entries belong to
+    const bool bok = which == 0 || has2;
+    // my output: node a1 (qd < 2) or a2, features 2 (qd & 1), +1
+    const int onode = qd >> 1;
+    const bool ook = onode == 0 || has2;
+    const long long obase = (long long)j * cs + (long long)(i1 + onode) * rs + 2 * (qd & 1);
+    {
+      const int4 sg = seg[sgi];
+      const int t0 = sg.x, nvalid = sg.y, pc = sg.z;
+      const int t = t0 + rw;
+      const bool tv = rw < nvalid;
+      double2 acc[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) acc[a] = make_double2(0.0, 0.0);
+      if (MODE == kDelta) {
+        const double* P = op.psi + ((long long)pc * g.nk + mynode) * 13 * B2 + orow * NS + qd;
+#pragma unroll
+        for (int e = 0; e < 18; ++e) {
+          const int ii = i1 + U13_DI[e], jj = j + U13_DJ[e];
+          const bool zok = ii >= 0 && ii < g.K && jj >= 0 && jj < g.N;
+          const double av = (zok && tv) ? __ldg(x + (long long)jj * cs + (long long)ii * rs +
+                                                (long long)t * NS + qd)
+                                        : 0.0;
+          const int o = which == 0 ? U13_O1[e] : U13_O2[e];
+          const double bv = (o >= 0 && bok) ? __ldg(P + o * B2) : 0.0;
+          dmma(acc[e & 3], av, bv);
+        }
+      }
+      // Xi_{t-1} x_{t-1} (t >= 1) and Xi_t' x_{t+1} (t + 1 <= T)
+      const bool tm = tv && t >= 1, tp = tv && t + 1 < g.T1;
+      double2 em = make_double2(0.0, 0.0), ep = em;
+      const double* xi = op.xi + mynode * 5 * B2 + orow * NS + qd;       // nxc == 1
+      const double* xit = op.xit + mynode * 5 * B2 + orow * NS + qd;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int ii = i1 + U5_DI[e], jj = j + U5_DJ[e];
+        const bool zok = ii >= 0 && ii < g.K && jj >= 0 && jj < g.N;
+        const double* xz = x + (long long)jj * cs + (long long)ii * rs + qd;
+        const double am = (zok && tm) ? __ldg(xz + (long long)(t - 1) * NS) : 0.0;
+        const double ap = (zok && tp) ? __ldg(xz + (long long)(t + 1) * NS) : 0.0;
+        const int u = which == 0 ? U5_U1[e] : U5_U2[e];
+        const double bm = (u >= 0 && bok) ? __ldg(xi + u * B2) : 0.0;
+        const double bp = (u >= 0 && bok) ? __ldg(xit + u * B2) : 0.0;
+        if (MODE == kDelta) {
+          dmma(acc[e & 3], am, bm);
+          dmma(acc[(e + 2) & 3], ap, bp);
+        } else {
+          dmma(em, am, bm);
+          dmma(ep, ap, bp);
+        }
+      }
+      double2 out;
+      if (MODE == kDelta) {
+        out = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+      } else {   // y = r + (-(Xi_{t-1} x_{t-1}) - Xi_t' x_{t+1})   (gq_grid.cu convention)
+        const double2 rv = (tv && ook) ? ld16(rin + obase + (long long)t * NS)
+                                       : make_double2(0.0, 0.0);
+        out.x = rv.x + ((0.0 - em.x) - ep.x);
+        out.y = rv.y + ((0.0 - em.y) - ep.y);
+      }
+      if (tv && ook && (MODE != kDelta || slab_owned(g, t))) {
+        *reinterpret_cast<double2*>(y + obase + (long long)t * NS) = out;
+        if (MODE == kDelta && dotmode != kDotNone) {
+          const double2 xs = ld16(x + obase + (long long)t * NS);
+          dot = fma(out.x, xs.x, dot);
+          dot = fma(out.y, xs.y, dot);
+        }
+      }
+    }
+  }
+  if (MODE == kDelta && dotmode != kDotNone) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    int last = 0;
+    if (lane == 0) {
+      partials[blockIdx.x] = dot;
+      __threadfence();
+      last = atomicAdd(&st->counter[0], 1u) == gridDim.x - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence();
+      double acc = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) acc += __ldcg(partials + b);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        st->counter[0] = 0u;
+        st->curv = acc;                      // pcg.py:101-108
+        if (acc <= 0.0) {
+          st->breakdown = 1;
+          st->done = 1;
+        } else {
+          st->alpha = st->mu / acc;
+        }
+      }
+    }
+  }
+}
+
 // Delta: uncapped (102 registers; every cap tried was slower: 96 -> 3.80 ms, 80 -> 3.17 ms
 // vs 2.52 ms at config 5).  Outer rhs: capped at 64 registers (from 66 at the default
 // bound, 122 at a looser one), 1.078 -> 0.997 ms.
@@ -176,13 +329,23 @@ static int s8env(const char* name, int dflt) {
 }
 
 bool st8_supported(const Geo& g, int nxc) {
-  return g.n == 8 && nxc == 1 && s8env("GQ_NO_ST8", 0) == 0;
+  return (g.n == 8 || g.n == 4) && nxc == 1 && s8env("GQ_NO_ST8", 0) == 0;
 }
 
 template <int MODE>
 static cudaError_t st8_launch(const Geo& g, const Ops& op, const int4* seg, int nseg,
                               const double* x, const double* rin, double* y, int sm_count,
                               double* partials, PcgState* st, int dotmode, cudaStream_t s) {
+  if (g.n == 4) {
+    static int cache4[64] = {0};
+    int per_sm4 = 1;
+    cudaError_t e4 = kernel_occupancy(k_st4<MODE>, 32, 0, cache4, per_sm4);
+    if (e4 != cudaSuccess) return e4;
+    const long long items = (long long)((g.K + 1) / 2) * g.N * nseg;
+    const long long blocks4 = std::min<long long>(items, (long long)per_sm4 * sm_count);
+    k_st4<MODE><<<(unsigned)blocks4, 32, 0, s>>>(g, op, seg, nseg, x, rin, y, partials, st, dotmode);
+    return cudaGetLastError();
+  }
   static int cache[64] = {0};
   int per_sm = 1;
   cudaError_t e = MODE == kDelta ? kernel_occupancy(k_st8<kDelta>, 32, 0, cache, per_sm)
