@@ -253,8 +253,11 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   {
     const char* np = getenv("GQ_NO_PAD");
     const int first = (g.T1 > 1 && pcls[0] != pcls[1]) ? 1 : 0;
-    c->t0pad = (np && *np == '1') ? 0 : (8 - first) % 8;
-    g.TS = (np && *np == '1') ? g.T1 : (c->t0pad + g.T1 + 7) / 8 * 8;
+    // short horizons stay dense: the padding must not cost more than a quarter of the bytes
+    const int padded = ((8 - first) % 8 + g.T1 + 7) / 8 * 8;
+    const bool dense = (np && *np == '1') || 4 * padded > 5 * g.T1;
+    c->t0pad = dense ? 0 : (8 - first) % 8;
+    g.TS = dense ? g.T1 : padded;
     g.T0 = c->t0pad;
     g.span = (g.nk - 1) * (long long)g.TS * g.n + (long long)g.T1 * g.n;
   }
