@@ -66,7 +66,7 @@ struct gq_ctx {
   int4* seg = nullptr;
   ChainOps co{};
   bool chain = false;          // lean DMMA chain sweeps (n in {2, 4})
-  bool fuse_x = false;         // x update fused into the direction update (opt-in)
+  bool fuse_x = false;         // x update fused into the direction update (L2-resident sizes)
   bool fuse_r = false;         // r update fused into the first outer sweep (chain kernel)
   bool grid = false;           // lean n = 2 grid stencils
   bool dstep = false;          // t-loop factored Delta apply (n = 2)
@@ -211,12 +211,6 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   c->L = inner_sweeps;
   c->S = outer_sweeps;
   c->n_dyn = D.n_dyn;
-  {
-    // measured at the headline (tools/steptime.py): the x update on its own graph branch
-    // overlaps the sweeps and beats the fused direction update by ~1.3%; fusion is opt-in
-    const char* e = getenv("GQ_FUSE_X");
-    c->fuse_x = e && *e == '1';
-  }
   c->n_cost = D.n_cost;
   Geo& g = c->g;
   g.K = D.K;
@@ -228,6 +222,14 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   g.nb = (D.K + 1) / 2;
   g.nk = (long long)D.K * D.N;
   g.dim = g.nk * D.n * g.T1;
+  {
+    // x += alpha d: at the headline its own graph branch overlaps the sweeps and beats the
+    // fused direction update by ~1% (tools/steptime.py); when the vectors fit in L2 the step
+    // is launch- and latency-bound and one kernel less wins (configs 1-3: +3-4%).
+    // GQ_FUSE_X=0/1 overrides.
+    const char* e = getenv("GQ_FUSE_X");
+    c->fuse_x = (e && *e) ? *e == '1' : g.dim * 8 <= (32LL << 20);
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev);

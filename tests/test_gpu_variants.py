@@ -19,6 +19,7 @@ VARIANTS = {
     "chainm": {"GQ_CHAINM": "2"},                # twelve-warp chain sweeps (every form) on the n=2 cases
     "dstep": {"GQ_DSTEP": "1"},                  # t-loop Delta on every (small) golden case
     "fuse_x": {"GQ_FUSE_X": "1"},                # x update fused into the direction update
+    "no_fuse_x": {"GQ_FUSE_X": "0"},             # ... and on its own graph branch for small sizes
     "no_fuse_r": {"GQ_NO_FUSE_R": "1"},          # separate r update kernel
     "no_fuse": {"GQ_NO_FUSE_R": "1", "GQ_NO_FORK": "1"},
     "no_fork": {"GQ_NO_FORK": "1"},              # x update in line instead of on a branch
