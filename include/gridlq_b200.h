@@ -163,6 +163,11 @@ int gq_build_offset(int32_t K, int32_t N, int32_t T, int32_t n, int32_t ncls,
                     const double* init, const double* blocks, const int32_t* cls,
                     const double* traj, double* out, void* stream);
 
+/* Host helper of the solver API (no reference counterpart: numpy's pcg_solve returns a fresh
+ * array, pcg.py:83): fault in the pages of a fresh host result buffer from several threads
+ * while the device iterates, so the device-to-host copy does not wait for the page faults. */
+void gq_touch_pages(void* p, int64_t bytes);
+
 /* Measurement helpers (bench.py): run `steps` PCG steps as individual launches with CUDA
  * events around every kernel; per-kernel total milliseconds go to ms_out[0..count) in the
  * order gq_kernel_name(ctx, i) reports.  Returns the number of kernels per step. */

@@ -531,6 +531,12 @@ static int import_vec(gq_ctx* c, const double* src, double* dst) {
     }
     ref = c->tmp1;
   }
+  if (c->g.TS != c->g.T1 || c->t0pad)
+    // padded layout: the transpose writes the real stages only; clear the padding too, so
+    // that nothing a previous solve left there (NaN scalars after a breakdown) reaches the
+    // flat reductions
+    CK(cudaMemsetAsync(dst - (size_t)c->t0pad * c->g.n, 0,
+                       ((size_t)c->g.span + (size_t)c->t0pad * c->g.n) * 8, c->stream));
   CK(launch_to_internal(c->g, ref, dst, c->stream));
   return GQ_OK;
 }
@@ -561,6 +567,30 @@ static void parallel_copy(double* dst, const double* src, size_t n) {
     const size_t b = i * per, e = std::min(n, b + per);
     if (b >= e) break;
     th.emplace_back([=] { memcpy(dst + b, src + b, (e - b) * 8); });
+  }
+  for (auto& t : th) t.join();
+}
+
+// Fault in the pages of a fresh host buffer from several threads (one write per 4 KiB page):
+// the result array of a solve is 211 MB at the headline, and a single thread takes tens of
+// milliseconds to touch it on some hosts -- as long as the whole 20-step solve.
+extern "C" void gq_touch_pages(void* p, int64_t bytes) {
+  if (!p || bytes <= 0) return;
+  char* base = static_cast<char*>(p);
+  const size_t n = (size_t)bytes, page = 4096;
+  unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (n < (8u << 20)) nt = 1;
+  const size_t pages = (n + page - 1) / page, per = (pages + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (unsigned i = 0; i < nt; ++i) {
+    const size_t b = i * per, e = std::min(pages, b + per);
+    if (b >= e) break;
+    th.emplace_back([=] {
+      for (size_t q = b; q < e; ++q) {
+        volatile char* c = base + q * page;
+        *c = 0;
+      }
+    });
   }
   for (auto& t : th) t.join();
 }

@@ -99,9 +99,9 @@ class _Vec:
 
 
 def _touch_pages(arr):
-    """Write one element per 4 KiB page so a fresh host array is resident before the
-    device-to-host copy lands in it."""
-    arr[::512] = 0.0
+    """Write one byte per 4 KiB page (from several threads, ``gq_touch_pages``) so a fresh
+    host array is resident before the device-to-host copy lands in it."""
+    _lib.load().gq_touch_pages(ctypes.c_void_p(arr.ctypes.data), arr.nbytes)
 
 
 def _ptr(out):

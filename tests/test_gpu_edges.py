@@ -76,3 +76,28 @@ def test_n8_kernels_against_generic_multi_round():
                     os.environ[k] = val
     assert rel_err(out["fast"][0], out["generic"][0]) < 1e-12
     assert rel_err(out["fast"][1], out["generic"][1]) < 1e-11
+
+
+def test_solves_after_a_breakdown_on_a_padded_context():
+    """Padded vector layout (T1 >= 60): a breakdown (curvature underflow) must not leave
+    anything in the padding stages that reaches the flat reductions of the next solve -- plain
+    CG afterwards (d.r and r.r over the padded span) reproduces the oracle."""
+    from oracle.gridlq_oracle import Oracle, pcg
+    from paper_2304_04980_b200 import (BreakdownError, GpuNestedJacobiPreconditioner,
+                                       GpuSchurOperator, MaxIterationsExceeded, cg_solve,
+                                       generators, pcg_solve)
+    ga = generators.config2(0, K=6, N=6, T=63)
+    op = GpuSchurOperator(ga, 2, 2)
+    pc = GpuNestedJacobiPreconditioner(op, 2, 2)
+    with pytest.raises(BreakdownError):
+        pcg_solve(op, pc, ga.offset * 1e-170, tol=1e-320, max_steps=5)
+    orc = Oracle(ga, 2, 2)
+    xo, ho, so, _, _ = pcg(orc, ga.offset, tol=1e-30, max_steps=15, precond=False)
+    try:
+        x, rep = cg_solve(op, ga.offset, tol=1e-30, max_steps=15)
+    except MaxIterationsExceeded as exc:
+        x, rep = exc.iterate, exc.report
+    h, ho = np.array(rep.residual_inf_history), np.array(ho)
+    assert rep.steps == so == 15 and np.all(np.isfinite(h))
+    assert np.all(np.abs(h - ho) <= 1e-9 * ho + 1e-14 * ho[0])
+    assert np.max(np.abs(x - xo)) <= 1e-9 * np.max(np.abs(xo))
