@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <functional>
 #include <thread>
+#include <sys/mman.h>
 
 #include "gq_internal.h"
 #include "../../include/gridlq_b200.h"
@@ -578,6 +579,13 @@ extern "C" void gq_touch_pages(void* p, int64_t bytes) {
   if (!p || bytes <= 0) return;
   char* base = static_cast<char*>(p);
   const size_t n = (size_t)bytes, page = 4096;
+  {
+    // ask for transparent huge pages on the 2 MiB-aligned interior (best effort: 100 faults
+    // instead of 51k for a 211 MB buffer, and a TLB-friendlier host copy afterwards)
+    const uintptr_t lo = (reinterpret_cast<uintptr_t>(base) + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(base) + n) & ~(uintptr_t)((2u << 20) - 1);
+    if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+  }
   unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   if (n < (8u << 20)) nt = 1;
   const size_t pages = (n + page - 1) / page, per = (pages + nt - 1) / nt;
