@@ -24,3 +24,25 @@ def test_kernel_passes_and_families():
     assert "outer sweep" in fam["sweep_s1_l0"] and "r update" not in fam["sweep_s1_l0"]
     assert "r update" in fam["sweep_s0_l0_r"]
     assert fam["delta"].startswith("delta") and fam["outer_rhs_s1"].startswith("outer rhs")
+
+
+def test_every_arm_prints_the_same_config_object():
+    """The product, stage-slab and reference arms describe one workload with one `config`
+    object (same keys, same values), so the driver's config comparison matches."""
+    import argparse
+
+    from paper_2304_04980_b200 import generators
+
+    ga = generators.config1(0)
+    args = argparse.Namespace(config=1, replicas=False)
+    a = bench.workload_config(args, ga, 2, 2, bench.parallelism_label(args, 1))
+    b = bench.workload_config(args, ga, 2, 2, "single GPU")
+    assert a == b and a["parallelism"] == "single GPU" and a["dim"] == ga.dim
+    assert set(a) == {"workload", "K", "N", "T", "n", "m", "outer_sweeps_S", "inner_sweeps_L",
+                      "dim", "parallelism", "l2"}
+    assert "fits in L2" in a["l2"]                      # config 1 is not an HBM measurement
+    big = generators.config4(0, K=8, N=8, T=4)
+    big_cfg = bench.workload_config(argparse.Namespace(config=4), big, 2, 2, "single GPU")
+    assert big_cfg["workload"].startswith("config4")
+    assert bench.parallelism_label(argparse.Namespace(replicas=False), 4) == "stage slabs x4"
+    assert bench.parallelism_label(argparse.Namespace(replicas=True), 4) == "replicas x4"
