@@ -68,6 +68,20 @@ def test_headline_100_fixed_steps():
     _check(res)
 
 
+@pytest.mark.parametrize("shape", [(16, 512, 200), (33, 255, 171)])
+def test_wide_grids_many_rounds_of_the_twelve_warp_kernel(shape):
+    """Grids whose chain items need more than two rounds of the twelve-warp kernel (6656 items
+    at 16 x 512 x 200: four rounds), and odd K / N / chunk counts with a partial last round
+    and a short last chunk, against the C oracle: 40 fixed steps."""
+    from paper_2304_04980_b200 import generators
+
+    K, N, T = shape
+    ga = generators.config4(3, K=K, N=N, T=T)
+    res = _solve_both(ga, 2, 2, 1e-300, 40)
+    assert res[2] == 40
+    _check(res)
+
+
 @pytest.mark.parametrize("L", [2, 4])
 def test_config3_200_fixed_steps(L):
     from paper_2304_04980_b200 import generators
