@@ -1373,7 +1373,7 @@ cudaError_t launch_stencil3(const Geo& g, const FastOps& fo, int mode, const dou
 int sweep3_warps(const Geo& g, int sm_count) {
   const int nchunk = (g.T1 + 31) / 32;
   const int n_items = g.V * nchunk;
-  const int wsm = std::max(1, env_int("GQ_SWEEP_WARPS_PER_SM", 4));
+  const int wsm = 4;   // warps per SM (measured round 1)
   return std::min(n_items, wsm * sm_count);
 }
 
@@ -1445,8 +1445,8 @@ static cudaError_t sweep4_n(const Geo& g, const FastOps& fo, bool inner, const d
                             double* partials, PcgState* st, int dotmode, cudaStream_t s) {
   // n = 4: the MT = 1 instantiation (255 registers + spills) faults with an illegal
   // instruction on B200; the two-tile variant is used instead.
-  const int mt = NS == 4 ? 2 : env_int("GQ_SWEEP_MT", 1);
-  const int wsm = env_int("GQ_SWEEP_WARPS_PER_SM", mt == 1 ? 8 : 4);
+  const int mt = NS == 4 ? 2 : 1;
+  const int wsm = mt == 1 ? 8 : 4;
   if (mt == 2) {
     if (inner) return sweep6_launch<NS, true, 2>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
     return sweep6_launch<NS, false, 2>(g, fo, rhs, th, out, rdot, sm_count, partials, st, dotmode, s, wsm);
