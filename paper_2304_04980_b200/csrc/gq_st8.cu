@@ -173,8 +173,10 @@ __device__ constexpr int U5_U1[8] = {1, 0, 2, -1, 3, -1, 4, -1};
 __device__ constexpr int U5_U2[8] = {-1, 1, 0, 2, -1, 3, -1, 4};
 }  // namespace
 
+constexpr int kSt4Group = 4;   // stage chunks per item: the B fragments are loaded once per item
+
 template <int MODE>
-__global__ void __launch_bounds__(32, MODE == kDelta ? 32 : 16) k_st4(Geo g, Ops op, const int4* __restrict__ seg, int nseg,
+__global__ void __launch_bounds__(32, 12) k_st4(Geo g, Ops op, const int4* __restrict__ seg, int nseg,
                                             const double* __restrict__ x,
                                             const double* __restrict__ rin,
                                             double* __restrict__ y, double* partials,
@@ -193,13 +195,14 @@ __global__ void __launch_bounds__(32, MODE == kDelta ? 32 : 16) k_st4(Geo g, Ops
   const long long rs = (long long)g.TS * NS, cs = (long long)g.K * rs;
   const int kp = (g.K + 1) / 2;                       // node pairs per column
   const long long npairs = (long long)kp * g.N;
+  const int ngr = (nseg + kSt4Group - 1) / kSt4Group;
   const int which = rw >> 2, orow = rw & 3;           // my B entry: node a1 / a2, output row
   double dot = 0.0;
-  // items = (node pair, stage chunk): the chunks of a pair go to consecutive warps
+  // items = (node pair, group of stage chunks): the groups of a pair go to consecutive warps
 #pragma unroll 1
-  for (long long item = blockIdx.x; item < npairs * nseg; item += gridDim.x) {
-    const long long pr = item / nseg;
-    const int sgi = (int)(item - pr * nseg);
+  for (long long item = blockIdx.x; item < npairs * ngr; item += gridDim.x) {
+    const long long pr = item / ngr;
+    const int gi = (int)(item - pr * ngr);
     const int j = (int)(pr / kp), i1 = 2 * (int)(pr % kp);
     const bool has2 = i1 + 1 < g.K;
     const long long node1 = (long long)j * g.K + i1;
@@ -209,7 +212,36 @@ __global__ void __launch_bounds__(32, MODE == kDelta ? 32 : 16) k_st4(Geo g, Ops
     const int onode = qd >> 1;
     const bool ook = onode == 0 || has2;
     const long long obase = (long long)j * cs + (long long)(i1 + onode) * rs + 2 * (qd & 1);
+    // A-fragment sources (stage 0) and validity of the input nodes
+    const double* xa = x + (long long)j * cs + (long long)i1 * rs + qd;
+    bool z13[18], z5[8];
+#pragma unroll
+    for (int e = 0; e < 18; ++e) {
+      const int ii = i1 + U13_DI[e], jj = j + U13_DJ[e];
+      z13[e] = ii >= 0 && ii < g.K && jj >= 0 && jj < g.N;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int ii = i1 + U5_DI[e], jj = j + U5_DJ[e];
+      z5[e] = ii >= 0 && ii < g.K && jj >= 0 && jj < g.N;
+    }
+    // B fragments of the Xi parts (one class: nxc == 1), loaded once per item
+    double bm[8], bp[8];
     {
+      const double* xi = op.xi + mynode * 5 * B2 + orow * NS + qd;
+      const double* xit = op.xit + mynode * 5 * B2 + orow * NS + qd;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int u = which == 0 ? U5_U1[e] : U5_U2[e];
+        bm[e] = (u >= 0 && bok) ? __ldg(xi + u * B2) : 0.0;
+        bp[e] = (u >= 0 && bok) ? __ldg(xit + u * B2) : 0.0;
+      }
+    }
+    double bpsi[MODE == kDelta ? 18 : 1];
+    int cur = -1;
+    const int s1 = min(nseg, (gi + 1) * kSt4Group);
+#pragma unroll 1
+    for (int sgi = gi * kSt4Group; sgi < s1; ++sgi) {
       const int4 sg = seg[sgi];
       const int t0 = sg.x, nvalid = sg.y, pc = sg.z;
       const int t = t0 + rw;
@@ -218,40 +250,37 @@ __global__ void __launch_bounds__(32, MODE == kDelta ? 32 : 16) k_st4(Geo g, Ops
 #pragma unroll
       for (int a = 0; a < 4; ++a) acc[a] = make_double2(0.0, 0.0);
       if (MODE == kDelta) {
-        const double* P = op.psi + ((long long)pc * g.nk + mynode) * 13 * B2 + orow * NS + qd;
+        if (pc != cur) {      // Psi B fragments of this stage class
+          const double* P = op.psi + ((long long)pc * g.nk + mynode) * 13 * B2 + orow * NS + qd;
+#pragma unroll
+          for (int e = 0; e < 18; ++e) {
+            const int o = which == 0 ? U13_O1[e] : U13_O2[e];
+            bpsi[e] = (o >= 0 && bok) ? __ldg(P + o * B2) : 0.0;
+          }
+          cur = pc;
+        }
 #pragma unroll
         for (int e = 0; e < 18; ++e) {
-          const int ii = i1 + U13_DI[e], jj = j + U13_DJ[e];
-          const bool zok = ii >= 0 && ii < g.K && jj >= 0 && jj < g.N;
-          const double av = (zok && tv) ? __ldg(x + (long long)jj * cs + (long long)ii * rs +
-                                                (long long)t * NS + qd)
-                                        : 0.0;
-          const int o = which == 0 ? U13_O1[e] : U13_O2[e];
-          const double bv = (o >= 0 && bok) ? __ldg(P + o * B2) : 0.0;
-          dmma(acc[e & 3], av, bv);
+          const double av = (z13[e] && tv) ? __ldg(xa + U13_DJ[e] * cs + U13_DI[e] * rs +
+                                                   (long long)t * NS)
+                                           : 0.0;
+          dmma(acc[e & 3], av, bpsi[e]);
         }
       }
       // Xi_{t-1} x_{t-1} (t >= 1) and Xi_t' x_{t+1} (t + 1 <= T)
       const bool tm = tv && t >= 1, tp = tv && t + 1 < g.T1;
       double2 em = make_double2(0.0, 0.0), ep = em;
-      const double* xi = op.xi + mynode * 5 * B2 + orow * NS + qd;       // nxc == 1
-      const double* xit = op.xit + mynode * 5 * B2 + orow * NS + qd;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int ii = i1 + U5_DI[e], jj = j + U5_DJ[e];
-        const bool zok = ii >= 0 && ii < g.K && jj >= 0 && jj < g.N;
-        const double* xz = x + (long long)jj * cs + (long long)ii * rs + qd;
-        const double am = (zok && tm) ? __ldg(xz + (long long)(t - 1) * NS) : 0.0;
-        const double ap = (zok && tp) ? __ldg(xz + (long long)(t + 1) * NS) : 0.0;
-        const int u = which == 0 ? U5_U1[e] : U5_U2[e];
-        const double bm = (u >= 0 && bok) ? __ldg(xi + u * B2) : 0.0;
-        const double bp = (u >= 0 && bok) ? __ldg(xit + u * B2) : 0.0;
+        const double* xz = xa + U5_DJ[e] * cs + U5_DI[e] * rs;
+        const double am = (z5[e] && tm) ? __ldg(xz + (long long)(t - 1) * NS) : 0.0;
+        const double ap = (z5[e] && tp) ? __ldg(xz + (long long)(t + 1) * NS) : 0.0;
         if (MODE == kDelta) {
-          dmma(acc[e & 3], am, bm);
-          dmma(acc[(e + 2) & 3], ap, bp);
+          dmma(acc[e & 3], am, bm[e]);
+          dmma(acc[(e + 2) & 3], ap, bp[e]);
         } else {
-          dmma(em, am, bm);
-          dmma(ep, ap, bp);
+          dmma(em, am, bm[e]);
+          dmma(ep, ap, bp[e]);
         }
       }
       double2 out;
@@ -341,7 +370,7 @@ static cudaError_t st8_launch(const Geo& g, const Ops& op, const int4* seg, int 
     int per_sm4 = 1;
     cudaError_t e4 = kernel_occupancy(k_st4<MODE>, 32, 0, cache4, per_sm4);
     if (e4 != cudaSuccess) return e4;
-    const long long items = (long long)((g.K + 1) / 2) * g.N * nseg;
+    const long long items = (long long)((g.K + 1) / 2) * g.N * ((nseg + kSt4Group - 1) / kSt4Group);
     const long long blocks4 = std::min<long long>(items, (long long)per_sm4 * sm_count);
     k_st4<MODE><<<(unsigned)blocks4, 32, 0, s>>>(g, op, seg, nseg, x, rin, y, partials, st, dotmode);
     return cudaGetLastError();
