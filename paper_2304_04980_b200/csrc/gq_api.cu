@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <functional>
 #include <thread>
+#include <tuple>
 #include <sys/mman.h>
 
 #include "gq_internal.h"
@@ -74,6 +75,8 @@ struct gq_ctx {
   DstepOps dso{};
   CUtensorMap map_d{}, map_tmp0{};   // TMA views of the Delta inputs (d, unit-apply scratch)
   CUtensorMap map_y{};               // ... and of its output
+  bool rstep = false;          // tiled outer rhs on the same TMA views
+  std::vector<std::tuple<const double*, int, CUtensorMap>> maps;   // (vector, halo) -> view
   bool st8 = false;            // n = 8 DMMA block stencils
   GridShape gsh{};
   bool fast = false;           // pipelined v2 kernels eligible (stage classes warp-compatible)
@@ -470,11 +473,13 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
     const char* f = getenv("GQ_FORCE_V1");
     if (dstep_supported(g) && dstep_preferred(g, c->sm_count) && !(e && *e == '1') &&
         !(f && *f == '1') &&
-        dstep_make_map(g, c->d, false, &c->map_d) &&
-        dstep_make_map(g, c->tmp0, false, &c->map_tmp0) &&
-        dstep_make_map(g, c->y, true, &c->map_y)) {
+        dstep_make_map(g, c->d, 2, &c->map_d) &&
+        dstep_make_map(g, c->tmp0, 2, &c->map_tmp0) &&
+        dstep_make_map(g, c->y, 0, &c->map_y)) {
       c->dso = DstepOps{c->A, c->C, c->qinv, c->brb, c->dcls, c->ccls};
       c->dstep = true;
+      const char* r = getenv("GQ_NO_RSTEP");
+      c->rstep = c->nxc == 1 && !(r && *r == '1');   // tiled outer rhs (one Xi class)
     }
   }
   c->sh_outer = stencil_shape(g, kOuter, c->sm_count);
@@ -642,6 +647,33 @@ static int export_vec(gq_ctx* c, const double* src, double* dst) {
   return GQ_OK;
 }
 
+// k_rstep's TMA view of a stage-inner vector (halo = 1: the x input), cached per pointer
+static const CUtensorMap* tma_view(gq_ctx* c, const double* v, int halo) {
+  for (auto& m : c->maps)
+    if (std::get<0>(m) == v && std::get<1>(m) == halo) return &std::get<2>(m);
+  CUtensorMap m;
+  if (!rstep_make_map(c->g, v, halo != 0, &m)) return nullptr;
+  if (c->maps.size() >= 32) c->maps.clear();   // callers' device vectors come and go
+  c->maps.emplace_back(v, halo, m);
+  return &std::get<2>(c->maps.back());
+}
+
+// y = rin + Xi~ x on the tiled kernel; false if a view cannot be built (caller falls back)
+static bool outer_rhs_tiled(gq_ctx* c, const double* x, const double* rin, double* y,
+                            PcgState* st, cudaError_t* err) {
+  if (!c->rstep) return false;
+  const CUtensorMap* mx = tma_view(c, x, 1);
+  if (!mx) return false;
+  const CUtensorMap xm = *mx;   // the cache may move on the next lookup
+  const CUtensorMap* mr = tma_view(c, rin, 0);
+  if (!mr) return false;
+  const CUtensorMap rm = *mr;
+  const CUtensorMap* my = tma_view(c, y, 0);
+  if (!my) return false;
+  *err = launch_rstep(c->g, xm, rm, *my, x, rin, y, c->xi, c->xit, st, c->sm_count, c->stream);
+  return true;
+}
+
 // Outer sweep s of the preconditioner, inner sweeps [l0, L) (the stage-slab phases run an
 // outer sweep in pieces; enqueue_precond runs them all).
 static int enqueue_outer(gq_ctx* c, int s, int l0, int l1, const double* rin, double* out,
@@ -651,7 +683,10 @@ static int enqueue_outer(gq_ctx* c, int s, int l0, int l1, const double* rin, do
   {
     if ((c->fast || c->chain) && s > 0 && l0 == 0) {
       // rhs_s = r + Xi~ delta_{s-1}, materialised once per outer sweep (nested_jacobi.py:119-121)
-      if (c->grid) {
+      cudaError_t te = cudaSuccess;
+      if (outer_rhs_tiled(c, c->dl[(s - 1) % 2], rin, c->rs, st, &te)) {
+        CK(te);
+      } else if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, c->dl[(s - 1) % 2], rin, c->rs, c->gsh,
                        c->partials, st, kDotNone, c->stream));
       } else if (c->st8) {
@@ -758,7 +793,11 @@ extern "C" int gq_nbjm_solve(gq_ctx* c, const double* rhs, double tol, int64_t m
     const double* rhs_s = c->r;
     const double* xi = nullptr;
     if (s > 0) {
-      if (c->grid) {
+      cudaError_t te = cudaSuccess;
+      if (outer_rhs_tiled(c, delta, c->r, c->rs, nullptr, &te)) {
+        CK(te);
+        rhs_s = c->rs;
+      } else if (c->grid) {
         CK(launch_grid(c->g, c->fo, kOuterRhs, delta, c->r, c->rs, c->gsh, c->partials,
                        nullptr, kDotNone, c->stream));
         rhs_s = c->rs;
@@ -831,8 +870,11 @@ extern "C" int gq_apply_outer_coupling(gq_ctx* c, const double* x, double* y) {
   int rc = import_vec(c, x, c->tmp0);
   if (rc) return rc;
   // the kernel the preconditioner runs (rhs = 0 + Xi~ x) where one is selected
-  if (c->grid) {
-    CK(cudaMemsetAsync(c->tmp1, 0, c->g.span * 8, c->stream));
+  cudaError_t te = cudaSuccess;
+  if (c->rstep || c->grid) CK(cudaMemsetAsync(c->tmp1, 0, c->g.span * 8, c->stream));
+  if (outer_rhs_tiled(c, c->tmp0, c->tmp1, c->y, nullptr, &te)) {
+    CK(te);
+  } else if (c->grid) {
     CK(launch_grid(c->g, c->fo, kOuterRhs, c->tmp0, c->tmp1, c->y, c->gsh, c->partials,
                    nullptr, kDotNone, c->stream));
   } else {

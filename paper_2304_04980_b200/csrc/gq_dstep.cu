@@ -458,6 +458,232 @@ __global__ void __launch_bounds__(NTHR, MINB) k_dstep(const __grid_constant__ CU
   }
 }
 
+// ---- outer rhs  y = r - (Xi_{t-1} x_{t-1} + Xi_t' x_{t+1})  by TMA tiles ------------------
+//
+// nested_jacobi.py:117-121 (rhs_s = r + Xi~ delta_{s-1}), kkt_assembly.py:414-425 (the
+// time-coupling part of Delta).  No plane exchange is needed here: with one Xi class the ten
+// 2 x 2 blocks of a node (Xi(a, .) and Xi(., a)') stay in registers and a thread forms y_t of
+// its node from x_{t-1} and x_{t+1} of its 5-point neighbourhood directly.
+//
+// A CTA (128 threads, two per SM) owns a 16 x 8 tile of nodes for a run of 8-stage chunks;
+// chunk c is stages 8c + 1 .. 8c + 8, whole 128-byte lines of the padded layout (stage 0 of a
+// tile is read and written straight from global memory when its first chunk starts).  Per
+// chunk one x box arrives by TMA -- the tile with a one-node halo, 128-byte rows with the
+// 128-byte swizzle, through a tensor map whose origin is stage 2, so that the box of chunk c
+// holds x_{t+1} for all of its stages -- and one r box of the tile; y is formed in the r box
+// and leaves by TMA from there.  The five points of x_{t+1} read at stage t stay in registers
+// and serve as x_{t-1} two stages later: 5 + 1 shared loads, 1 store and 40 DFMA per
+// node-stage, one __syncthreads per chunk.  The (tile, chunk) sequence is cut into equal
+// contiguous runs, one per CTA; both rings run through tile boundaries.
+//
+// Measured on the way (headline, one launch): 4-stage boxes as in k_dstep (64-byte rows bound
+// the TMA unit near 3.9 TB/s of loads per chip) 0.184 ms; 8-stage boxes with r / y rows that
+// straddle two lines (origin at stage 0) 0.175 ms, whole lines 0.154 ms; with the r ring one
+// box deeper than the x ring (r is refilled only after its y store has left) 0.129 ms; one
+// CTA per SM with deeper rings 0.158-0.170 ms (four warps do not hide the arithmetic).  The
+// same traffic with the arithmetic removed takes 0.126 ms: what is left is DRAM traffic (the
+// halo rows of neighbouring tiles are read at different times and miss L2).
+namespace rs {
+constexpr int TI = 16, TJ = 8;                   // tile
+constexpr int CH = 8;                            // stages per chunk
+constexpr int ROWB = CH * 16;                    // 128-byte rows
+constexpr int QI = TI + 2, QJ = TJ + 2;          // x box: tile + 1-node halo
+constexpr int XBYTES = ROWB * QI * QJ;
+constexpr int XBOX = (XBYTES + 1023) / 1024 * 1024;   // slot stride (swizzle alignment)
+constexpr int YBOX = ROWB * TI * TJ;             // r / y box
+constexpr int NX = 2;                            // x boxes in the ring
+constexpr int NR = 3;                            // r / y boxes in the ring
+constexpr int NT = TI * TJ;                      // one thread per tile node
+constexpr int SMEM = 1024 + NX * XBOX + NR * YBOX + (NX + NR) * 8;
+static_assert(YBOX % 1024 == 0, "boxes keep the 1024-byte swizzle alignment");
+}  // namespace rs
+
+struct RsArgs {
+  Geo g;
+  const double* x;
+  const double* r;
+  double* y;
+  const double* xi;    // [N][K][5][2][2]
+  const double* xit;
+  PcgState* st;
+  int ntI, nch;
+  long long total;     // tiles x chunks
+};
+
+__global__ void __launch_bounds__(rs::NT, 2) k_rstep(const __grid_constant__ CUtensorMap xmap,
+                                                     const __grid_constant__ CUtensorMap rmap,
+                                                     const __grid_constant__ CUtensorMap ymap,
+                                                     const RsArgs a) {
+  constexpr int TI = rs::TI, TJ = rs::TJ, CH = rs::CH, ROWB = rs::ROWB, QI = rs::QI;
+  constexpr int XBYTES = rs::XBYTES, XBOX = rs::XBOX, YBOX = rs::YBOX, NX = rs::NX, NR = rs::NR;
+  extern __shared__ unsigned char smem_raw[];
+  const Geo& g = a.g;
+  if (halted(a.st)) return;
+  const unsigned base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const unsigned rbase = base + NX * XBOX;
+  const unsigned xbar = rbase + NR * YBOX, rbar = xbar + NX * 8;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < NX; ++s) mbar_init_u(xbar + 8 * s, 1);
+    for (int s = 0; s < NR; ++s) mbar_init_u(rbar + 8 * s, 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+
+  const int ti = tid % TI, tj = tid / TI;
+  // 128-byte swizzle: 16-byte piece s of box row R sits at R * 128 + ((s ^ (R & 7)) << 4)
+  unsigned pq[5];
+#pragma unroll
+  for (int u = 0; u < 5; ++u) {
+    const unsigned R = (unsigned)((tj + 1 + odj(u)) * QI + (ti + 1 + odi(u)));
+    pq[u] = R * ROWB + ((R & 7u) << 4);
+  }
+  const unsigned yq = (unsigned)tid * ROWB + (((unsigned)tid & 7u) << 4);
+
+  // this CTA's run of the (tile, chunk) sequence
+  const long long lo = a.total * blockIdx.x / gridDim.x, hi = a.total * (blockIdx.x + 1) / gridDim.x;
+  auto origin = [&](long long q, int& i0, int& j0, int& c) {
+    const int tile = (int)(q / a.nch);
+    c = (int)(q - (long long)tile * a.nch);
+    i0 = (tile % a.ntI) * TI;
+    j0 = (tile / a.ntI) * TJ;
+  };
+  // producers (every thread tracks the cursors, thread 0 issues).  The x map starts at stage
+  // 2: its box c holds stages 8c + 2 .. 8c + 9.  A run that starts inside a tile first takes
+  // the box before its first chunk (x_{t-1}, x_t of its first stage).
+  long long px_g = lo, pr_g = lo;
+  bool px_pre = lo < hi && lo % a.nch != 0;
+  unsigned px_q = 0, pr_q = 0;
+  auto produce_x = [&](unsigned limit) {
+    while (px_g < hi && px_q < limit) {
+      int i0, j0, c;
+      origin(px_g, i0, j0, c);
+      if (tid == 0) {
+        const unsigned slot = px_q % NX;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_u(xbar + 8 * slot, XBYTES);
+        tma3(base + slot * XBOX, &xmap, (px_pre ? c - 1 : c) * CH * 2, i0 - 1, j0 - 1,
+             xbar + 8 * slot);
+      }
+      ++px_q;
+      if (px_pre)
+        px_pre = false;
+      else
+        ++px_g;
+    }
+  };
+  auto produce_r = [&](unsigned limit) {
+    while (pr_g < hi && pr_q < limit) {
+      int i0, j0, c;
+      origin(pr_g, i0, j0, c);
+      if (tid == 0) {
+        const unsigned slot = pr_q % NR;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_u(rbar + 8 * slot, YBOX);
+        tma3(rbase + slot * YBOX, &rmap, c * CH * 2, i0, j0, rbar + 8 * slot);
+      }
+      ++pr_q;
+      ++pr_g;
+    }
+  };
+  auto wait_x = [&](unsigned q) { mbar_wait_u(xbar + 8 * (q % NX), (q / NX) & 1u); };
+  auto wait_r = [&](unsigned q) { mbar_wait_u(rbar + 8 * (q % NR), (q / NR) & 1u); };
+  auto xpts = [&](unsigned q, int s, double2* v) {
+    const unsigned xb = base + (q % NX) * XBOX, sx = (unsigned)s << 4;
+#pragma unroll
+    for (int u = 0; u < 5; ++u) v[u] = lds2u((xb + pq[u]) ^ sx);
+  };
+
+  produce_x(NX);
+  produce_r(NR);
+  unsigned xq = 0, rq = 0;   // next x box / r box to consume
+  double Xm[5][4], Xp[5][4];
+  double2 xa[5], xb_[5];     // x_{t-1}, x_t of the 5-point neighbourhood
+#pragma unroll 1
+  for (long long q = lo; q < hi; ++q) {
+    int i0, j0, c;
+    origin(q, i0, j0, c);
+    if (q == lo || c == 0) {   // a new tile: the node's Xi blocks and the stage window
+      const int i = i0 + ti, j = j0 + tj;
+      const bool in = i < g.K && j < g.N;
+      const long long node = (long long)j * g.K + i;
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        zero4(Xm[u]);
+        zero4(Xp[u]);
+        if (in) {
+          ld4(Xm[u], a.xi + (node * 5 + u) * 4);
+          ld4(Xp[u], a.xit + (node * 5 + u) * 4);
+        }
+      }
+      if (c > 0) {
+        wait_x(xq);
+        xpts(xq, CH - 2, xa);
+        xpts(xq, CH - 1, xb_);
+        ++xq;
+        __syncthreads();   // the box may be refilled
+      } else {
+        // stage 0 straight from global memory: x_0 and x_1 open the window, and
+        // y_0 = r_0 - Xi_0' x_1 (no Xi_{-1})
+        double2 ep = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < 5; ++u) {
+          const int ii = i + odi(u), jj = j + odj(u);
+          xa[u] = xb_[u] = make_double2(0.0, 0.0);
+          if (in && ii >= 0 && ii < g.K && jj >= 0 && jj < g.N) {
+            const double2* px =
+                reinterpret_cast<const double2*>(a.x + ((long long)jj * g.K + ii) * g.TS * 2);
+            xa[u] = __ldg(px);
+            xb_[u] = __ldg(px + 1);
+          }
+          ep = mac(ep, Xp[u], xb_[u]);
+        }
+        if (in) {
+          const double2 rv = __ldg(reinterpret_cast<const double2*>(a.r + node * g.TS * 2));
+          *reinterpret_cast<double2*>(a.y + node * g.TS * 2) =
+              make_double2(rv.x + ((0.0 - 0.0) - ep.x), rv.y + ((0.0 - 0.0) - ep.y));
+        }
+      }
+    }
+    // every box before xq is free: the barrier that ended the previous chunk ordered the reads
+    produce_x(xq + NX);
+    wait_x(xq);
+    wait_r(rq);
+    const unsigned rb = rbase + (rq % NR) * YBOX;
+#pragma unroll
+    for (int s = 0; s < CH; ++s) {
+      double2 xc[5];
+      xpts(xq, s, xc);
+      const unsigned ra = (rb + yq) ^ ((unsigned)s << 4);
+      const double2 rv = lds2u(ra);
+      double2 em = make_double2(0.0, 0.0), ep = em;
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        em = mac(em, Xm[u], xa[u]);
+        ep = mac(ep, Xp[u], xc[u]);
+      }
+      // y = r + (-(Xi_{t-1} x_{t-1}) - Xi_t' x_{t+1})   (the convention of gq_grid.cu)
+      sts2u(ra, make_double2(rv.x + ((0.0 - em.x) - ep.x), rv.y + ((0.0 - em.y) - ep.y)));
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        xa[u] = xb_[u];
+        xb_[u] = xc[u];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tma3_store(&ymap, rb, c * CH * 2, i0, j0);
+      bulk_commit();
+      bulk_wait_read<1>();   // the box stored one chunk ago (refilled next) has been read out
+    }
+    produce_r(rq + NR);
+    ++rq;
+    ++xq;
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -498,17 +724,35 @@ bool dstep_preferred(const Geo& g, int sm_count) {
 long long dstep_max_blocks(int sm_count) { return sm_count; }
 
 // vector v[j][i][t][k] as a 3-D tensor (2*T1 doubles, K rows, N columns); box = one chunk of
-// the tile with its 2-node halo (inputs, out = false) or of the tile itself (out = true)
-bool dstep_make_map(const Geo& g, const double* base, bool out, CUtensorMap* m) {
+// the tile with a halo of 2 nodes (Delta input) or none (its output)
+bool dstep_make_map(const Geo& g, const double* base, int halo, CUtensorMap* m) {
   EncodeTiled enc = encoder();
   if (!enc || base == nullptr) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)g.T1 * 2, (cuuint64_t)g.K, (cuuint64_t)g.N};
   const cuuint64_t strides[2] = {(cuuint64_t)g.TS * 16, (cuuint64_t)g.TS * 16 * g.K};
-  const cuuint32_t box[3] = {(cuuint32_t)(CH * 2), (cuuint32_t)(out ? TI : PI),
-                             (cuuint32_t)(out ? TJ : PJ)};
+  const cuuint32_t box[3] = {(cuuint32_t)(CH * 2), (cuuint32_t)(TI + 2 * halo),
+                             (cuuint32_t)(TJ + 2 * halo)};
   const cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// views for k_rstep: 8-stage boxes with the 128-byte swizzle, origin at stage 1 (whole lines
+// of the padded layout); the x view (input = true) starts at stage 2 and carries a one-node halo
+bool rstep_make_map(const Geo& g, const double* base, bool input, CUtensorMap* m) {
+  EncodeTiled enc = encoder();
+  if (!enc || base == nullptr) return false;
+  const int stages = input ? g.T - 1 : g.T;   // from stage 2 (x) / stage 1 (r, y) on
+  if (stages < 1) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)stages * 2, (cuuint64_t)g.K, (cuuint64_t)g.N};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.TS * 16, (cuuint64_t)g.TS * 16 * g.K};
+  const cuuint32_t box[3] = {(cuuint32_t)(rs::CH * 2), (cuuint32_t)(input ? rs::QI : rs::TI),
+                             (cuuint32_t)(input ? rs::QJ : rs::TJ)};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base + (input ? 4 : 2)),
+             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
@@ -555,6 +799,33 @@ cudaError_t launch_dstep(const Geo& g, const CUtensorMap& dmap, const CUtensorMa
   a.n_items = (int)(tiles * a.nr);
   const int blocks = (int)std::min<long long>(a.n_items, slots);
   k_dstep<<<blocks, NTHR, smem, s>>>(dmap, ymap, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rstep(const Geo& g, const CUtensorMap& xmap, const CUtensorMap& rmap,
+                         const CUtensorMap& ymap, const double* x, const double* r,
+                         double* y, const double* xi, const double* xit, PcgState* st,
+                         int sm_count, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_rstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         rs::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  RsArgs a;
+  a.g = g;
+  a.x = x;
+  a.r = r;
+  a.y = y;
+  a.xi = xi;
+  a.xit = xit;
+  a.st = st;
+  a.ntI = (g.K + rs::TI - 1) / rs::TI;
+  a.nch = (g.T + rs::CH - 1) / rs::CH;   // chunk c = stages 8c + 1 .. 8c + 8
+  a.total = (long long)a.ntI * ((g.N + rs::TJ - 1) / rs::TJ) * a.nch;
+  const int blocks = (int)std::min<long long>(a.total, 2LL * sm_count);
+  k_rstep<<<blocks, rs::NT, rs::SMEM, s>>>(xmap, rmap, ymap, a);
   return cudaGetLastError();
 }
 

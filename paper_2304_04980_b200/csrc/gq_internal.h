@@ -160,13 +160,21 @@ struct DstepOps {
 bool dstep_supported(const Geo& g);
 bool dstep_preferred(const Geo& g, int sm_count);   // large enough grid (or GQ_DSTEP=1)
 long long dstep_max_blocks(int sm_count);
-// TMA view of a stage-inner vector: input boxes (tile + halo) or output boxes (tile)
-bool dstep_make_map(const Geo& g, const double* base, bool out, CUtensorMap* m);
+// TMA view of a stage-inner vector: 4-stage boxes of a tile with a halo of `halo` nodes (2:
+// the Delta input, 0: its output)
+bool dstep_make_map(const Geo& g, const double* base, int halo, CUtensorMap* m);
 // y = Delta x for the vector behind `dmap` into the vector behind `ymap` (+ y.x curvature,
 // alpha, breakdown when dotmode != kDotNone); stage-slab halo rows are written as zeros
 cudaError_t launch_dstep(const Geo& g, const CUtensorMap& dmap, const CUtensorMap& ymap,
                          const DstepOps& op, double* y, double* partials, PcgState* st,
                          int dotmode, int sm_count, cudaStream_t s);
+// y = r - (Xi_{t-1} x_{t-1} + Xi_t' x_{t+1}) by TMA tiles (n = 2, one Xi class): views of x
+// (input = true: one-node halo) and of r / y; needs T >= 2
+bool rstep_make_map(const Geo& g, const double* base, bool input, CUtensorMap* m);
+cudaError_t launch_rstep(const Geo& g, const CUtensorMap& xmap, const CUtensorMap& rmap,
+                         const CUtensorMap& ymap, const double* x, const double* r,
+                         double* y, const double* xi, const double* xit, PcgState* st,
+                         int sm_count, cudaStream_t s);
 
 // ---- lean n = 2 grid stencils (gq_grid.cu) ----
 struct GridShape {

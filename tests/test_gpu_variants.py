@@ -17,7 +17,8 @@ VARIANTS = {
     "no_chain": {"GQ_NO_CHAIN": "1"},            # FMA / v6 sweeps instead of the chain kernel
     "no_grid": {"GQ_NO_GRID": "1"},              # v2 stencils instead of the n=2 grid kernel
     "chainm": {"GQ_CHAINM": "2"},                # twelve-warp chain sweeps (every form) on the n=2 cases
-    "dstep": {"GQ_DSTEP": "1"},                  # t-loop Delta on every (small) golden case
+    "dstep": {"GQ_DSTEP": "1"},                  # t-loop Delta + tiled outer rhs on every (small) golden case
+    "dstep_no_rstep": {"GQ_DSTEP": "1", "GQ_NO_RSTEP": "1"},   # ... with the lane-per-stage outer rhs
     "fuse_x": {"GQ_FUSE_X": "1"},                # x update fused into the direction update
     "no_fuse_x": {"GQ_FUSE_X": "0"},             # ... and on its own graph branch for small sizes
     "no_fuse_r": {"GQ_NO_FUSE_R": "1"},          # separate r update kernel

@@ -21,7 +21,7 @@ __device__ __forceinline__ bool tryw(unsigned b, unsigned p) {
 }
 
 __global__ void stream(const __grid_constant__ CUtensorMap m, int nb0, int nbR, int nbC, int b0,
-                       int bR, int bC, int ns, unsigned box_bytes, double* sink) {
+                       int bR, int bC, int ns, unsigned box_bytes, double* sink, int runs) {
   extern __shared__ unsigned char raw[];
   const unsigned base = (su(raw) + 1023u) & ~1023u;
   const unsigned slot_bytes = (box_bytes + 1023u) & ~1023u;
@@ -33,9 +33,12 @@ __global__ void stream(const __grid_constant__ CUtensorMap m, int nb0, int nbR, 
   const long long total = (long long)nb0 * nbR * nbC;
   // my boxes: b = blockIdx.x + k * gridDim.x
   long long nmine = total > blockIdx.x ? (total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // runs = 1: every CTA walks one contiguous run of the box sequence (stage axis fastest)
+  const long long lo = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
+  if (runs) nmine = hi - lo;
   auto issue = [&](long long k) {
     if (threadIdx.x == 0 && k < nmine) {
-      const long long b = blockIdx.x + k * gridDim.x;
+      const long long b = runs ? lo + k : blockIdx.x + k * gridDim.x;
       const int c0 = (int)(b % nb0), r = (int)((b / nb0) % nbR), c = (int)(b / nb0 / nbR);
       const unsigned s = (unsigned)(k % ns);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -62,7 +65,7 @@ typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, co
                         CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 int main() {
-  const int D0 = 402, R = 256, C = 256;   // the headline vector: 2 T1 doubles x K x N
+  const int D0 = 416, R = 256, C = 1024;   // 4 x   // the headline vector: 2 T1 doubles x K x N
   double* x;
   cudaMalloc(&x, (size_t)D0 * R * C * 8);
   cudaMemset(x, 0, (size_t)D0 * R * C * 8);
@@ -75,15 +78,15 @@ int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  struct Shape { int b0, bR, bC, ns, per_sm, thr; };
+  struct Shape { int b0, bR, bC, ns, per_sm, thr, runs; };
   const Shape shapes[] = {
-      {8, 36, 12, 3, 1, 352},  {8, 34, 10, 3, 1, 256},  {8, 32, 8, 3, 1, 256},
-      {8, 36, 12, 6, 1, 352},  {8, 32, 8, 6, 1, 256},   {8, 32, 8, 12, 1, 256},
-      {8, 32, 8, 4, 2, 256},   {8, 32, 8, 6, 2, 128},
-      {16, 32, 8, 3, 1, 256},  {16, 32, 8, 6, 1, 256},  {16, 34, 10, 3, 1, 256},
-      {32, 32, 4, 3, 1, 256},  {32, 32, 4, 6, 1, 256},  {32, 32, 8, 3, 1, 256},
-      {2, 32, 8, 6, 1, 256},   {4, 32, 8, 6, 1, 256},
+      {8, 16, 8, 6, 2, 128, 1},  {16, 16, 8, 3, 2, 128, 1}, {16, 16, 8, 6, 2, 128, 1},
+      {32, 16, 8, 3, 2, 128, 1}, {32, 16, 4, 6, 2, 128, 1}, {16, 16, 8, 3, 2, 128, 0},
+      {32, 16, 8, 3, 2, 128, 0}, {16, 18, 10, 3, 2, 128, 1}, {16, 18, 10, 4, 2, 128, 1},
+      {32, 18, 10, 2, 2, 128, 1},
   };
+
+
   for (const Shape& s : shapes) {
     CUtensorMap m;
     const cuuint64_t dims[3] = {(cuuint64_t)D0, (cuuint64_t)R, (cuuint64_t)C};
@@ -108,7 +111,7 @@ int main() {
     float best = 1e30f;
     for (int it = 0; it < 4; ++it) {
       cudaEventRecord(e0);
-      stream<<<grid, s.thr, smem>>>(m, nb0, nbR, nbC, s.b0, s.bR, s.bC, s.ns, bytes, sink);
+      stream<<<grid, s.thr, smem>>>(m, nb0, nbR, nbC, s.b0, s.bR, s.bC, s.ns, bytes, sink, s.runs);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -117,8 +120,8 @@ int main() {
     }
     cudaError_t err = cudaGetLastError();
     const double moved = (double)nb0 * nbR * nbC * bytes;
-    printf("box {%2d dbl = %3d B rows, %2d x %2d} ns %2d per_sm %d thr %3d smem %6zu: %7.1f GB/s (%.3f ms) %s\n",
-           s.b0, s.b0 * 8, s.bR, s.bC, s.ns, s.per_sm, s.thr, smem, moved / best / 1e6, best,
+    printf("%s box {%2d dbl = %3d B rows, %2d x %2d} ns %2d per_sm %d thr %3d smem %6zu: %7.1f GB/s (%.3f ms) %s\n",
+           s.runs ? "runs" : "intl", s.b0, s.b0 * 8, s.bR, s.bC, s.ns, s.per_sm, s.thr, smem, moved / best / 1e6, best,
            err == cudaSuccess ? "" : cudaGetErrorString(err));
   }
   return 0;
