@@ -473,8 +473,8 @@ __global__ void __launch_bounds__(NTHR, MINB) k_dstep(const __grid_constant__ CU
 // holds x_{t+1} for all of its stages -- and one r box of the tile; y is formed in the r box
 // and leaves by TMA from there.  The five points of x_{t+1} read at stage t stay in registers
 // and serve as x_{t-1} two stages later: 5 + 1 shared loads, 1 store and 40 DFMA per
-// node-stage, one __syncthreads per chunk.  The (tile, chunk) sequence is cut into equal
-// contiguous runs, one per CTA; both rings run through tile boundaries.
+// node-stage, one __syncthreads per chunk.  Items are whole tiles (pieces of a tile's chunks on
+// small grids), dealt round-robin; both rings run through item boundaries.
 //
 // Measured on the way (headline, one launch): 4-stage boxes as in k_dstep (64-byte rows bound
 // the TMA unit near 3.9 TB/s of loads per chip) 0.184 ms; 8-stage boxes with r / y rows that
@@ -506,8 +506,8 @@ struct RsArgs {
   const double* xi;    // [N][K][5][2][2]
   const double* xit;
   PcgState* st;
-  int ntI, nch;
-  long long total;     // tiles x chunks
+  int ntI, nch, tiles, pieces;
+  long long total;     // items = tiles x pieces
 };
 
 __global__ void __launch_bounds__(rs::NT, 2) k_rstep(const __grid_constant__ CUtensorMap xmap,
@@ -540,50 +540,63 @@ __global__ void __launch_bounds__(rs::NT, 2) k_rstep(const __grid_constant__ CUt
   }
   const unsigned yq = (unsigned)tid * ROWB + (((unsigned)tid & 7u) << 4);
 
-  // this CTA's run of the (tile, chunk) sequence
-  const long long lo = a.total * blockIdx.x / gridDim.x, hi = a.total * (blockIdx.x + 1) / gridDim.x;
-  auto origin = [&](long long q, int& i0, int& j0, int& c) {
-    const int tile = (int)(q / a.nch);
-    c = (int)(q - (long long)tile * a.nch);
-    i0 = (tile % a.ntI) * TI;
-    j0 = (tile / a.ntI) * TJ;
+  // Items are (tile, piece of its chunks); item k of this CTA is blockIdx.x + k * gridDim.x,
+  // tiles fastest, so that at any time the CTAs work on neighbouring tiles at about the same
+  // chunk (the halo rows of a box are then still in L2 from the neighbour's own read).
+  struct Cur {
+    int k, c, cs, ce, i0, j0;
+    bool valid;
+  };
+  auto start = [&](Cur& u, int k) {
+    const long long item = blockIdx.x + (long long)k * gridDim.x;
+    u.k = k;
+    u.valid = item < a.total;
+    if (!u.valid) return;
+    const int piece = (int)(item / a.tiles), tile = (int)(item - (long long)piece * a.tiles);
+    u.cs = u.c = piece * a.nch / a.pieces;
+    u.ce = (piece + 1) * a.nch / a.pieces;
+    u.i0 = (tile % a.ntI) * TI;
+    u.j0 = (tile / a.ntI) * TJ;
+  };
+  auto step = [&](Cur& u) {
+    if (++u.c == u.ce) start(u, u.k + 1);
   };
   // producers (every thread tracks the cursors, thread 0 issues).  The x map starts at stage
-  // 2: its box c holds stages 8c + 2 .. 8c + 9.  A run that starts inside a tile first takes
+  // 2: its box c holds stages 8c + 2 .. 8c + 9.  An item that starts inside a tile first takes
   // the box before its first chunk (x_{t-1}, x_t of its first stage).
-  long long px_g = lo, pr_g = lo;
-  bool px_pre = lo < hi && lo % a.nch != 0;
+  Cur px, pr, cu;
+  start(px, 0);
+  pr = cu = px;
+  bool px_pre = px.valid && px.c > 0;
   unsigned px_q = 0, pr_q = 0;
   auto produce_x = [&](unsigned limit) {
-    while (px_g < hi && px_q < limit) {
-      int i0, j0, c;
-      origin(px_g, i0, j0, c);
+    while (px.valid && px_q < limit) {
       if (tid == 0) {
         const unsigned slot = px_q % NX;
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_expect_u(xbar + 8 * slot, XBYTES);
-        tma3(base + slot * XBOX, &xmap, (px_pre ? c - 1 : c) * CH * 2, i0 - 1, j0 - 1,
-             xbar + 8 * slot);
+        tma3(base + slot * XBOX, &xmap, (px_pre ? px.c - 1 : px.c) * CH * 2, px.i0 - 1,
+             px.j0 - 1, xbar + 8 * slot);
       }
       ++px_q;
-      if (px_pre)
+      if (px_pre) {
         px_pre = false;
-      else
-        ++px_g;
+      } else {
+        step(px);
+        px_pre = px.valid && px.c == px.cs && px.c > 0;
+      }
     }
   };
   auto produce_r = [&](unsigned limit) {
-    while (pr_g < hi && pr_q < limit) {
-      int i0, j0, c;
-      origin(pr_g, i0, j0, c);
+    while (pr.valid && pr_q < limit) {
       if (tid == 0) {
         const unsigned slot = pr_q % NR;
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_expect_u(rbar + 8 * slot, YBOX);
-        tma3(rbase + slot * YBOX, &rmap, c * CH * 2, i0, j0, rbar + 8 * slot);
+        tma3(rbase + slot * YBOX, &rmap, pr.c * CH * 2, pr.i0, pr.j0, rbar + 8 * slot);
       }
       ++pr_q;
-      ++pr_g;
+      step(pr);
     }
   };
   auto wait_x = [&](unsigned q) { mbar_wait_u(xbar + 8 * (q % NX), (q / NX) & 1u); };
@@ -600,10 +613,9 @@ __global__ void __launch_bounds__(rs::NT, 2) k_rstep(const __grid_constant__ CUt
   double Xm[5][4], Xp[5][4];
   double2 xa[5], xb_[5];     // x_{t-1}, x_t of the 5-point neighbourhood
 #pragma unroll 1
-  for (long long q = lo; q < hi; ++q) {
-    int i0, j0, c;
-    origin(q, i0, j0, c);
-    if (q == lo || c == 0) {   // a new tile: the node's Xi blocks and the stage window
+  for (; cu.valid; step(cu)) {
+    const int i0 = cu.i0, j0 = cu.j0, c = cu.c;
+    if (c == cu.cs) {   // a new item: the node's Xi blocks and the stage window
       const int i = i0 + ti, j = j0 + tj;
       const bool in = i < g.K && j < g.N;
       const long long node = (long long)j * g.K + i;
@@ -823,8 +835,17 @@ cudaError_t launch_rstep(const Geo& g, const CUtensorMap& xmap, const CUtensorMa
   a.st = st;
   a.ntI = (g.K + rs::TI - 1) / rs::TI;
   a.nch = (g.T + rs::CH - 1) / rs::CH;   // chunk c = stages 8c + 1 .. 8c + 8
-  a.total = (long long)a.ntI * ((g.N + rs::TJ - 1) / rs::TJ) * a.nch;
-  const int blocks = (int)std::min<long long>(a.total, 2LL * sm_count);
+  a.tiles = a.ntI * ((g.N + rs::TJ - 1) / rs::TJ);
+  const long long slots = 2LL * sm_count;
+  // One piece per tile once the tiles fill the machine: the kernel is bound by DRAM traffic,
+  // and CTAs that walk neighbouring tiles in step find each other's halo rows in L2 (headline:
+  // 462 MB read and 0.118 ms with one piece, 580 MB and 0.141 ms with four, 584 MB and
+  // 0.134 ms with equal contiguous runs of the (tile, chunk) sequence).  Small grids are cut
+  // into pieces to give every CTA slot an item.
+  a.pieces = a.tiles >= slots ? 1 : (int)std::max<long long>(1, std::min<long long>(a.nch, slots / a.tiles));
+  if (const char* e = getenv("GQ_RS_PIECES")) a.pieces = std::max(1, std::min(a.nch, atoi(e)));
+  a.total = (long long)a.tiles * a.pieces;
+  const int blocks = (int)std::min<long long>(a.total, slots);
   k_rstep<<<blocks, rs::NT, rs::SMEM, s>>>(xmap, rmap, ymap, a);
   return cudaGetLastError();
 }
