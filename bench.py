@@ -126,7 +126,7 @@ def kernel_family(name):
         return ("pair-chain outer sweep + r update (k_chainm / k_chain)" if name.endswith("_r")
                 else "pair-chain outer sweep (k_chain)")
     if name.startswith("outer_rhs"):
-        return "outer rhs (k_grid)"
+        return "outer rhs (k_rstep / k_grid)"
     if name == "delta":
         return "delta (k_dstep / k_grid)"
     return name

@@ -3,6 +3,6 @@
 OUT=${1:-step}
 export STEPS=3
 python tools/stepprof.py > gpurun_out/sp.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"^(k_dstep|k_update_x|k_chain|k_chainm|k_grid|k_dirupdate)$" \
+ncu --set full --clock-control none --import-source on -k regex:"^(k_dstep|k_rstep|k_update_x|k_chain|k_chainm|k_grid|k_dirupdate)$" \
     --launch-skip 13 -c 8 -o gpurun_out/$OUT python tools/stepprof.py > gpurun_out/ncu_$OUT.log 2>&1
 tail -3 gpurun_out/ncu_$OUT.log

@@ -28,7 +28,7 @@ def step_name(fn, seen):
         return "update_x"
     if "k_dirupdate" in fn:
         return "dirupdate"
-    if "k_grid<3" in fn:
+    if "k_grid<3" in fn or "k_rstep" in fn:
         return "outer_rhs_s1"
     if "k_chainm<" in fn:   # k_chainm<NS, INNER, P, W, FR, DOT>
         targs = [x.strip() for x in fn.split("k_chainm<")[1].split(">")[0].split(",")]
