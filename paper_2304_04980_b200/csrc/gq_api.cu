@@ -411,6 +411,16 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
       CKB(cudaStreamSynchronize(c->stream));
       c->co = ChainOps{c->cff, c->cfb, c->seg, (int)s8.size(), c->seg + s8.size(),
                        (int)s16.size()};
+      {
+        // classes without coupling tiles (stage 0: Psi_0 = Q_0^-1) read only L^-1 and L^-T
+        int* flags = nullptr;
+        CKB(dalloc(&flags, (size_t)c->npc));
+        cudaError_t me = launch_chainm_mark(g, c->npc, c->co, c->seg, (int)s8.size(), flags,
+                                            c->stream);
+        if (me == cudaSuccess) me = cudaStreamSynchronize(c->stream);
+        cudaFree(flags);
+        CKB(me);
+      }
       c->chain = true;
       c->st8 = st8_supported(g, c->nxc);   // n = 4: DMMA block stencils (two nodes per warp)
     }

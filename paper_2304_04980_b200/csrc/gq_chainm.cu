@@ -51,6 +51,11 @@ __device__ __forceinline__ void stg2_out(double* p, double2 v) {
 __device__ __forceinline__ void ldgsts_f(unsigned dst, const double* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
 }
+// ... of `sz` (16 or 0) bytes: size 0 zero-fills the destination without touching memory
+__device__ __forceinline__ void ldgsts_fz(unsigned dst, const double* src, unsigned sz) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(sz)
+               : "memory");
+}
 // vector data read once (prologue fragments): bypass L1
 __device__ __forceinline__ double2 ldcg2(const double* p) {
   return __ldcg(reinterpret_cast<const double2*>(p));
@@ -87,8 +92,8 @@ __device__ __forceinline__ void chainm_item(const Geo& g, const ChainOps& co,
                                             const double* __restrict__ rhs,
                                             const double* __restrict__ th, double* out,
                                             const double* __restrict__ rdot, double* ring, int v,
-                                            int t0, int nvalid, int cls, uint64_t pol_k,
-                                            double& dot, const double* __restrict__ yv,
+                                            int t0, int nvalid, int cls, bool diag,
+                                            uint64_t pol_k, double& dot, const double* __restrict__ yv,
                                             double* rupd, double alpha, double& rmax) {
   using C = Cm<NS, INNER, FR, DOT>;
   constexpr int QQ = C::QQ, NT = C::NT, KT = C::KT, KC = C::KC, REC = C::RSTR, R = P + 1;
@@ -132,6 +137,9 @@ __device__ __forceinline__ void chainm_item(const Geo& g, const ChainOps& co,
   const unsigned facf_dst = lane_opaque(ring_u + (unsigned)(C::NRF * REC * 8 + 16 * lane));
   const unsigned facb_dst = lane_opaque(ring_u + (unsigned)(C::NRB * REC * 8 + 16 * lane));
   const double* ffb = co.ff + ((long long)cls * g.V + v) * nb * C::FFS + 2 * lane;
+  // a class whose coupling tiles (G, L^-1 Omega~, H) are all zero -- stage 0, where Psi_0 =
+  // Q_0^-1 is block diagonal -- stages only L^-1 and L^-T; the other tiles are zero-filled
+  const unsigned offsz = diag ? 0u : 16u;
 
   // last block (and the prologue): rows outside [0, K) zero-fill
   auto issue_f_chk = [&](int k, int slot) {
@@ -142,8 +150,9 @@ __device__ __forceinline__ void chainm_item(const Geo& g, const ChainOps& co,
       ldgsts(rec_dst + sb + j * C::RPI * REC * 8, ok ? fsrc[j] + k * rs2 : rhs, ok ? 16 : 0, 0);
     }
     const double* fp = ffb + (long long)k * C::FFS;
+    ldgsts_f(facf_dst + sb, fp);
 #pragma unroll
-    for (int i = 0; i < C::CFF; ++i) ldgsts_f(facf_dst + sb + 512 * i, fp + 64 * i);
+    for (int i = 1; i < C::CFF; ++i) ldgsts_fz(facf_dst + sb + 512 * i, fp + 64 * i, offsz);
   };
 
   double2 wd[NT];
@@ -203,8 +212,9 @@ __device__ __forceinline__ void chainm_item(const Geo& g, const ChainOps& co,
 #pragma unroll
         for (int j = 0; j < C::JF; ++j)
           ldgsts(rec_dst + sb + j * C::RPI * REC * 8, fcur[j], fsz[j], 0);
+        ldgsts_f(facf_dst + sb, fpc);
 #pragma unroll
-        for (int i = 0; i < C::CFF; ++i) ldgsts_f(facf_dst + sb + 512 * i, fpc + 64 * i);
+        for (int i = 1; i < C::CFF; ++i) ldgsts_fz(facf_dst + sb + 512 * i, fpc + 64 * i, offsz);
       }
     }
     commit();
@@ -320,8 +330,9 @@ __device__ __forceinline__ void chainm_item(const Geo& g, const ChainOps& co,
       ldgsts(rec_dst + sb + j * C::RPI * REC * 8, ok ? bsrc[j] + k * rs2 : rhs, ok ? 16 : 0, 0);
     }
     const double* fp = fbb + (long long)k * C::FB;
+    ldgsts_f(facb_dst + sb, fp);
 #pragma unroll
-    for (int i = 0; i < C::CFB; ++i) ldgsts_f(facb_dst + sb + 512 * i, fp + 64 * i);
+    for (int i = 1; i < C::CFB; ++i) ldgsts_fz(facb_dst + sb + 512 * i, fp + 64 * i, offsz);
   };
   {
     const int pro = P < nb ? P : nb;
@@ -352,8 +363,9 @@ __device__ __forceinline__ void chainm_item(const Geo& g, const ChainOps& co,
 #pragma unroll
       for (int j = 0; j < C::JB; ++j)
         ldgsts(rec_dst + sb + j * C::RPI * REC * 8, bcur[j], bsz[j], 0);
+      ldgsts_f(facb_dst + sb, fbc);
 #pragma unroll
-      for (int i = 0; i < C::CFB; ++i) ldgsts_f(facb_dst + sb + 512 * i, fbc + 64 * i);
+      for (int i = 1; i < C::CFB; ++i) ldgsts_fz(facb_dst + sb + 512 * i, fbc + 64 * i, offsz);
     }
     commit();
 #pragma unroll
@@ -470,7 +482,7 @@ __global__ void __launch_bounds__(32 * W, 1)
     const int v = u / nseg;
     const int4 sg = co.seg[u - v * nseg];
     chainm_item<NS, INNER, P, FR, DOT>(g, co, rhs, th, out, rdot, ring, v, sg.x, sg.y, sg.z,
-                                       pol_k, dot, yv, rupd, alpha, rmax);
+                                       sg.w != 0, pol_k, dot, yv, rupd, alpha, rmax);
   }
   if constexpr (FR) {
     // max |r| over the grid, then the reference's history / convergence step (pcg.py:113-121)
@@ -496,6 +508,26 @@ __global__ void __launch_bounds__(32 * W, 1)
       }
     }
   }
+}
+
+// flags[cls] = 1 if any coupling tile of the class (forward: everything after L^-1, backward:
+// everything after L^-T) has a nonzero entry
+__global__ void k_tiles_nonzero(long long blocks_per_cls, int npc, const double* __restrict__ ff,
+                                const double* __restrict__ fb, int* flags) {
+  using C = Cm<2, true, false, false>;
+  const long long total = (long long)npc * blocks_per_cls;
+  for (long long b = blockIdx.x; b < total; b += gridDim.x) {
+    const double* f = ff + b * C::FFS;
+    const double* h = fb + b * C::FB;
+    bool nz = false;
+    for (int e = C::QQ + threadIdx.x; e < C::FFS; e += blockDim.x) nz = nz || f[e] != 0.0;
+    for (int e = C::QQ + threadIdx.x; e < C::FB; e += blockDim.x) nz = nz || h[e] != 0.0;
+    if (nz) flags[b / blocks_per_cls] = 1;
+  }
+}
+__global__ void k_seg_mark(int4* seg, int nseg, const int* __restrict__ flags) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nseg) seg[i].w = flags[seg[i].z] ? 0 : 1;
 }
 
 int env_or(const char* name, int dflt) {
@@ -537,6 +569,18 @@ bool chainm_supported(const Geo& g, int sm_count) {
 }
 
 bool chainm_all() { return env_or("GQ_CHAINM", 0) == 2; }
+
+cudaError_t launch_chainm_mark(const Geo& g, int npc, const ChainOps& co, int4* seg, int nseg,
+                               int* flags, cudaStream_t s) {
+  if (g.n != 2 || env_or("GQ_NO_ZTILES", 0)) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)npc * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  const long long per = (long long)g.V * g.nb;
+  k_tiles_nonzero<<<(unsigned)std::min<long long>(npc * per, 4096), 128, 0, s>>>(per, npc, co.ff,
+                                                                               co.fb, flags);
+  k_seg_mark<<<(nseg + 127) / 128, 128, 0, s>>>(seg, nseg, flags);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_chainm(const Geo& g, const ChainOps& co, bool inner, const double* rhs,
                           const double* th, double* out, const double* rdot, int sm_count,

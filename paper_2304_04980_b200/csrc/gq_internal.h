@@ -115,6 +115,11 @@ struct ChainOps {
   const int4* grp = nullptr;       // CTA items (n = 8: all classes; n = 2: class-1 runs)
   int ngrp = 0;
 };
+// seg[i].w = 1 for the segments of classes whose coupling tiles (G, L^-1 Omega~, H) are all
+// zero (n = 2; flags: npc ints of scratch); k_chainm zero-fills those tiles instead of reading
+// them (gq_chainm.cu)
+cudaError_t launch_chainm_mark(const Geo& g, int npc, const ChainOps& co, int4* seg, int nseg,
+                               int* flags, cudaStream_t s);
 
 // n = 8 pair-chain sweeps with CTA-shared factor tiles (gq_chain8c.cu)
 bool chain8c_enabled();
