@@ -227,12 +227,11 @@ extern "C" int gq_create(const gq_problem_desc* desc, int32_t inner_sweeps,
   g.nk = (long long)D.K * D.N;
   g.dim = g.nk * D.n * g.T1;
   {
-    // x += alpha d: at the headline its own graph branch overlaps the sweeps and beats the
-    // fused direction update by ~1% (tools/steptime.py); when the vectors fit in L2 the step
-    // is launch- and latency-bound and one kernel less wins (configs 1-3: +3-4%).
-    // GQ_FUSE_X=0/1 overrides.
+    // x += alpha d rides in the direction update (one pass over d less; the five-stream
+    // kernel runs at 6.4 TB/s): headline 710 against 693 steps/s with the x update on its own
+    // graph branch, configs 1-3 +3-4% for one kernel less.  GQ_FUSE_X=0 brings the branch back.
     const char* e = getenv("GQ_FUSE_X");
-    c->fuse_x = (e && *e) ? *e == '1' : g.dim * 8 <= (32LL << 20);
+    c->fuse_x = (e && *e) ? *e == '1' : true;
   }
   int dev = 0;
   cudaGetDevice(&dev);

@@ -4,6 +4,7 @@
 // explicitly rounded multiply and add (no FMA contraction) so that, given identical
 // inputs, they reproduce numpy's `x += alpha*d`, `r - alpha*y`, `q + beta*d` bit for bit.
 // Reductions are grid-wide with a fixed partial order (bitwise reproducible run to run).
+#include <algorithm>
 #include "gq_internal.h"
 
 namespace gq {
@@ -200,30 +201,20 @@ __global__ void __launch_bounds__(256) k_dirupdate_x(long long dim, double* __re
   const long long n2 = dim >> 1;
   const long long nth = (long long)gridDim.x * blockDim.x;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  for (long long b = tid; b < n2; b += nth * kVU) {
-    double2 dv[kVU], qv[kVU], xv[kVU];
-#pragma unroll
-    for (int u = 0; u < kVU; ++u) {
-      const long long e = 2 * (b + u * nth);
-      if (b + u * nth < n2) {
-        dv[u] = *reinterpret_cast<const double2*>(d + e);
-        xv[u] = ld_stream(x + e);
-        if (dir) qv[u] = ld_stream(q + e);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kVU; ++u) {
-      const long long e = 2 * (b + u * nth);
-      if (b + u * nth < n2) {
-        xv[u].x = __dadd_rn(xv[u].x, __dmul_rn(alpha, dv[u].x));
-        xv[u].y = __dadd_rn(xv[u].y, __dmul_rn(alpha, dv[u].y));
-        __stcs(reinterpret_cast<double2*>(x + e), xv[u]);
-        if (dir) {
-          dv[u].x = __dadd_rn(qv[u].x, __dmul_rn(beta, dv[u].x));
-          dv[u].y = __dadd_rn(qv[u].y, __dmul_rn(beta, dv[u].y));
-          *reinterpret_cast<double2*>(d + e) = dv[u];
-        }
-      }
+  // one 16-byte element per thread and pass over a large grid: five streams (3 reads, 2
+  // writes) at 6.4 TB/s on B200; four elements per thread a grid apart ran at 5.1 TB/s
+  for (long long b = tid; b < n2; b += nth) {
+    const long long e = 2 * b;
+    double2 dv = *reinterpret_cast<const double2*>(d + e);
+    double2 xv = ld_stream(x + e);
+    xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, dv.x));
+    xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, dv.y));
+    __stcs(reinterpret_cast<double2*>(x + e), xv);
+    if (dir) {
+      const double2 qv = ld_stream(q + e);
+      dv.x = __dadd_rn(qv.x, __dmul_rn(beta, dv.x));
+      dv.y = __dadd_rn(qv.y, __dmul_rn(beta, dv.y));
+      *reinterpret_cast<double2*>(d + e) = dv;
     }
   }
   if ((dim & 1) && tid == 0) {
@@ -332,7 +323,10 @@ cudaError_t launch_dirupdate(const Geo& g, double* d, const double* q, int block
 cudaError_t launch_dirupdate_x(const Geo& g, double* d, const double* q, double* x, int blocks,
                                PcgState* st, cudaStream_t s) {
   const long long fp = (long long)g.T0 * g.n;
-  k_dirupdate_x<<<blocks, 256, 0, s>>>(g.span + fp, d - fp, q - fp, x - fp, st);
+  const long long n2 = (g.span + fp) >> 1;
+  // `blocks` is the streaming kernels' 8 per SM: up to 64 per SM here, one pass for small sizes
+  const long long want = std::max<long long>(1, std::min<long long>((n2 + 255) / 256, 8LL * blocks));
+  k_dirupdate_x<<<(unsigned)want, 256, 0, s>>>(g.span + fp, d - fp, q - fp, x - fp, st);
   return cudaGetLastError();
 }
 
