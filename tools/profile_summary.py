@@ -26,6 +26,8 @@ def step_name(fn, seen):
         return "delta"
     if "k_update_x" in fn:
         return "update_x"
+    if "k_dirupdate_x" in fn:
+        return "dirupdate_x"
     if "k_dirupdate" in fn:
         return "dirupdate"
     if "k_grid<3" in fn or "k_rstep" in fn:
