@@ -168,6 +168,14 @@ int gq_build_offset(int32_t K, int32_t N, int32_t T, int32_t n, int32_t ncls,
  * while the device iterates, so the device-to-host copy does not wait for the page faults. */
 void gq_touch_pages(void* p, int64_t bytes);
 
+/* Page-locked host memory for result arrays (same place in the API: the array pcg_solve
+ * returns, pcg.py:83).  The device-to-host copy of a result lands in it directly at PCIe speed
+ * instead of through the staging vector and a host copy; the Python side keeps freed buffers
+ * in a small pool, because page-locking 211 MB takes longer than a 100-step solve.
+ * gq_host_alloc returns NULL when the allocation fails (callers fall back to pageable memory). */
+void* gq_host_alloc(int64_t bytes);
+void gq_host_free(void* p);
+
 /* Measurement helpers (bench.py): run `steps` PCG steps as individual launches with CUDA
  * events around every kernel; per-kernel total milliseconds go to ms_out[0..count) in the
  * order gq_kernel_name(ctx, i) reports.  Returns the number of kernels per step. */

@@ -32,7 +32,7 @@ EXPORTS = (
     "gq_profile_steps", "gq_kernel_name", "gq_launches_per_step", "gq_input_dim",
     "gq_recover", "gq_kkt_residual", "gq_nbjm_solve", "gq_slab_enable", "gq_slab_start",
     "gq_slab_phase", "gq_slab_pack", "gq_slab_unpack", "gq_slab_scalar_ptr", "gq_slab_status",
-    "gq_build_offset", "gq_touch_pages",
+    "gq_build_offset", "gq_touch_pages", "gq_host_alloc", "gq_host_free",
 )
 
 
@@ -104,6 +104,8 @@ def load():
                            + [ctypes.POINTER(ctypes.c_int32)] * 3),
         "gq_build_offset": (ctypes.c_int, [i32, i32, i32, i32, i32, dp, dp, dp, dp, dp, vp]),
         "gq_touch_pages": (None, [vp, i64]),
+        "gq_host_alloc": (ctypes.c_void_p, [i64]),
+        "gq_host_free": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -589,6 +589,19 @@ static void parallel_copy(double* dst, const double* src, size_t n) {
 // Fault in the pages of a fresh host buffer from several threads (one write per 4 KiB page):
 // the result array of a solve is 211 MB at the headline, and a single thread takes tens of
 // milliseconds to touch it on some hosts -- as long as the whole 20-step solve.
+extern "C" void* gq_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (bytes <= 0 || cudaMallocHost(&p, (size_t)bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+extern "C" void gq_host_free(void* p) {
+  if (p && cudaFreeHost(p) != cudaSuccess) cudaGetLastError();
+}
+
 extern "C" void gq_touch_pages(void* p, int64_t bytes) {
   if (!p || bytes <= 0) return;
   char* base = static_cast<char*>(p);

@@ -18,9 +18,12 @@ drive the GPU operators (one device apply per call); the fast path is this modul
 
 from __future__ import annotations
 
+import atexit
 import ctypes
+import os
 import threading
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -96,6 +99,55 @@ class _Vec:
             import torch
             return torch.empty_like(self.obj)
         return np.empty_like(self.obj)
+
+
+class _PinnedPool:
+    """Page-locked host buffers for result arrays.  A result array is a numpy view of a ctypes
+    array over ``gq_host_alloc`` memory; when the last reference to it (or to any view of it)
+    goes, the buffer comes back here instead of being unlocked -- page-locking 211 MB costs more
+    than a 100-step solve, re-using a locked buffer costs nothing.  At most ``keep`` free buffers
+    per size are held; the rest are released."""
+
+    def __init__(self, keep=2):
+        self.keep = keep
+        self.free = {}
+        self.closed = False
+        atexit.register(self.close)
+
+    def _give(self, nbytes, ptr):
+        lst = self.free.setdefault(nbytes, [])
+        if self.closed or len(lst) >= self.keep:
+            try:
+                _lib.load().gq_host_free(ctypes.c_void_p(ptr))
+            except Exception:      # interpreter shutdown
+                pass
+        else:
+            lst.append(ptr)
+
+    def take(self, n):
+        """A float64 array of n entries in page-locked memory, or None."""
+        if self.closed or os.environ.get("GQ_NO_PINNED_RESULT") == "1":
+            return None
+        nbytes = 8 * int(n)
+        lst = self.free.get(nbytes)
+        ptr = lst.pop() if lst else _lib.load().gq_host_alloc(nbytes)
+        if not ptr:
+            return None
+        buf = (ctypes.c_double * int(n)).from_address(ptr)
+        weakref.finalize(buf, self._give, nbytes, ptr)
+        return np.frombuffer(buf, dtype=np.float64)
+
+    def close(self):
+        self.closed = True
+        for lst in self.free.values():
+            while lst:
+                try:
+                    _lib.load().gq_host_free(ctypes.c_void_p(lst.pop()))
+                except Exception:
+                    pass
+
+
+_pinned = _PinnedPool()
 
 
 def _touch_pages(arr):
@@ -397,11 +449,17 @@ def pcg_solve(schur, preconditioner, rhs, tol=1e-9, max_steps=None, x0=None, poo
     _lib.check(lib.gq_pcg_start(ctx.h, rv.ptr, x0v.ptr if x0v else None, int(use_pc)), "pcg")
     steps = ctypes.c_int64()
     conv = ctypes.c_int32()
-    x = rv.like()
+    # large host results land in page-locked memory (from a pool); failing that, in a fresh
+    # array whose pages are faulted in while the device iterates (ctypes drops the GIL)
+    x = None
+    if not rv.device and 8 * ctx.dim >= (8 << 20):
+        x = _pinned.take(ctx.dim)
+    pinned = x is not None
+    if x is None:
+        x = rv.like()
     if callback is None:
-        # fault in the host result pages while the device iterates (ctypes drops the GIL)
         toucher = None
-        if not rv.device and x.nbytes >= (8 << 20):
+        if not rv.device and not pinned and x.nbytes >= (8 << 20):
             toucher = threading.Thread(target=_touch_pages, args=(x,), daemon=True)
             toucher.start()
         status = lib.gq_pcg_run(ctx.h, float(tol), int(max_steps), ctypes.byref(steps),

@@ -164,3 +164,45 @@ def test_unsupported_state_dimension():
     rc, msg, h = _create_raw(ga)
     assert rc == _lib.GQ_UNSUPPORTED and "n=5" in msg, (rc, msg)
     assert h is None
+
+
+def test_host_results_come_from_a_pinned_pool_without_aliasing():
+    """Large host results live in page-locked memory from a pool: two results that are alive
+    together never share a buffer, a view keeps its buffer out of the pool, and a dropped
+    result's buffer is the next one handed out."""
+    import gc
+
+    from paper_2304_04980_b200 import (GpuNestedJacobiPreconditioner, GpuSchurOperator,
+                                       MaxIterationsExceeded, generators, pcg_solve)
+    from paper_2304_04980_b200.solver import _pinned
+
+    ga = generators.msd_case(48, 40, 300, 0)          # 9.3 MB per vector: above the threshold
+    op = GpuSchurOperator(ga, 2, 2)
+    pc = GpuNestedJacobiPreconditioner(op, 2, 2)
+
+    def solve(steps):
+        try:
+            return pcg_solve(op, pc, ga.offset, tol=1e-300, max_steps=steps)[0]
+        except MaxIterationsExceeded as exc:
+            return exc.iterate
+
+    x3 = solve(3)
+    if _pinned.take(4) is None:
+        pytest.skip("page-locked host memory is not available")
+    keep = x3.copy()
+    x5 = solve(5)
+    assert x3.ctypes.data != x5.ctypes.data
+    assert np.array_equal(x3, keep)                   # the second solve did not touch it
+    addr = x5.ctypes.data
+    view = x5[10:20]
+    vals = view.copy()
+    del x5
+    gc.collect()
+    x4 = solve(4)                                     # x5's buffer is still held by the view
+    assert x4.ctypes.data != addr and np.array_equal(view, vals)
+    addr4 = x4.ctypes.data
+    del x4
+    gc.collect()
+    x6 = solve(6)                                     # ... x4's came back and is re-used
+    assert x6.ctypes.data == addr4
+    assert np.array_equal(solve(3), keep)
