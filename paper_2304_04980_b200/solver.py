@@ -106,21 +106,29 @@ class _PinnedPool:
     array over ``gq_host_alloc`` memory; when the last reference to it (or to any view of it)
     goes, the buffer comes back here instead of being unlocked -- page-locking 211 MB costs more
     than a 100-step solve, re-using a locked buffer costs nothing.  At most ``keep`` free buffers
-    per size are held; the rest are released."""
+    per size are held; the rest are released.  Page-locked memory is a scarce resource: once
+    ``max(limit, 4 buffers)`` bytes are locked (results the caller still holds plus the pool),
+    further results go to ordinary pageable arrays."""
 
-    def __init__(self, keep=2):
+    def __init__(self, keep=2, limit=2 << 30):
         self.keep = keep
+        self.limit = limit
+        self.locked = 0
         self.free = {}
         self.closed = False
         atexit.register(self.close)
 
+    def _release(self, nbytes, ptr):
+        self.locked -= nbytes
+        try:
+            _lib.load().gq_host_free(ctypes.c_void_p(ptr))
+        except Exception:      # interpreter shutdown
+            pass
+
     def _give(self, nbytes, ptr):
         lst = self.free.setdefault(nbytes, [])
         if self.closed or len(lst) >= self.keep:
-            try:
-                _lib.load().gq_host_free(ctypes.c_void_p(ptr))
-            except Exception:      # interpreter shutdown
-                pass
+            self._release(nbytes, ptr)
         else:
             lst.append(ptr)
 
@@ -130,21 +138,24 @@ class _PinnedPool:
             return None
         nbytes = 8 * int(n)
         lst = self.free.get(nbytes)
-        ptr = lst.pop() if lst else _lib.load().gq_host_alloc(nbytes)
-        if not ptr:
-            return None
+        if lst:
+            ptr = lst.pop()
+        else:
+            if self.locked + nbytes > max(self.limit, 4 * nbytes):
+                return None
+            ptr = _lib.load().gq_host_alloc(nbytes)
+            if not ptr:
+                return None
+            self.locked += nbytes
         buf = (ctypes.c_double * int(n)).from_address(ptr)
         weakref.finalize(buf, self._give, nbytes, ptr)
         return np.frombuffer(buf, dtype=np.float64)
 
     def close(self):
         self.closed = True
-        for lst in self.free.values():
+        for nbytes, lst in self.free.items():
             while lst:
-                try:
-                    _lib.load().gq_host_free(ctypes.c_void_p(lst.pop()))
-                except Exception:
-                    pass
+                self._release(nbytes, lst.pop())
 
 
 _pinned = _PinnedPool()
