@@ -668,12 +668,17 @@ __global__ void __launch_bounds__(rs::NT, 2) k_rstep(const __grid_constant__ CUt
       xpts(xq, s, xc);
       const unsigned ra = (rb + yq) ^ ((unsigned)s << 4);
       const double2 rv = lds2u(ra);
-      double2 em = make_double2(0.0, 0.0), ep = em;
-#pragma unroll
-      for (int u = 0; u < 5; ++u) {
-        em = mac(em, Xm[u], xa[u]);
-        ep = mac(ep, Xp[u], xc[u]);
-      }
+      // four short FMA chains per component instead of two long ones
+      double2 em = mv(Xm[0], xa[0]), em2 = mv(Xm[2], xa[2]);
+      double2 ep = mv(Xp[0], xc[0]), ep2 = mv(Xp[2], xc[2]);
+      em = mac(em, Xm[1], xa[1]);
+      ep = mac(ep, Xp[1], xc[1]);
+      em2 = mac(em2, Xm[3], xa[3]);
+      ep2 = mac(ep2, Xp[3], xc[3]);
+      em2 = mac(em2, Xm[4], xa[4]);
+      ep2 = mac(ep2, Xp[4], xc[4]);
+      em = add(em, em2);
+      ep = add(ep, ep2);
       // y = r + (-(Xi_{t-1} x_{t-1}) - Xi_t' x_{t+1})   (the convention of gq_grid.cu)
       sts2u(ra, make_double2(rv.x + ((0.0 - em.x) - ep.x), rv.y + ((0.0 - em.y) - ep.y)));
 #pragma unroll
