@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import gc
 import json
 import os
 import subprocess
@@ -319,6 +320,7 @@ def run_ours(args, ws, rank, local):
         pcg_solve(op, pc, rhs_host, tol=tol, max_steps=max(W, 1))
     except MaxIterationsExceeded:
         pass
+    gc.collect()    # the warm-up's result is gone: its page-locked buffer is back in the pool
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     try:
