@@ -724,6 +724,15 @@ EncodeTiled encoder() {
 
 }  // namespace
 
+// "shared-memory attribute set" flags per kernel and device (one process may drive several
+// GPUs in the in-process stage-slab mode)
+static bool& device_flag(int kernel) {
+  static bool flags[2][64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return flags[kernel][(dev < 0 || dev >= 64) ? 63 : dev];
+}
+
 bool dstep_supported(const Geo& g) {
   return g.n == 2 && g.T >= 1 && g.T1 <= MAXT1 && encoder() != nullptr;
 }
@@ -778,7 +787,7 @@ cudaError_t launch_dstep(const Geo& g, const CUtensorMap& dmap, const CUtensorMa
                          const DstepOps& op, double* y, double* partials, PcgState* st,
                          int dotmode, int sm_count, cudaStream_t s) {
   const size_t smem = (size_t)SMEM0 + 3 * (size_t)g.T1 * 4;
-  static bool attr = false;
+  bool& attr = device_flag(0);   // the attribute is per device
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_dstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          SMEM0 + 3 * MAXT1 * 4);
@@ -823,7 +832,7 @@ cudaError_t launch_rstep(const Geo& g, const CUtensorMap& xmap, const CUtensorMa
                          const CUtensorMap& ymap, const double* x, const double* r,
                          double* y, const double* xi, const double* xit, PcgState* st,
                          int sm_count, cudaStream_t s) {
-  static bool attr = false;
+  bool& attr = device_flag(1);
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_rstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          rs::SMEM);
